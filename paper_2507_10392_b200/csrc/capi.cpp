@@ -1,0 +1,78 @@
+// C-ABI plumbing for libzorse_b200: thread-local error strings, device queries,
+// and the driver entry point used to encode TMA tensor maps.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "zb_internal.h"
+
+namespace zb {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* where) {
+  return set_error(ZB_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int tensor_map_encode(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* gaddr,
+                      const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                      const cuuint32_t* estrides, CUtensorMapInterleave il,
+                      CUtensorMapSwizzle sw, CUtensorMapL2promotion l2,
+                      CUtensorMapFloatOOBfill oob) {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) return set_error(ZB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUresult r = fn(m, dt, rank, gaddr, dims, strides, box, estrides, il, sw, l2, oob);
+  if (r != CUDA_SUCCESS)
+    return set_error(ZB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): dims %llu x %llu box %u x %u",
+                     (int)r, (unsigned long long)dims[0], (unsigned long long)(rank > 1 ? dims[1] : 1),
+                     box[0], rank > 1 ? box[1] : 1);
+  return 0;
+}
+
+}  // namespace zb
+
+extern "C" const char* zb_last_error(void) { return zb::g_err; }
+
+extern "C" int zb_version(void) { return 1; }
+
+extern "C" int zb_device_sync(void) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return zb::set_cuda_error(e, "cudaDeviceSynchronize");
+  return 0;
+}

@@ -1,0 +1,24 @@
+// Internal helpers shared by the libzorse_b200 translation units (host side).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define ZB_ERR_INVALID 1001
+#define ZB_ERR_CUDA 1002
+#define ZB_ERR_NCCL 1003
+#define ZB_ERR_UNSUPPORTED 1004
+
+namespace zb {
+// Record an error message (thread-local) and return `code`.
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(cudaError_t e, const char* where);
+// Number of SMs on the current device (cached per device).
+int num_sms();
+// cuTensorMapEncodeTiled resolved through the runtime's driver entry point.
+int tensor_map_encode(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* gaddr,
+                      const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                      const cuuint32_t* estrides, CUtensorMapInterleave il,
+                      CUtensorMapSwizzle sw, CUtensorMapL2promotion l2,
+                      CUtensorMapFloatOOBfill oob);
+}  // namespace zb

@@ -1,0 +1,147 @@
+"""Torch-tensor front end over the C-ABI kernels (device memory is owned by torch).
+
+Each function validates shapes/dtypes/devices, then calls exactly one
+`zb_*` entry point on the current CUDA stream.  Nothing here computes on the
+CPU: a missing library or a non-CUDA tensor raises.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from ._lib import call
+
+# GEMM epilogues (csrc/gemm_sm100.cu)
+EPI_BF16 = 0
+EPI_BIAS = 1
+EPI_BIAS_GELU = 2
+EPI_BIAS_RESID = 3
+EPI_GELU_BWD = 4
+EPI_F32 = 5
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libzorse_b200 kernels take CUDA tensors only (no CPU fallback)")
+
+
+def gemm(a, b, out, *, a_t=False, b_t=False, epilogue=EPI_BF16, bias=None, resid=None,
+         aux=None, beta=0.0, M=None, N=None, K=None):
+    """out[M,N] = op(a) @ op(b)^T with tcgen05.
+
+    a: [M,K] (a_t=False) or [K,M] (a_t=True);  b: [N,K] (b_t=False) or [K,N] (b_t=True).
+    All 2-D, row-major with unit inner stride; leading dims taken from stride(0).
+    """
+    _need_cuda(a, b, out, bias, resid, aux)
+    if a_t:
+        K_, M_ = a.shape
+    else:
+        M_, K_ = a.shape
+    if b_t:
+        K2, N_ = b.shape
+    else:
+        N_, K2 = b.shape
+    if K_ != K2:
+        raise ValueError(f"gemm: K mismatch {tuple(a.shape)} {tuple(b.shape)}")
+    M = M_ if M is None else M
+    N = N_ if N is None else N
+    K = K_ if K is None else K
+    for t in (a, b, out):
+        if t.stride(-1) != 1:
+            raise ValueError("gemm operands need unit inner stride")
+    call("zb_gemm_bf16", _ptr(a), _ptr(b), _ptr(out), _ptr(bias), _ptr(resid), _ptr(aux),
+         M, N, K, a.stride(0), b.stride(0), out.stride(0),
+         resid.stride(0) if resid is not None else 0,
+         aux.stride(0) if aux is not None else 0,
+         int(a_t), int(b_t), epilogue, float(beta), _stream())
+    return out
+
+
+def layernorm_fwd(x, w, b, y, mean, rstd, eps=1e-5):
+    _need_cuda(x, w, b, y, mean, rstd)
+    rows, d = x.shape
+    call("zb_layernorm_fwd", _ptr(x), _ptr(w), _ptr(b), _ptr(y), _ptr(mean), _ptr(rstd),
+         None, rows, d, float(eps), _stream())
+
+
+def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None):
+    """dx (+)= LN'(dy); dw, db (fp32) += parameter grads.  dx_accum: residual grad to add."""
+    _need_cuda(dy, x, w, mean, rstd, dx, dw, db, dx_accum)
+    rows, d = x.shape
+    call("zb_layernorm_bwd", _ptr(dy), _ptr(x), _ptr(w), _ptr(mean), _ptr(rstd), _ptr(dx),
+         _ptr(dw), _ptr(db), _ptr(dx_accum), rows, d, _stream())
+
+
+def embedding_fwd(tokens, wte, wpe, out, seq_len):
+    _need_cuda(tokens, wte, wpe, out)
+    rows, d = out.shape
+    call("zb_embedding_fwd", _ptr(tokens), _ptr(wte), _ptr(wpe), _ptr(out), rows, d, seq_len,
+         _stream())
+
+
+def embedding_bwd(tokens, dout, dwte, dwpe, seq_len):
+    _need_cuda(tokens, dout, dwte, dwpe)
+    rows, d = dout.shape
+    call("zb_embedding_bwd", _ptr(tokens), _ptr(dout), _ptr(dwte), _ptr(dwpe), rows, d, seq_len,
+         _stream())
+
+
+def xent_fwd_bwd(logits, labels, loss_sum, dlogits, scale):
+    """Per-row softmax cross-entropy: loss_sum (+)= sum_rows CE; dlogits = (p - 1hot) * scale."""
+    _need_cuda(logits, labels, loss_sum, dlogits)
+    rows, V = logits.shape
+    call("zb_xent_fwd_bwd", _ptr(logits), _ptr(labels), _ptr(loss_sum), _ptr(dlogits), rows, V,
+         logits.stride(0), float(scale), _stream())
+
+
+def bias_grad(dy, db, beta=1.0):
+    """db (fp32) = beta*db + column sums of dy [rows, n] (bf16)."""
+    _need_cuda(dy, db)
+    rows, n = dy.shape
+    call("zb_bias_grad", _ptr(dy), _ptr(db), rows, n, dy.stride(0), _stream())
+
+
+def attn_fwd(qkv, out, lse, n_seq, seq_len, n_head, head_dim, scale):
+    _need_cuda(qkv, out, lse)
+    call("zb_attn_fwd", _ptr(qkv), _ptr(out), _ptr(lse), n_seq, seq_len, n_head, head_dim,
+         qkv.stride(0), float(scale), _stream())
+
+
+def attn_bwd(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, seq_len, n_head, head_dim,
+             scale):
+    _need_cuda(qkv, out, dout, lse, dqkv, dq_accum, delta)
+    call("zb_attn_bwd", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), _ptr(dqkv), _ptr(dq_accum),
+         _ptr(delta), n_seq, seq_len, n_head, head_dim, qkv.stride(0), float(scale), _stream())
+
+
+def adamw_shard(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, lr, beta1, beta2, eps,
+                weight_decay, grad_scale, step):
+    _need_cuda(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq)
+    n = master.numel()
+    call("zb_adamw_shard", _ptr(master), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(grad),
+         _ptr(param_bf16), _ptr(sumsq), n, float(lr), float(beta1), float(beta2), float(eps),
+         float(weight_decay), float(grad_scale), int(step), _stream())
+
+
+def cast_f32_bf16(src, dst):
+    _need_cuda(src, dst)
+    call("zb_cast_f32_bf16", _ptr(src), _ptr(dst), src.numel(), _stream())
+
+
+def fill_f32(t, value):
+    _need_cuda(t)
+    call("zb_fill_f32", _ptr(t), float(value), t.numel(), _stream())
+
+
+def add_bf16(a, b, out):
+    _need_cuda(a, b, out)
+    call("zb_add_bf16", _ptr(a), _ptr(b), _ptr(out), a.numel(), _stream())

@@ -1,0 +1,91 @@
+"""tcgen05 GEMM parity vs a torch fp32 reference of the same op (bf16 inputs)."""
+
+import pytest
+import torch
+
+from paper_2507_10392_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand(*shape, scale=1.0):
+    return (torch.randn(*shape, device="cuda") * scale).to(torch.bfloat16)
+
+
+def _gelu(x):
+    return 0.5 * x * (1 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def _gelu_grad(x):
+    k0, k1 = 0.7978845608028654, 0.044715
+    t = torch.tanh(k0 * (x + k1 * x ** 3))
+    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * k0 * (1 + 3 * k1 * x * x)
+
+
+def _close(out, ref, tol=2e-2):
+    err = (out.float() - ref).abs().max().item()
+    scale = ref.abs().max().item() + 1e-6
+    assert err / scale < tol, f"rel max err {err / scale:.3e}"
+
+
+SHAPES = [(128, 128, 64), (256, 256, 128), (384, 768, 768), (200, 136, 72), (1024, 2304, 768),
+          (8192, 50304 // 8, 768), (128, 64, 1024), (130, 300, 96)]
+
+
+@pytest.mark.parametrize("M,N,Kd", SHAPES)
+def test_gemm_tn(cuda, M, N, Kd):
+    torch.manual_seed(0)
+    a = _rand(M, Kd)
+    b = _rand(N, Kd)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(a, b, out)
+    torch.cuda.synchronize()
+    _close(out, a.float() @ b.float().t())
+
+
+@pytest.mark.parametrize("M,N,Kd", SHAPES)
+def test_gemm_dgrad_layout(cuda, M, N, Kd):
+    # out = a @ w where w is stored [K, N] (N contiguous): B operand MN-major
+    torch.manual_seed(1)
+    a = _rand(M, Kd)
+    w = _rand(Kd, N)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(a, w, out, b_t=True)
+    torch.cuda.synchronize()
+    _close(out, a.float() @ w.float())
+
+
+@pytest.mark.parametrize("M,N,Kd", [(128, 128, 64), (768, 2304, 1024), (3072, 768, 2048),
+                                    (200, 136, 72), (64, 192, 4096)])
+def test_gemm_wgrad_layout_f32_accumulate(cuda, M, N, Kd):
+    # dW[M,N] += dY^T @ X with dY [K, M], X [K, N]: both MN-major, fp32 accumulate
+    torch.manual_seed(2)
+    dy = _rand(Kd, M)
+    x = _rand(Kd, N)
+    c = torch.randn(M, N, device="cuda")
+    ref = c + dy.float().t() @ x.float()
+    K.gemm(dy, x, c, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=1.0)
+    torch.cuda.synchronize()
+    _close(c, ref, tol=1e-3)
+
+
+def test_gemm_epilogues(cuda):
+    torch.manual_seed(3)
+    M, N, Kd = 512, 1536, 384
+    a = _rand(M, Kd)
+    b = _rand(N, Kd, scale=0.05)
+    bias = _rand(N)
+    acc = a.float() @ b.float().t()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(a, b, out, epilogue=K.EPI_BIAS, bias=bias)
+    _close(out, acc + bias.float())
+    aux = torch.empty_like(out)
+    K.gemm(a, b, out, epilogue=K.EPI_BIAS_GELU, bias=bias, aux=aux)
+    _close(aux, acc + bias.float())
+    _close(out, _gelu(aux.float()))
+    r = _rand(M, N)
+    K.gemm(a, b, out, epilogue=K.EPI_BIAS_RESID, bias=bias, resid=r)
+    _close(out, acc + bias.float() + r.float())
+    K.gemm(a, b, out, epilogue=K.EPI_GELU_BWD, aux=aux)
+    _close(out, acc * _gelu_grad(aux.float()))
+    torch.cuda.synchronize()
