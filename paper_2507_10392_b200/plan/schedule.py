@@ -1,0 +1,396 @@
+"""Microbatch schedule: the plan's per-iteration task graph and its list order.
+
+Restates the task graph of hetplan ``simulate._Builder.build``
+(simulate.py:256-558) and the deterministic list scheduler of ``simulate_plan``
+(simulate.py:590-649).  The reference uses them to *model* an iteration; here
+they define what the B200 executor *runs*: every rank walks the global event
+order filtered to the events it participates in, which is a valid static
+instruction stream (each pick is the global minimum start, so per-device event
+order respects every dependency).  Task keys, creation order, priorities and
+durations follow the reference exactly so the event sequence is bit-identical
+(pinned by tests/golden/schedule_*.json).
+
+Memory-accounting effects of the simulator (simulate.py:660-696) are not part
+of the execution contract and are not restated.
+"""
+
+from __future__ import annotations
+
+from collections import defaultdict
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from .configure import TrainingPlan
+from .costs import CostContext, Strategy, allgather_time, best_cross_link, reduce_scatter_time
+
+# Tie-break rank of each event kind (simulate.py:47-59).
+KIND_RANK = {
+    "AllGather": 0, "P2PRecv": 1, "LoadAct": 2, "Fwd": 3, "Recompute": 4, "Bwd": 5,
+    "P2PSend": 6, "OffloadAct": 7, "FreeParams": 8, "ReduceScatter": 9, "OptimStep": 10,
+}
+_FORWARD_KEYS = {"F", "OA"}
+
+
+class SimulationError(RuntimeError):
+    """Malformed plan or a wedged task graph."""
+
+
+@dataclass
+class Task:
+    seq: int
+    key: tuple
+    kind: str
+    group: int
+    stage: int
+    microbatch: int
+    layer: int
+    duration: float
+    lanes: Tuple[Tuple[str, str], ...]
+    deps: Tuple[tuple, ...]
+    prio: tuple
+
+
+@dataclass(frozen=True)
+class Event:
+    """One scheduled task (fields of the reference's ScheduledEvent + its key)."""
+
+    key: tuple
+    kind: str
+    group: int
+    stage: int
+    microbatch: int
+    layer: int
+    start: float
+    end: float
+    device_ids: Tuple[str, ...]
+    lane: str
+
+
+class TaskGraph:
+    """Builds the task list for one iteration of ``plan``."""
+
+    def __init__(self, ctx: CostContext, plan: TrainingPlan) -> None:
+        self.ctx, self.plan = ctx, plan
+        self.order = plan.global_order()
+        self.ranges = plan.stage_layer_ranges()
+        self.n = len(self.order)
+        covered = sum(g.layers_assigned for g in plan.groups)
+        if covered != ctx.model.num_layers:
+            raise SimulationError(f"plan covers {covered} layers, model has {ctx.model.num_layers}")
+        self.tasks: List[Task] = []
+        self.by_key: Dict[tuple, Task] = {}
+        self._fwd_stages = {gi: [s for s in range(self.n) if self.order[s][0] == gi]
+                            for gi in range(len(plan.groups))}
+
+    # ------------------------------------------------------------ geometry
+    def group_of(self, s: int) -> int:
+        return self.order[s][0]
+
+    def layers(self, s: int) -> List[int]:
+        lo, hi = self.ranges[s]
+        return list(range(lo, hi))
+
+    def ids(self, gi: int) -> Tuple[str, ...]:
+        return self.plan.groups[gi].device_ids
+
+    def lanes(self, gi: int, lane: str):
+        return tuple((d, lane) for d in self.ids(gi))
+
+    def compute_time(self, s: int, part: str) -> float:
+        """Slowest member's per-microbatch time through the ministage."""
+        group = self.plan.groups[self.group_of(s)]
+        worst = 0.0
+        for dev in group.devices:
+            share = group.shares[dev.id]
+            if share <= 0:
+                continue
+            t = 0.0
+            for layer in self.layers(s):
+                f = self.ctx.runtime.fit_for(dev.kind, self.ctx.model.class_of(layer))
+                t += (f.fwd_alpha + f.fwd_beta * share) if part == "fwd" else \
+                     (f.bwd_alpha + f.bwd_beta * share)
+            worst = max(worst, t)
+        return worst
+
+    def act_unit(self, gi: int, dev_id: str) -> int:
+        ctx = self.ctx
+        return (self.plan.groups[gi].shares[dev_id] * ctx.workload.seq_len
+                * ctx.model.hidden_size * ctx.model.bytes_per_element)
+
+    def act_transfer_time(self, gi: int) -> float:
+        return max(self.act_unit(gi, d) for d in self.ids(gi)) / self.ctx.host_transfer_bw
+
+    def layer_bytes(self, layer: int) -> int:
+        return self.ctx.model.params_of(layer) * self.ctx.model.bytes_per_element
+
+    def ag_time(self, s: int, layer: int) -> float:
+        gi = self.group_of(s)
+        return allgather_time(self.ctx, self.layer_bytes(layer) / len(self.ids(gi)), self.ids(gi))
+
+    def rs_time(self, s: int, layer: int) -> float:
+        gi = self.group_of(s)
+        return reduce_scatter_time(self.ctx, self.layer_bytes(layer), self.ids(gi))
+
+    # ------------------------------------------------------------ emission
+    def add(self, key, kind, stage, microbatch=-1, layer=-1, *, duration, lanes, deps) -> None:
+        if key in self.by_key:
+            raise SimulationError(f"duplicate task key {key}")
+        forward = key[0].endswith("f") or key[0] in _FORWARD_KEYS
+        if kind == "OptimStep" or stage < 0:
+            pos = 2 * self.n
+        else:
+            pos = stage if forward else 2 * self.n - 1 - stage
+        t = Task(seq=len(self.tasks), key=key, kind=kind,
+                 group=self.group_of(stage) if stage >= 0 else -1, stage=stage,
+                 microbatch=microbatch, layer=layer, duration=duration, lanes=tuple(lanes),
+                 deps=tuple(deps), prio=(pos, microbatch, KIND_RANK[kind], layer, len(self.tasks)))
+        self.by_key[key] = t
+        self.tasks.append(t)
+
+    def build(self) -> List[Task]:
+        plan, ctx = self.plan, self.ctx
+        M = plan.n_microbatches
+        offload = plan.strategy.offloads
+        per_mb = plan.strategy.gathers_per_microbatch
+        link: Dict[Tuple[int, str], Tuple[str, str, float]] = {}
+        for b in range(self.n - 1):
+            lo, hi = self.group_of(b), self.group_of(b + 1)
+            if lo != hi:
+                link[(b, "f")] = best_cross_link(ctx, self.ids(lo), self.ids(hi))
+                link[(b, "b")] = best_cross_link(ctx, self.ids(hi), self.ids(lo))
+        boundary_bytes = (plan.microbatch_size * ctx.workload.seq_len * ctx.model.hidden_size
+                          * ctx.model.bytes_per_element)
+        fwd_slots = {gi: [(s, m) for s in st for m in range(M)] for gi, st in self._fwd_stages.items()}
+        bwd_slots = {gi: [(s, m) for s in reversed(st) for m in range(M)]
+                     for gi, st in self._fwd_stages.items()}
+
+        # ---------------- forward: gathers, Fwd, offload, boundary sends ----
+        for s in range(self.n):
+            gi = self.group_of(s)
+            mine = self._fwd_stages[gi]
+            q = mine.index(s)
+            lays = self.layers(s)
+            coll = self.lanes(gi, "collective")
+            if per_mb:
+                for m in range(M):
+                    for i, layer in enumerate(lays):
+                        if i > 0:
+                            deps = [("AGf", s, i - 1, m)]
+                        elif m > 0:
+                            deps = [("F", s, m - 1)]
+                        elif q >= 1:
+                            deps = [("F", mine[q - 1], M - 1)]
+                        else:
+                            deps = []
+                        self.add(("AGf", s, i, m), "AllGather", s, m, layer,
+                                 duration=self.ag_time(s, layer), lanes=coll, deps=deps)
+            else:
+                for i, layer in enumerate(lays):
+                    deps = [("AGf", s, i - 1)] if i > 0 else []
+                    if offload and q >= 2:
+                        deps.append(("FREEf", mine[q - 2]))
+                    self.add(("AGf", s, i), "AllGather", s, -1, layer,
+                             duration=self.ag_time(s, layer), lanes=coll, deps=deps)
+            fwd_t = self.compute_time(s, "fwd")
+            for m in range(M):
+                deps = ([("AGf", s, i, m) for i in range(len(lays))] if per_mb
+                        else [("AGf", s, i) for i in range(len(lays))])
+                if m > 0:
+                    deps.append(("F", s, m - 1))
+                if s > 0:
+                    deps.append(("F", s - 1, m) if self.group_of(s - 1) == gi else ("PRf", s - 1, m))
+                if offload:
+                    p = fwd_slots[gi].index((s, m))
+                    if p >= 2:
+                        deps.append(("OA",) + fwd_slots[gi][p - 2])
+                self.add(("F", s, m), "Fwd", s, m, duration=fwd_t,
+                         lanes=self.lanes(gi, "compute"), deps=deps)
+                if offload:
+                    self.add(("OA", s, m), "OffloadAct", s, m, duration=self.act_transfer_time(gi),
+                             lanes=self.lanes(gi, "host"), deps=[("F", s, m)])
+                if s + 1 < self.n and self.group_of(s + 1) != gi:
+                    src, dst, bw = link[(s, "f")]
+                    self.add(("PSf", s, m), "P2PSend", s, m, duration=boundary_bytes / bw,
+                             lanes=((src, "p2p"),), deps=[("F", s, m)])
+                    self.add(("PRf", s, m), "P2PRecv", s + 1, m, duration=ctx.comm.p2p_latency,
+                             lanes=((dst, "p2p"),), deps=[("PSf", s, m)])
+            if offload:
+                self.add(("FREEf", s), "FreeParams", s, duration=0.0, lanes=(),
+                         deps=[("F", s, M - 1)])
+
+        # ---------------- backward: gathers, reload, recompute, Bwd, RS -----
+        for s in reversed(range(self.n)):
+            gi = self.group_of(s)
+            chunks = list(reversed(self._fwd_stages[gi]))
+            r = chunks.index(s)
+            lays = self.layers(s)
+            coll = self.lanes(gi, "collective")
+            if per_mb:
+                for m in range(M):
+                    for i, layer in enumerate(lays):
+                        if i > 0:
+                            deps = [("AGb", s, i - 1, m)]
+                        else:
+                            deps = [("F", s, M - 1)]
+                            if m > 0:
+                                deps.append(("B", s, m - 1))
+                            elif r >= 1:
+                                deps.append(("B", chunks[r - 1], M - 1))
+                        self.add(("AGb", s, i, m), "AllGather", s, m, layer,
+                                 duration=self.ag_time(s, layer), lanes=coll, deps=deps)
+            else:
+                for i, layer in enumerate(lays):
+                    if i > 0:
+                        deps = [("AGb", s, i - 1)]
+                    elif offload:
+                        deps = [("FREEf", s)]
+                        if r >= 2:
+                            deps.append(("FREEb", chunks[r - 2]))
+                    else:
+                        deps = [("F", s, M - 1)]
+                    self.add(("AGb", s, i), "AllGather", s, -1, layer,
+                             duration=self.ag_time(s, layer), lanes=coll, deps=deps)
+            rc_t = self.compute_time(s, "fwd")
+            bwd_t = self.compute_time(s, "bwd")
+            for m in range(M):
+                if offload:
+                    p = bwd_slots[gi].index((s, m))
+                    deps = [("OA", s, m), ("RC",) + bwd_slots[gi][p - 1] if p >= 1 else ("F", s, M - 1)]
+                    self.add(("LA", s, m), "LoadAct", s, m, duration=self.act_transfer_time(gi),
+                             lanes=self.lanes(gi, "host"), deps=deps)
+                deps = [("F", s, m)]
+                if m > 0:
+                    deps.append(("B", s, m - 1))
+                if offload:
+                    deps.append(("LA", s, m))
+                deps += ([("AGb", s, i, m) for i in range(len(lays))] if per_mb
+                         else [("AGb", s, i) for i in range(len(lays))])
+                if m == 0 and r >= 1:
+                    prev = chunks[r - 1]
+                    deps.append(("RS", prev, len(self.layers(prev)) - 1))
+                self.add(("RC", s, m), "Recompute", s, m, duration=rc_t,
+                         lanes=self.lanes(gi, "compute"), deps=deps)
+                deps = [("RC", s, m)]
+                if s + 1 < self.n:
+                    deps.append(("B", s + 1, m) if self.group_of(s + 1) == gi else ("PRb", s, m))
+                self.add(("B", s, m), "Bwd", s, m, duration=bwd_t,
+                         lanes=self.lanes(gi, "compute"), deps=deps)
+                if s > 0 and self.group_of(s - 1) != gi:
+                    src, dst, bw = link[(s - 1, "b")]
+                    self.add(("PSb", s - 1, m), "P2PSend", s, m, duration=boundary_bytes / bw,
+                             lanes=((src, "p2p"),), deps=[("B", s, m)])
+                    self.add(("PRb", s - 1, m), "P2PRecv", s - 1, m, duration=ctx.comm.p2p_latency,
+                             lanes=((dst, "p2p"),), deps=[("PSb", s - 1, m)])
+            if offload:
+                self.add(("FREEb", s), "FreeParams", s, duration=0.0, lanes=(),
+                         deps=[("B", s, M - 1)])
+            for i, layer in enumerate(lays):
+                deps = [("B", s, M - 1)] + ([("RS", s, i - 1)] if i > 0 else [])
+                self.add(("RS", s, i), "ReduceScatter", s, -1, layer,
+                         duration=self.rs_time(s, layer), lanes=coll, deps=deps)
+
+        # ---------------- per-ministage optimizer -------------------------
+        for s in range(self.n):
+            gi = self.group_of(s)
+            deps = [("RS", s, i) for i in range(len(self.layers(s)))]
+            if not plan.strategy.offloads:
+                for other in self._fwd_stages[gi]:
+                    deps += [("RS", other, i) for i in range(len(self.layers(other)))]
+                deps = sorted(set(deps))
+            local = sum(ctx.model.params_of(layer) for layer in self.layers(s)) / plan.groups[gi].d_dp
+            self.add(("OPT", s), "OptimStep", s, duration=local * ctx.optim_update_per_param,
+                     lanes=self.lanes(gi, "compute"), deps=deps)
+
+        for t in self.tasks:
+            for dep in t.deps:
+                if dep not in self.by_key:
+                    raise SimulationError(f"task {t.key} depends on unknown {dep}")
+        return self.tasks
+
+
+def list_schedule(tasks: Sequence[Task], plan: TrainingPlan) -> List[Event]:
+    """Greedy list scheduling: repeatedly start the ready task with the least
+    (earliest start, priority); a task occupies all its lanes."""
+    waiting = {t.key: len(t.deps) for t in tasks}
+    children: Dict[tuple, List[Task]] = defaultdict(list)
+    for t in tasks:
+        for dep in t.deps:
+            children[dep].append(t)
+    lane_free: Dict[Tuple[str, str], float] = defaultdict(float)
+    earliest = {t.key: 0.0 for t in tasks}
+    ready = [t for t in tasks if not t.deps]
+    out: List[Event] = []
+    while ready:
+        def start_of(t: Task) -> float:
+            s = earliest[t.key]
+            for ln in t.lanes:
+                if lane_free[ln] > s:
+                    s = lane_free[ln]
+            return s
+
+        pick = min(ready, key=lambda t: (start_of(t), t.prio))
+        start = start_of(pick)
+        end = start + pick.duration
+        for ln in pick.lanes:
+            lane_free[ln] = end
+        ready.remove(pick)
+        out.append(Event(key=pick.key, kind=pick.kind, group=pick.group, stage=pick.stage,
+                         microbatch=pick.microbatch, layer=pick.layer, start=start, end=end,
+                         device_ids=tuple(d for d, _ in pick.lanes) or plan.groups[pick.group].device_ids,
+                         lane=pick.lanes[0][1] if pick.lanes else "none"))
+        for child in children[pick.key]:
+            waiting[child.key] -= 1
+            if end > earliest[child.key]:
+                earliest[child.key] = end
+            if waiting[child.key] == 0:
+                ready.append(child)
+    if len(out) != len(tasks):
+        done = {e.key for e in out}
+        stuck = [t.key for t in tasks if t.key not in done][:8]
+        raise SimulationError(f"simulation deadlocked with {len(tasks) - len(out)} tasks blocked; "
+                              f"first stuck: {stuck}")
+    return out
+
+
+@dataclass
+class Schedule:
+    """The iteration's global event order plus derived per-device streams."""
+
+    plan: TrainingPlan
+    events: List[Event]
+
+    @property
+    def iteration_time(self) -> float:
+        return max(e.end for e in self.events)
+
+    def collective_counts(self) -> Dict[int, Dict[str, int]]:
+        counts = {gi: {"allgather": 0, "reduce_scatter": 0} for gi in range(len(self.plan.groups))}
+        for e in self.events:
+            if e.kind == "AllGather":
+                counts[e.group]["allgather"] += 1
+            elif e.kind == "ReduceScatter":
+                counts[e.group]["reduce_scatter"] += 1
+        return counts
+
+    def group_of_device(self, dev_id: str) -> int:
+        for gi, g in enumerate(self.plan.groups):
+            if dev_id in g.device_ids:
+                return gi
+        raise KeyError(dev_id)
+
+    def stream_for(self, dev_id: str) -> List[Event]:
+        """Events device ``dev_id`` executes, in global order.
+
+        Every task is tagged with the group of its stage (simulate.py:236), so
+        P2PSend belongs to the sending group and P2PRecv to the receiving one.
+        On B200 a boundary transfer is many-to-many — every member of the
+        sending group holds part of the microbatch and every member of the
+        receiving group needs part of it — so all members of the group execute
+        the event, not only the single best link the reference charges.
+        """
+        gi = self.group_of_device(dev_id)
+        return [e for e in self.events if e.group == gi]
+
+
+def build_schedule(ctx: CostContext, plan: TrainingPlan) -> Schedule:
+    return Schedule(plan=plan, events=list_schedule(TaskGraph(ctx, plan).build(), plan))
