@@ -1,0 +1,118 @@
+/*
+ * zorse_b200.h — C ABI of libzorse_b200.so, the B200 (sm_100a) executor of the
+ * Zorse training-step hot path.
+ *
+ * The reference (hetplan, arXiv 2507.10392) has no runtime: every hot-path
+ * operation is a MODELLED task in its discrete-event simulator.  Each entry
+ * point below is the real operation behind one of those tasks; the comment on
+ * each names the reference task / formula it replaces (paths relative to
+ * /root/reference/pkg/src/hetplan/).
+ *
+ * Conventions
+ *   - Every function returns 0 on success, a nonzero code otherwise
+ *     (1001 invalid argument, 1002 CUDA error, 1003 NCCL error, 1004
+ *     unsupported shape); zb_last_error() gives a thread-local message.
+ *   - The caller owns all device memory; the library allocates nothing on the
+ *     hot path.  Pointers are device pointers unless stated otherwise.
+ *   - Every kernel is enqueued on the given stream; no call synchronises.
+ *   - bf16 = IEEE bfloat16, fp32 accumulators; matrices are row-major with the
+ *     given leading dimension (elements).
+ *   - There is no CPU fallback: without a B200 these calls fail.
+ */
+#ifndef ZORSE_B200_H
+#define ZORSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* zb_stream_t; /* == cudaStream_t */
+
+/* ---------------------------------------------------------------- status */
+const char* zb_last_error(void);
+int zb_version(void);
+int zb_device_sync(void);
+
+/* ---------------------------------------------------------------- GEMM
+ * C[M,N] = A[M,K] * B[N,K]^T on tcgen05 tensor cores (TMA-fed, TMEM accumulators).
+ * a_mn_major: A stored [K][lda] (M contiguous) instead of [M][lda].
+ * b_mn_major: B stored [K][ldb] (N contiguous) instead of [N][ldb].
+ * epilogue: 0 C=acc | 1 C=acc+bias | 2 aux=acc+bias, C=gelu(aux) | 3 C=acc+bias+R
+ *           4 C=acc*gelu'(aux) | 5 C(fp32)=beta*C+acc
+ * Replaces the modelled per-layer compute of Fwd / Recompute / Bwd tasks
+ * (simulate.py:330-367, 469-505; compute_time simulate.py:177-195). */
+int zb_gemm_bf16(const void* A, const void* B, void* C, const void* bias, const void* R,
+                 void* aux, int M, int N, int K, int lda, int ldb, int ldc, int ldr, int ldaux,
+                 int a_mn_major, int b_mn_major, int epilogue, float beta, zb_stream_t stream);
+
+/* ---------------------------------------------------------------- attention
+ * Causal attention over the fused QKV rows ([q|k|v] per token, pitch ld),
+ * n_seq sequences of S tokens, H heads of dim D (64 or 128).
+ * out [n_seq*S, H*D] bf16; lse [n_seq, H, S] fp32.  Same tasks as above. */
+int zb_attn_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int D, int ld,
+                float scale, zb_stream_t stream);
+/* Writes dQ, dK, dV into the matching columns of dqkv (pitch ld).
+ * delta: fp32 scratch [n_seq, H, S].  dq_accum: reserved (may be NULL). */
+int zb_attn_bwd(const void* qkv, const void* out, const void* dout, const void* lse, void* dqkv,
+                void* dq_accum, void* delta, int n_seq, int S, int H, int D, int ld, float scale,
+                zb_stream_t stream);
+
+/* ---------------------------------------------------------------- elementwise
+ * LayerNorm over rows of length d (d % 8 == 0).  mean/rstd: fp32 [rows]. */
+int zb_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void* mean, void* rstd,
+                     void* reserved, int rows, int d, float eps, zb_stream_t stream);
+/* dx = dres + LN'(dy) (dres may be NULL; dx may alias dres); dw, db (fp32) += grads. */
+int zb_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mean,
+                     const void* rstd, void* dx, void* dw, void* db, const void* dres, int rows,
+                     int d, zb_stream_t stream);
+/* out[t] = wte[tok[t]] + wpe[t % seq]  (tok: int32). */
+int zb_embedding_fwd(const void* tok, const void* wte, const void* wpe, void* out, int rows, int d,
+                     int seq, zb_stream_t stream);
+/* dwte[tok[t]] += dout[t]; dwpe[t % seq] += dout[t]  (fp32 accumulators). */
+int zb_embedding_bwd(const void* tok, const void* dout, void* dwte, void* dwpe, int rows, int d,
+                     int seq, zb_stream_t stream);
+/* Fused softmax cross-entropy: *loss_sum += sum_rows (lse - logit[label]);
+ * dlogits = (softmax - onehot) * scale (may alias logits); label < 0 ignores a row. */
+int zb_xent_fwd_bwd(const void* logits, const void* labels, void* loss_sum, void* dlogits,
+                    int rows, int V, int ld, float scale, zb_stream_t stream);
+/* db[n] (fp32) += sum_rows dy[row, n]. */
+int zb_bias_grad(const void* dy, void* db, int rows, int n, int ld, zb_stream_t stream);
+int zb_cast_f32_bf16(const void* src, void* dst, int64_t n, zb_stream_t stream);
+int zb_fill_f32(void* p, float value, int64_t n, zb_stream_t stream);
+int zb_add_bf16(const void* a, const void* b, void* out, int64_t n, zb_stream_t stream);
+
+/* ---------------------------------------------------------------- optimizer
+ * Fused AdamW on one rank's uneven fp32 shard; writes the bf16 parameter shard.
+ * sumsq (fp32 scalar, may be NULL) += sum (grad*grad_scale)^2.
+ * Replaces the OptimStep task (simulate.py:536-550; optim_update_per_param costs.py:81). */
+int zb_adamw_shard(void* master, void* exp_avg, void* exp_avg_sq, const void* grad,
+                   void* param_bf16, void* sumsq, int64_t n, float lr, float beta1, float beta2,
+                   float eps, float weight_decay, float grad_scale, int step, zb_stream_t stream);
+
+/* ---------------------------------------------------------------- collectives
+ * Communicators are opaque NCCL handles owned by the executor. dtype: 0 bf16, 1 fp32. */
+int zb_nccl_unique_id_size(void);
+int zb_nccl_get_unique_id(void* out /* host, zb_nccl_unique_id_size() bytes */);
+int zb_comm_init(void** comm_out, const void* unique_id /* host */, int nranks, int rank);
+int zb_comm_destroy(void* comm);
+/* Uneven in-place AllGather of a flat buffer: rank r's shard is
+ * buf[displs[r] : displs[r]+counts[r]] (counts/displs: host int64 arrays).
+ * Replaces the AllGather task (simulate.py:292-328, 408-446; costs.py:138-149). */
+int zb_allgather_v(void* comm, void* buf, const int64_t* counts, const int64_t* displs,
+                   int nranks, int dtype, zb_stream_t stream);
+/* Uneven in-place ReduceScatter (sum): afterwards rank r's slice holds the group sum.
+ * Replaces the ReduceScatter task (simulate.py:523-534; costs.py:152-158). */
+int zb_reduce_scatter_v(void* comm, void* buf, const int64_t* counts, const int64_t* displs,
+                        int nranks, int dtype, zb_stream_t stream);
+/* Grouped point-to-point transfers (world ranks); stage-boundary activations and
+ * gradients.  Replaces P2PSend / P2PRecv (simulate.py:378-385, 507-514; costs.py:161-186). */
+int zb_p2p_group(void* comm, int n, const int* peers, void* const* bufs, const int64_t* counts,
+                 const int* is_send, int dtype, zb_stream_t stream);
+int zb_allreduce_sum(void* comm, void* buf, int64_t count, int dtype, zb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZORSE_B200_H */

@@ -36,9 +36,10 @@ SIGNATURES = {
     "zb_nccl_get_unique_id": [P],
     "zb_comm_init": [P, P, I, I],
     "zb_comm_destroy": [P],
-    "zb_allgather_v": [P, P, P, P, P, I, P],
-    "zb_reduce_scatter_v": [P, P, P, P, P, I, P],
-    "zb_p2p_exchange": [P, I, P, P, P, P, P, P, P, I, P],
+    "zb_allgather_v": [P, P, P, P, I, I, P],
+    "zb_reduce_scatter_v": [P, P, P, P, I, I, P],
+    "zb_p2p_group": [P, I, P, P, P, P, I, P],
+    "zb_allreduce_sum": [P, P, I64, I, P],
     "zb_version": [],
     "zb_device_sync": [],
 }

@@ -1,0 +1,112 @@
+// Fused AdamW over one rank's uneven fp32 shard (master, exp_avg, exp_avg_sq)
+// with the reduce-scattered gradient shard as input; writes the updated bf16
+// parameter shard in the same pass (that slice of the layer's flat bf16 buffer
+// is what the next AllGather-v broadcasts).  Replaces the reference's modelled
+// OptimStep task (hetplan simulate.py:536-550; 1e-10 s/param, costs.py:81).
+//
+// HBM traffic per element: read master/m/v/grad (16 B) + write master/m/v (12 B)
+// + bf16 param (2 B) = 30 B.  float4 vectorised, grid-stride, plus an optional
+// per-shard sum of squared gradients reduced with warp shuffles (for logging;
+// the interleaved per-ministage optimizer cannot clip by a global norm).
+// Update rule follows torch.optim.AdamW (decoupled weight decay, bias-corrected).
+#include "common.cuh"
+#include "zb_internal.h"
+
+namespace zb {
+
+struct AdamParams {
+  float lr, beta1, beta2, eps, wd, grad_scale;
+  float step_size;      // lr / (1 - beta1^t)
+  float inv_bc2_sqrt;   // 1 / sqrt(1 - beta2^t)
+  float decay;          // 1 - lr * wd
+};
+
+ZB_DEVICE void adam_elem(float& p, float& m, float& v, float g, const AdamParams& a) {
+  p *= a.decay;
+  m = m + (g - m) * (1.f - a.beta1);
+  v = v * a.beta2 + (1.f - a.beta2) * g * g;
+  const float denom = sqrtf(v) * a.inv_bc2_sqrt + a.eps;
+  p = p - a.step_size * (m / denom);
+}
+
+__global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master,
+                                                    float* __restrict__ exp_avg,
+                                                    float* __restrict__ exp_avg_sq,
+                                                    const float* __restrict__ grad,
+                                                    __nv_bfloat16* __restrict__ param,
+                                                    float* __restrict__ sumsq, int64_t n,
+                                                    AdamParams a) {
+  float ss = 0.f;
+  const int64_t n4 = n >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 p = reinterpret_cast<float4*>(master)[i];
+    float4 m = reinterpret_cast<float4*>(exp_avg)[i];
+    float4 v = reinterpret_cast<float4*>(exp_avg_sq)[i];
+    float4 g = reinterpret_cast<const float4*>(grad)[i];
+    g.x *= a.grad_scale; g.y *= a.grad_scale; g.z *= a.grad_scale; g.w *= a.grad_scale;
+    ss += g.x * g.x + g.y * g.y + g.z * g.z + g.w * g.w;
+    adam_elem(p.x, m.x, v.x, g.x, a);
+    adam_elem(p.y, m.y, v.y, g.y, a);
+    adam_elem(p.z, m.z, v.z, g.z, a);
+    adam_elem(p.w, m.w, v.w, g.w, a);
+    reinterpret_cast<float4*>(master)[i] = p;
+    reinterpret_cast<float4*>(exp_avg)[i] = m;
+    reinterpret_cast<float4*>(exp_avg_sq)[i] = v;
+    uint2 o;
+    o.x = pack_bf16(p.x, p.y);
+    o.y = pack_bf16(p.z, p.w);
+    reinterpret_cast<uint2*>(param)[i] = o;
+  }
+  for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    float p = master[i], m = exp_avg[i], v = exp_avg_sq[i], g = grad[i] * a.grad_scale;
+    ss += g * g;
+    adam_elem(p, m, v, g, a);
+    master[i] = p;
+    exp_avg[i] = m;
+    exp_avg_sq[i] = v;
+    param[i] = __float2bfloat16(p);
+  }
+  if (sumsq) {
+    __shared__ float red[8];
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+      t = warp_sum(t);
+      if (threadIdx.x == 0) atomicAdd(sumsq, t);
+    }
+  }
+}
+
+}  // namespace zb
+
+using namespace zb;
+
+extern "C" int zb_adamw_shard(void* master, void* exp_avg, void* exp_avg_sq, const void* grad,
+                              void* param_bf16, void* sumsq, int64_t n, float lr, float beta1,
+                              float beta2, float eps, float weight_decay, float grad_scale,
+                              int step, cudaStream_t s) {
+  if (n <= 0) return 0;
+  if (step < 1) return set_error(ZB_ERR_INVALID, "adamw: step must be >= 1");
+  const uintptr_t al = (uintptr_t)master | (uintptr_t)exp_avg | (uintptr_t)exp_avg_sq |
+                       (uintptr_t)grad;
+  if ((al & 15) || ((uintptr_t)param_bf16 & 7))
+    return set_error(ZB_ERR_INVALID, "adamw: shard buffers must be 16-byte aligned");
+  AdamParams a;
+  a.lr = lr; a.beta1 = beta1; a.beta2 = beta2; a.eps = eps; a.wd = weight_decay;
+  a.grad_scale = grad_scale;
+  const double bc1 = 1.0 - pow((double)beta1, step), bc2 = 1.0 - pow((double)beta2, step);
+  a.step_size = (float)(lr / bc1);
+  a.inv_bc2_sqrt = (float)(1.0 / sqrt(bc2));
+  a.decay = 1.f - lr * weight_decay;
+  int64_t want = (n / 4 + 255) / 256;
+  int64_t cap = (int64_t)num_sms() * 8;
+  int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
+  adamw_kernel<<<grid, 256, 0, s>>>((float*)master, (float*)exp_avg, (float*)exp_avg_sq,
+                                    (const float*)grad, (__nv_bfloat16*)param_bf16, (float*)sumsq,
+                                    n, a);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "adamw");
+}

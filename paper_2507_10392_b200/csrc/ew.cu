@@ -1,0 +1,425 @@
+// HBM-bound elementwise / reduction kernels of the transformer step:
+// LayerNorm fwd/bwd, token+position embedding fwd/bwd, fused softmax
+// cross-entropy (loss + dlogits in one pass over the logits), bias gradients,
+// casts. All vectorised 16-byte accesses, warp-shuffle reductions, fp32 math.
+#include "common.cuh"
+#include "zb_internal.h"
+
+namespace zb {
+
+// ------------------------------------------------------------------ LayerNorm
+// One warp per row; the row (<= 20 KB) stays in L1 between the passes.
+__global__ void layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                     const __nv_bfloat16* __restrict__ w,
+                                     const __nv_bfloat16* __restrict__ b,
+                                     __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                                     float* __restrict__ rstd_out, int rows, int d, float eps) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * d);
+  const int nv = d >> 3;
+  float s = 0.f;
+  for (int v = lane; v < nv; v += 32) {
+    uint4 q = xr[v];
+    float2 a = unpack_bf16(q.x), c = unpack_bf16(q.y), e = unpack_bf16(q.z), f = unpack_bf16(q.w);
+    s += a.x + a.y + c.x + c.y + e.x + e.y + f.x + f.y;
+  }
+  const float mean = warp_sum(s) / d;
+  float ss = 0.f;
+  for (int v = lane; v < nv; v += 32) {
+    uint4 q = xr[v];
+    float2 p[4] = {unpack_bf16(q.x), unpack_bf16(q.y), unpack_bf16(q.z), unpack_bf16(q.w)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float a0 = p[k].x - mean, a1 = p[k].y - mean;
+      ss += a0 * a0 + a1 * a1;
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(ss) / d + eps);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  const uint4* br = reinterpret_cast<const uint4*>(b);
+  uint4* yr = reinterpret_cast<uint4*>(y + (size_t)row * d);
+  for (int v = lane; v < nv; v += 32) {
+    uint4 q = xr[v], qw = wr[v], qb = br[v];
+    uint32_t* qi = &q.x;
+    uint32_t* wi = &qw.x;
+    uint32_t* bi = &qb.x;
+    uint4 o;
+    uint32_t* oi = &o.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 xv = unpack_bf16(qi[k]), wv = unpack_bf16(wi[k]), bv = unpack_bf16(bi[k]);
+      oi[k] = pack_bf16((xv.x - mean) * rstd * wv.x + bv.x, (xv.y - mean) * rstd * wv.y + bv.y);
+    }
+    yr[v] = o;
+  }
+  if (lane == 0) {
+    mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+// dx = dres + rstd * (g - mean(g) - xhat * mean(g * xhat)),  g = dy * w
+// dw += sum_rows dy * xhat,  db += sum_rows dy   (block partials in smem, then
+// one fp32 atomic per column per block).
+__global__ void layernorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                     const __nv_bfloat16* __restrict__ x,
+                                     const __nv_bfloat16* __restrict__ w,
+                                     const float* __restrict__ mean_in,
+                                     const float* __restrict__ rstd_in, __nv_bfloat16* dx,
+                                     float* __restrict__ dw, float* __restrict__ db,
+                                     const __nv_bfloat16* dres, int rows, int d) {
+  extern __shared__ float sh[];  // [2*d]: dw partial, db partial
+  float* sdw = sh;
+  float* sdb = sh + d;
+  for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) sh[i] = 0.f;
+  __syncthreads();
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nv = d >> 3;
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + (size_t)row * d);
+    const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * d);
+    const float mean = mean_in[row], rstd = rstd_in[row];
+    float sg = 0.f, sgx = 0.f;
+    for (int v = lane; v < nv; v += 32) {
+      uint4 qd = dyr[v], qx = xr[v], qw = wr[v];
+      uint32_t *di = &qd.x, *xi = &qx.x, *wi = &qw.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
+        float g0 = dv.x * wv.x, g1 = dv.y * wv.y;
+        float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
+        sg += g0 + g1;
+        sgx += g0 * h0 + g1 * h1;
+        const int c = v * 8 + 2 * k;
+        atomicAdd(&sdw[c], dv.x * h0);
+        atomicAdd(&sdw[c + 1], dv.y * h1);
+        atomicAdd(&sdb[c], dv.x);
+        atomicAdd(&sdb[c + 1], dv.y);
+      }
+    }
+    const float mg = warp_sum(sg) / d, mgx = warp_sum(sgx) / d;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + (size_t)row * d);
+    const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + (size_t)row * d) : nullptr;
+    for (int v = lane; v < nv; v += 32) {
+      uint4 qd = dyr[v], qx = xr[v], qw = wr[v];
+      uint4 qr = rr ? rr[v] : make_uint4(0, 0, 0, 0);
+      uint32_t *di = &qd.x, *xi = &qx.x, *wi = &qw.x, *ri = &qr.x;
+      uint4 o;
+      uint32_t* oi = &o.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
+        float2 rv = rr ? unpack_bf16(ri[k]) : make_float2(0.f, 0.f);
+        float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
+        float o0 = rstd * (dv.x * wv.x - mg - h0 * mgx) + rv.x;
+        float o1 = rstd * (dv.y * wv.y - mg - h1 * mgx) + rv.y;
+        oi[k] = pack_bf16(o0, o1);
+      }
+      dxr[v] = o;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    atomicAdd(&dw[i], sdw[i]);
+    atomicAdd(&db[i], sdb[i]);
+  }
+}
+
+// ------------------------------------------------------------------ embedding
+__global__ void embedding_fwd_kernel(const int* __restrict__ tok,
+                                     const __nv_bfloat16* __restrict__ wte,
+                                     const __nv_bfloat16* __restrict__ wpe,
+                                     __nv_bfloat16* __restrict__ out, int rows, int d, int seq) {
+  const int nv = d >> 3;
+  const size_t total = (size_t)rows * nv;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i / nv), v = (int)(i % nv);
+    const uint4 a = reinterpret_cast<const uint4*>(wte + (size_t)tok[row] * d)[v];
+    const uint4 p = reinterpret_cast<const uint4*>(wpe + (size_t)(row % seq) * d)[v];
+    const uint32_t *ai = &a.x, *pi = &p.x;
+    uint4 o;
+    uint32_t* oi = &o.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 x = unpack_bf16(ai[k]), y = unpack_bf16(pi[k]);
+      oi[k] = pack_bf16(x.x + y.x, x.y + y.y);
+    }
+    reinterpret_cast<uint4*>(out + (size_t)row * d)[v] = o;
+  }
+}
+
+__global__ void embedding_bwd_kernel(const int* __restrict__ tok,
+                                     const __nv_bfloat16* __restrict__ dout,
+                                     float* __restrict__ dwte, float* __restrict__ dwpe, int rows,
+                                     int d, int seq) {
+  const int nv = d >> 3;
+  const size_t total = (size_t)rows * nv;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i / nv), v = (int)(i % nv);
+    const uint4 g = reinterpret_cast<const uint4*>(dout + (size_t)row * d)[v];
+    const uint32_t* gi = &g.x;
+    float* te = dwte + (size_t)tok[row] * d + v * 8;
+    float* pe = dwpe + (size_t)(row % seq) * d + v * 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 x = unpack_bf16(gi[k]);
+      atomicAdd(te + 2 * k, x.x);
+      atomicAdd(te + 2 * k + 1, x.y);
+      atomicAdd(pe + 2 * k, x.x);
+      atomicAdd(pe + 2 * k + 1, x.y);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ cross-entropy
+// One CTA per row: online (max, sum-exp) pass, then dlogits = (softmax - onehot)*scale
+// written in place (bf16).  loss_sum += (lse - logit[label]).  label < 0: ignored row.
+constexpr int XENT_THREADS = 512;
+__global__ void __launch_bounds__(XENT_THREADS) xent_kernel(const __nv_bfloat16* logits,
+                                                          const int* __restrict__ labels,
+                                                          float* __restrict__ loss_sum,
+                                                          __nv_bfloat16* dlogits, int V, int ld,
+                                                          float scale) {
+  const int row = blockIdx.x;
+  const __nv_bfloat16* lr = logits + (size_t)row * ld;
+  __nv_bfloat16* gr = dlogits + (size_t)row * ld;
+  const int label = labels[row];
+  const int nv = V >> 3;  // V % 8 == 0 enforced on the host
+  float m = -INFINITY, s = 0.f;
+  for (int v = threadIdx.x; v < nv; v += XENT_THREADS) {
+    uint4 q = reinterpret_cast<const uint4*>(lr)[v];
+    const uint32_t* qi = &q.x;
+    float vals[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = unpack_bf16(qi[k]);
+      vals[2 * k] = f.x;
+      vals[2 * k + 1] = f.y;
+    }
+    float lm = vals[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) lm = fmaxf(lm, vals[k]);
+    const float nm = fmaxf(m, lm);
+    float acc = s * __expf(m - nm);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += __expf(vals[k] - nm);
+    m = nm;
+    s = acc;
+  }
+  // block-reduce (m, s)
+  __shared__ float sm[XENT_THREADS / 32], ssum[XENT_THREADS / 32];
+  __shared__ float s_lse;
+  {
+    const float wm = warp_max(m);
+    float ws = (m == -INFINITY) ? 0.f : s * __expf(m - wm);
+    ws = warp_sum(ws);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+      sm[w] = wm;
+      ssum[w] = ws;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int nw = XENT_THREADS / 32;
+      float a = threadIdx.x < nw ? sm[threadIdx.x] : -INFINITY;
+      float bm = warp_max(a);
+      float bsum = (threadIdx.x < nw && a != -INFINITY) ? ssum[threadIdx.x] * __expf(a - bm) : 0.f;
+      bsum = warp_sum(bsum);
+      if (threadIdx.x == 0) s_lse = bm + __logf(bsum);
+    }
+    __syncthreads();
+  }
+  const float lse = s_lse;
+  if (threadIdx.x == 0 && label >= 0)
+    atomicAdd(loss_sum, lse - __bfloat162float(lr[label]));
+  const float sc = label >= 0 ? scale : 0.f;
+  for (int v = threadIdx.x; v < nv; v += XENT_THREADS) {
+    uint4 q = reinterpret_cast<const uint4*>(lr)[v];
+    const uint32_t* qi = &q.x;
+    uint4 o;
+    uint32_t* oi = &o.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = unpack_bf16(qi[k]);
+      const int c = v * 8 + 2 * k;
+      float p0 = __expf(f.x - lse) - (c == label ? 1.f : 0.f);
+      float p1 = __expf(f.y - lse) - (c + 1 == label ? 1.f : 0.f);
+      oi[k] = pack_bf16(p0 * sc, p1 * sc);
+    }
+    reinterpret_cast<uint4*>(gr)[v] = o;
+  }
+}
+
+// ------------------------------------------------------------------ bias grad
+// db[n] += sum_r dy[r, n].  Block: 32 column-vectors (256 columns) x 8 row lanes.
+__global__ void bias_grad_kernel(const __nv_bfloat16* __restrict__ dy, float* __restrict__ db,
+                                 int rows, int n, int ld, int rows_per_block) {
+  const int cv = blockIdx.x * 32 + (threadIdx.x & 31);  // column vector (8 cols)
+  const int rl = threadIdx.x >> 5;                       // 0..7
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const bool ok = cv * 8 < n;
+  if (ok) {
+    for (int r = r0 + rl; r < r1; r += 8) {
+      uint4 q = *reinterpret_cast<const uint4*>(dy + (size_t)r * ld + cv * 8);
+      const uint32_t* qi = &q.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 f = unpack_bf16(qi[k]);
+        acc[2 * k] += f.x;
+        acc[2 * k + 1] += f.y;
+      }
+    }
+  }
+  __shared__ float red[8][32][9];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[rl][threadIdx.x & 31][k] = acc[k];
+  __syncthreads();
+  if (rl == 0 && ok) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t += red[j][threadIdx.x & 31][k];
+      atomicAdd(&db[cv * 8 + k], t);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ small ops
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ d,
+                                     int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = __float2bfloat16(s[i]);
+}
+__global__ void fill_f32_kernel(float* __restrict__ p, float v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void add_bf16_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b,
+                                __nv_bfloat16* o, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = __float2bfloat16(__bfloat162float(a[i]) + __bfloat162float(b[i]));
+}
+
+static int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 16;
+  return (int)(g < cap ? (g > 0 ? g : 1) : cap);
+}
+
+static int launched(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, what);
+}
+
+}  // namespace zb
+
+using namespace zb;
+
+extern "C" int zb_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void* mean,
+                                void* rstd, void* /*reserved*/, int rows, int d, float eps,
+                                cudaStream_t s) {
+  if (d % 8) return set_error(ZB_ERR_INVALID, "layernorm: d must be a multiple of 8");
+  if (rows <= 0) return 0;
+  const int threads = 256, per = threads / 32;
+  layernorm_fwd_kernel<<<(rows + per - 1) / per, threads, 0, s>>>(
+      (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, (const __nv_bfloat16*)b,
+      (__nv_bfloat16*)y, (float*)mean, (float*)rstd, rows, d, eps);
+  return launched("layernorm_fwd");
+}
+
+extern "C" int zb_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mean,
+                                const void* rstd, void* dx, void* dw, void* db, const void* dres,
+                                int rows, int d, cudaStream_t s) {
+  if (d % 8) return set_error(ZB_ERR_INVALID, "layernorm: d must be a multiple of 8");
+  if (rows <= 0) return 0;
+  const int threads = 256, per = threads / 32;
+  int blocks = (rows + per * 4 - 1) / (per * 4);
+  if (blocks > 2 * num_sms()) blocks = 2 * num_sms();
+  size_t smem = 2 * (size_t)d * sizeof(float);
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(layernorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  }
+  layernorm_bwd_kernel<<<blocks, threads, smem, s>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w,
+      (const float*)mean, (const float*)rstd, (__nv_bfloat16*)dx, (float*)dw, (float*)db,
+      (const __nv_bfloat16*)dres, rows, d);
+  return launched("layernorm_bwd");
+}
+
+extern "C" int zb_embedding_fwd(const void* tok, const void* wte, const void* wpe, void* out,
+                                int rows, int d, int seq, cudaStream_t s) {
+  if (d % 8) return set_error(ZB_ERR_INVALID, "embedding: d must be a multiple of 8");
+  if (rows <= 0) return 0;
+  int64_t n = (int64_t)rows * (d / 8);
+  embedding_fwd_kernel<<<grid_for(n, 256), 256, 0, s>>>(
+      (const int*)tok, (const __nv_bfloat16*)wte, (const __nv_bfloat16*)wpe, (__nv_bfloat16*)out,
+      rows, d, seq);
+  return launched("embedding_fwd");
+}
+
+extern "C" int zb_embedding_bwd(const void* tok, const void* dout, void* dwte, void* dwpe,
+                                int rows, int d, int seq, cudaStream_t s) {
+  if (d % 8) return set_error(ZB_ERR_INVALID, "embedding: d must be a multiple of 8");
+  if (rows <= 0) return 0;
+  int64_t n = (int64_t)rows * (d / 8);
+  embedding_bwd_kernel<<<grid_for(n, 256), 256, 0, s>>>(
+      (const int*)tok, (const __nv_bfloat16*)dout, (float*)dwte, (float*)dwpe, rows, d, seq);
+  return launched("embedding_bwd");
+}
+
+extern "C" int zb_xent_fwd_bwd(const void* logits, const void* labels, void* loss_sum,
+                               void* dlogits, int rows, int V, int ld, float scale,
+                               cudaStream_t s) {
+  if (V % 8 || ld % 8) return set_error(ZB_ERR_INVALID, "xent: V and ld must be multiples of 8");
+  if (rows <= 0) return 0;
+  xent_kernel<<<rows, XENT_THREADS, 0, s>>>((const __nv_bfloat16*)logits, (const int*)labels,
+                                            (float*)loss_sum, (__nv_bfloat16*)dlogits, V, ld,
+                                            scale);
+  return launched("xent");
+}
+
+extern "C" int zb_bias_grad(const void* dy, void* db, int rows, int n, int ld, cudaStream_t s) {
+  if (n % 8 || ld % 8) return set_error(ZB_ERR_INVALID, "bias_grad: n, ld must be multiples of 8");
+  if (rows <= 0) return 0;
+  const int cblocks = (n / 8 + 31) / 32;
+  int rblocks = (2 * num_sms() + cblocks - 1) / cblocks;
+  int rpb = (rows + rblocks - 1) / rblocks;
+  rpb = ((rpb + 7) / 8) * 8;
+  rblocks = (rows + rpb - 1) / rpb;
+  bias_grad_kernel<<<dim3(cblocks, rblocks), 256, 0, s>>>((const __nv_bfloat16*)dy, (float*)db,
+                                                          rows, n, ld, rpb);
+  return launched("bias_grad");
+}
+
+extern "C" int zb_cast_f32_bf16(const void* src, void* dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return 0;
+  cast_f32_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>((const float*)src, (__nv_bfloat16*)dst, n);
+  return launched("cast_f32_bf16");
+}
+
+extern "C" int zb_fill_f32(void* p, float v, int64_t n, cudaStream_t s) {
+  if (n <= 0) return 0;
+  fill_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>((float*)p, v, n);
+  return launched("fill_f32");
+}
+
+extern "C" int zb_add_bf16(const void* a, const void* b, void* o, int64_t n, cudaStream_t s) {
+  if (n <= 0) return 0;
+  add_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>((const __nv_bfloat16*)a,
+                                                   (const __nv_bfloat16*)b, (__nv_bfloat16*)o, n);
+  return launched("add_bf16");
+}

@@ -1,0 +1,406 @@
+"""Per-rank executor of a hetplan ``TrainingPlan`` on B200.
+
+Each rank (one process per GPU) walks the global event order of the plan's
+schedule (``plan.schedule``; the reference's simulate.py task graph) filtered
+to its DP group, and turns every modelled task into real work:
+
+  AllGather      -> uneven in-place AllGather-v of the layer's bf16 flat buffer
+  Fwd            -> embedding (first stage) + transformer blocks + LM head,
+                    loss and dlogits (last stage); stores layer-boundary
+                    checkpoints for every microbatch
+  P2PSend/Recv   -> many-to-many reshuffle of boundary activations / grads
+                    between asymmetric groups, following the plan's routing
+  Recompute      -> block forwards again, keeping the internals for Bwd
+  Bwd            -> block backwards; fp32 weight grads accumulate per layer
+  ReduceScatter  -> uneven in-place ReduceScatter-v (sum) of the fp32 grads
+  OptimStep      -> fused AdamW on this rank's shard of the ministage's layers
+                    (interleaved optimizer: right after that ministage's RS)
+  OffloadAct / LoadAct / FreeParams -> no-ops: activations and gathered
+                    parameters stay resident in 180 GB of HBM
+
+Every rank of every group issues its communication in one global order, so
+the NCCL calls can never form the cyclic wait the paper had to work around
+with Gloo.
+
+Samples: microbatch m covers global samples [m*mbs, (m+1)*mbs); inside a group
+they are dealt contiguously to devices in ``routing[group][m]`` order
+(configure.py:414-430), so a boundary transfer is the set of interval
+intersections between the sending and the receiving group's sample ranges.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+
+from ..plan.configure import TrainingPlan
+from ..plan.costs import CostContext
+from ..plan.emulated import ModelConfig
+from ..plan.schedule import Event, build_schedule
+from ..plan.shard import ShardSpec, split_flat
+from .model import (FlatLayout, GptOps, alloc_acts, alloc_bwd_scratch, embed_layout,
+                    head_layout, init_flat, layer_layout)
+
+
+@dataclass
+class AdamConfig:
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.95
+    eps: float = 1e-8
+    weight_decay: float = 0.1
+
+
+class ParamUnit:
+    """One flat parameter buffer (a layer, the embedding or the head) on one rank.
+
+    full  : bf16 [P]  gathered parameters (this rank's shard lives in place at [lo, hi))
+    grad  : fp32 [P]  gradient accumulator; after RS-v its [lo, hi) slice is the shard sum
+    master, exp_avg, exp_avg_sq : fp32 [hi - lo]  optimizer state of the shard
+    """
+
+    def __init__(self, name: str, layout: FlatLayout, spec: ShardSpec, pos: int, init_full,
+                 device):
+        self.name, self.layout, self.spec, self.pos = name, layout, spec, pos
+        self.lo, self.hi = spec.bounds[pos]
+        n = self.hi - self.lo
+        self.master = init_full[self.lo:self.hi].to(device=device, dtype=torch.float32).clone()
+        self.exp_avg = torch.zeros(n, device=device, dtype=torch.float32)
+        self.exp_avg_sq = torch.zeros(n, device=device, dtype=torch.float32)
+        self.full = torch.full((layout.numel,), float("nan"), device=device, dtype=torch.bfloat16)
+        self.full[self.lo:self.hi] = self.master.to(torch.bfloat16)
+        self.grad = torch.zeros(layout.numel, device=device, dtype=torch.float32)
+        self.p = layout.views(self.full)
+        self.g = layout.views(self.grad)
+        self.counts = spec.counts
+        self.displs = spec.displs
+
+    @property
+    def shard_numel(self) -> int:
+        return self.hi - self.lo
+
+
+class StageExecutor:
+    """Runs one rank's part of every training step of ``plan``."""
+
+    def __init__(self, plan: TrainingPlan, ctx: CostContext, cfg: ModelConfig, dev_id: str,
+                 rank_of: Dict[str, int], world_comm, group_comm, ops, device,
+                 seed: int = 1234, adam: AdamConfig = AdamConfig(), init_device="cpu"):
+        if plan.routing is None:
+            raise ValueError("plan has no routing; attach it (configure.attach_routing) first")
+        if ctx.model.num_layers != cfg.n_layer:
+            raise ValueError("model spec and model config disagree on the layer count")
+        self.plan, self.ctx, self.cfg, self.dev_id = plan, ctx, cfg, dev_id
+        self.rank_of = rank_of
+        self.world, self.group_comm, self.ops, self.device = world_comm, group_comm, ops, device
+        self.adam = adam
+        self.model = GptOps(cfg, ops)
+        self.schedule = build_schedule(ctx, plan)
+        self.events: List[Event] = self.schedule.stream_for(dev_id)
+        self.order = plan.global_order()
+        self.ranges = plan.stage_layer_ranges()
+        self.n_stages = len(self.order)
+        self.gi = self.schedule.group_of_device(dev_id)
+        self.group = plan.groups[self.gi]
+        self.pos = self.group.device_ids.index(dev_id)
+        self.share = self.group.shares[dev_id]
+        S = cfg.seq_len
+        self.n_tok = self.share * S
+        self.mbs = plan.microbatch_size
+        self.M = plan.n_microbatches
+        self.global_tokens = ctx.workload.global_batch * S
+        self.my_stages = [s for s in range(self.n_stages) if self.order[s][0] == self.gi]
+        self.has_embed = self.order[0][0] == self.gi
+        self.has_head = self.order[-1][0] == self.gi
+        self.step_count = 0
+        self.capture_grads = False   # tests: keep each reduced grad shard before Adam
+        self.captured: Dict[object, torch.Tensor] = {}
+
+        # ---------------- parameters (uneven ZeRO-3 shards) ----------------
+        shares = [self.group.shares[d] for d in self.group.device_ids]
+        self.units: Dict[object, ParamUnit] = {}
+        lay = layer_layout(cfg)
+        if lay.numel != ctx.model.params_of(0):
+            raise ValueError(f"layer layout has {lay.numel} params, planner spec says "
+                             f"{ctx.model.params_of(0)}")
+        for s in self.my_stages:
+            for layer in range(*self.ranges[s]):
+                full = init_flat(lay, "layer", layer, cfg, seed, device=init_device)
+                self.units[layer] = ParamUnit(f"layer{layer}", lay, split_flat(lay.numel, shares),
+                                              self.pos, full, device)
+        if self.has_embed:
+            el = embed_layout(cfg)
+            self.units["embed"] = ParamUnit("embed", el, split_flat(el.numel, shares), self.pos,
+                                            init_flat(el, "embed", 0, cfg, seed, init_device), device)
+        if self.has_head:
+            hl = head_layout(cfg)
+            self.units["head"] = ParamUnit("head", hl, split_flat(hl.numel, shares), self.pos,
+                                           init_flat(hl, "head", 0, cfg, seed, init_device), device)
+
+        # ---------------- activations ----------------
+        d = cfg.d_model
+        n = max(self.n_tok, 1)
+        bf = dict(device=device, dtype=torch.bfloat16)
+        self.act: Dict[Tuple[int, int], torch.Tensor] = {}
+        self.gbuf: Dict[Tuple[int, int], torch.Tensor] = {}
+        for s in self.my_stages:
+            lo, hi = self.ranges[s]
+            for m in range(self.M):
+                for layer in range(lo, hi + 1):
+                    if (layer, m) not in self.act:
+                        self.act[(layer, m)] = torch.empty(n, d, **bf)
+                for key in ((lo, m), (hi, m)):
+                    if key not in self.gbuf:
+                        self.gbuf[key] = torch.empty(n, d, **bf)
+        max_ms = max(self.ranges[s][1] - self.ranges[s][0] for s in self.my_stages)
+        self.acts = [alloc_acts(cfg, self.n_tok, device) for _ in range(max_ms)]
+        self.fwd_acts = alloc_acts(cfg, self.n_tok, device)
+        self.fwd_out = torch.empty(n, d, **bf)
+        self.bscr = alloc_bwd_scratch(cfg, self.n_tok, device)
+        self.dy_pp = [torch.empty(n, d, **bf), torch.empty(n, d, **bf)]
+        if self.has_head:
+            self.logits = torch.empty(n, cfg.vocab, **bf)
+            self.hf = torch.empty(n, d, **bf)
+            self.hf_mean = torch.empty(n, device=device)
+            self.hf_rstd = torch.empty(n, device=device)
+            self.dhf = torch.empty(n, d, **bf)
+        self.tokens = torch.zeros(self.M, n, device=device, dtype=torch.int32)
+        self.labels = torch.zeros(self.M, n, device=device, dtype=torch.int32)
+        self.loss_sum = torch.zeros(1, device=device, dtype=torch.float32)
+        self.gsumsq = torch.zeros(1, device=device, dtype=torch.float32)
+
+        # ---------------- sample ranges and boundary transfer lists ----------
+        self._sample_ranges = self._compute_sample_ranges()
+        self.transfers = self._compute_transfers()
+
+    # ------------------------------------------------------------ geometry
+    def _compute_sample_ranges(self):
+        """ranges[gi][m][dev] = (lo, hi) sample offsets inside microbatch m."""
+        out = []
+        for gi, g in enumerate(self.plan.groups):
+            per_m = []
+            for m in range(self.M):
+                off, r = 0, {}
+                for dev, cnt in self.plan.routing[gi][m]:
+                    r[dev] = (off, off + cnt)
+                    off += cnt
+                if off != self.mbs:
+                    raise ValueError(f"routing of group {gi} microbatch {m} covers {off} samples")
+                for dev in g.device_ids:
+                    r.setdefault(dev, (0, 0))
+                per_m.append(r)
+            out.append(per_m)
+        return out
+
+    def my_samples(self, m: int) -> Tuple[int, int]:
+        lo, hi = self._sample_ranges[self.gi][m][self.dev_id]
+        return m * self.mbs + lo, m * self.mbs + hi
+
+    def _pairs(self, g_from: int, g_to: int, m: int):
+        """(src dev, dst dev, sample lo, sample hi) intersections for microbatch m."""
+        src, dst = self._sample_ranges[g_from][m], self._sample_ranges[g_to][m]
+        out = []
+        for a in self.plan.groups[g_from].device_ids:
+            alo, ahi = src[a]
+            for b in self.plan.groups[g_to].device_ids:
+                blo, bhi = dst[b]
+                lo, hi = max(alo, blo), min(ahi, bhi)
+                if lo < hi:
+                    out.append((a, b, lo, hi))
+        return out
+
+    def _compute_transfers(self):
+        """Per (direction, boundary s, m): list of (peer rank, row lo, row hi, is_send)
+        where rows index this rank's [n_tok, d] buffer."""
+        S = self.cfg.seq_len
+        me = self.dev_id
+        out = {}
+        for s in range(self.n_stages - 1):
+            ga, gb = self.order[s][0], self.order[s + 1][0]
+            if ga == gb:
+                continue
+            for m in range(self.M):
+                for direction, (g_from, g_to) in (("f", (ga, gb)), ("b", (gb, ga))):
+                    lst = []
+                    for a, b, lo, hi in self._pairs(g_from, g_to, m):
+                        if a == me:
+                            base = self._sample_ranges[g_from][m][me][0]
+                            lst.append((self.rank_of[b], (lo - base) * S, (hi - base) * S, True))
+                        if b == me:
+                            base = self._sample_ranges[g_to][m][me][0]
+                            lst.append((self.rank_of[a], (lo - base) * S, (hi - base) * S, False))
+                    out[(direction, s, m)] = lst
+        return out
+
+    # ------------------------------------------------------------ data
+    def load_batch(self, batch: torch.Tensor) -> int:
+        """Copy this rank's token / label slices of the global batch
+        ([global_batch, S+1] int32, ideally pinned host memory) to the device.
+        Returns the number of bytes copied host->device."""
+        S = self.cfg.seq_len
+        nbytes = 0
+        if self.n_tok == 0 or not (self.has_embed or self.has_head):
+            return 0
+        for m in range(self.M):
+            lo, hi = self.my_samples(m)
+            rows = batch[lo:hi]
+            if self.has_embed:
+                self.tokens[m, :self.n_tok].copy_(rows[:, :S].reshape(-1), non_blocking=True)
+                nbytes += self.n_tok * 4
+            if self.has_head:
+                self.labels[m, :self.n_tok].copy_(rows[:, 1:].reshape(-1), non_blocking=True)
+                nbytes += self.n_tok * 4
+        return nbytes
+
+    # ------------------------------------------------------------ step
+    def step(self) -> None:
+        """One training iteration (data must be loaded).  Enqueues everything on
+        the current stream; does not synchronise."""
+        self.step_count += 1
+        for u in self.units.values():
+            u.grad.zero_()
+        self.loss_sum.zero_()
+        self.gsumsq.zero_()
+        for ev in self.events:
+            handler = _DISPATCH[ev.kind]
+            handler(self, ev)
+
+    # ------------------------------------------------------------ handlers
+    def _extras(self, stage: int, forward: bool, first_index: bool, last_index: bool):
+        out = []
+        if forward:
+            if stage == 0 and self.has_embed and first_index:
+                out.append("embed")
+            if stage == self.n_stages - 1 and self.has_head and first_index:
+                out.append("head")
+        return out
+
+    def _on_allgather(self, ev: Event) -> None:
+        key = ev.key
+        s, i = key[1], key[2]
+        units = [ev.layer] + self._extras(s, key[0] == "AGf", i == 0, False)
+        if self.group_comm is None:
+            return
+        for u in units:
+            pu = self.units[u]
+            self.group_comm.allgather_v(pu.full, pu.counts, pu.displs)
+
+    def _on_reduce_scatter(self, ev: Event) -> None:
+        s, i = ev.key[1], ev.key[2]
+        lo, hi = self.ranges[s]
+        units = [ev.layer]
+        if s == 0 and self.has_embed and i == hi - lo - 1:
+            units.append("embed")
+        if s == self.n_stages - 1 and self.has_head and i == 0:
+            units.append("head")
+        if self.group_comm is None:
+            return
+        for u in units:
+            pu = self.units[u]
+            self.group_comm.reduce_scatter_v(pu.grad, pu.counts, pu.displs)
+
+    def _on_optim(self, ev: Event) -> None:
+        s = ev.key[1]
+        units = list(range(*self.ranges[s]))
+        if s == 0 and self.has_embed:
+            units.append("embed")
+        if s == self.n_stages - 1 and self.has_head:
+            units.append("head")
+        a = self.adam
+        for u in units:
+            pu = self.units[u]
+            if self.capture_grads:
+                self.captured[u] = pu.grad[pu.lo:pu.hi].clone()
+            self.ops.adamw_shard(pu.master, pu.exp_avg, pu.exp_avg_sq, pu.grad[pu.lo:pu.hi],
+                                 pu.full[pu.lo:pu.hi], self.gsumsq, a.lr, a.beta1, a.beta2, a.eps,
+                                 a.weight_decay, 1.0, self.step_count)
+
+    def _on_fwd(self, ev: Event) -> None:
+        s, m = ev.key[1], ev.key[2]
+        if self.n_tok == 0:
+            return
+        lo, hi = self.ranges[s]
+        n = self.n_tok
+        if s == 0:
+            self.model.embed_fwd(self.units["embed"].p, self.tokens[m], self.act[(lo, m)], n)
+        for layer in range(lo, hi):
+            self.model.layer_fwd(self.units[layer].p, self.act[(layer, m)][:n],
+                                 self.act[(layer + 1, m)][:n], self.fwd_acts, n)
+        if s == self.n_stages - 1:
+            hu = self.units["head"]
+            self.model.head_fwd_bwd(hu.p, hu.g, self.act[(hi, m)][:n], self.labels[m],
+                                    self.gbuf[(hi, m)][:n], self.logits, self.hf, self.hf_mean,
+                                    self.hf_rstd, self.dhf, self.loss_sum,
+                                    1.0 / self.global_tokens, n)
+
+    def _on_recompute(self, ev: Event) -> None:
+        s, m = ev.key[1], ev.key[2]
+        if self.n_tok == 0:
+            return
+        lo, hi = self.ranges[s]
+        n = self.n_tok
+        for j, layer in enumerate(range(lo, hi)):
+            self.model.layer_fwd(self.units[layer].p, self.act[(layer, m)][:n], self.fwd_out[:n],
+                                 self.acts[j], n)
+
+    def _on_bwd(self, ev: Event) -> None:
+        s, m = ev.key[1], ev.key[2]
+        if self.n_tok == 0:
+            return
+        lo, hi = self.ranges[s]
+        n = self.n_tok
+        dy = self.gbuf[(hi, m)][:n]
+        for j in reversed(range(hi - lo)):
+            layer = lo + j
+            dx = self.gbuf[(lo, m)][:n] if j == 0 else self.dy_pp[j & 1][:n]
+            u = self.units[layer]
+            self.model.layer_bwd(u.p, u.g, self.act[(layer, m)][:n], dy, dx, self.acts[j],
+                                 self.bscr, n)
+            dy = dx
+        if s == 0:
+            self.model.embed_bwd(self.units["embed"].g, self.tokens[m], self.gbuf[(lo, m)][:n], n)
+
+    def _on_send(self, ev: Event) -> None:
+        kind, b, m = ev.key
+        if kind == "PSf":
+            buf = self.act[(self.ranges[b][1], m)]
+            lst = self.transfers[("f", b, m)]
+        else:  # PSb: gradient of stage b+1's input goes to group of stage b
+            buf = self.gbuf[(self.ranges[b + 1][0], m)]
+            lst = self.transfers[("b", b, m)]
+        self.world.p2p([(peer, buf[lo:hi], True) for peer, lo, hi, snd in lst if snd])
+
+    def _on_recv(self, ev: Event) -> None:
+        kind, b, m = ev.key
+        if kind == "PRf":
+            buf = self.act[(self.ranges[b + 1][0], m)]
+            lst = self.transfers[("f", b, m)]
+        else:  # PRb
+            buf = self.gbuf[(self.ranges[b][1], m)]
+            lst = self.transfers[("b", b, m)]
+        self.world.p2p([(peer, buf[lo:hi], False) for peer, lo, hi, snd in lst if not snd])
+
+    def _noop(self, ev: Event) -> None:
+        return None
+
+    # ------------------------------------------------------------ results
+    def gather_master(self, unit) -> Tuple[int, int, torch.Tensor]:
+        pu = self.units[unit]
+        return pu.lo, pu.hi, pu.master
+
+
+_DISPATCH = {
+    "AllGather": StageExecutor._on_allgather,
+    "ReduceScatter": StageExecutor._on_reduce_scatter,
+    "OptimStep": StageExecutor._on_optim,
+    "Fwd": StageExecutor._on_fwd,
+    "Recompute": StageExecutor._on_recompute,
+    "Bwd": StageExecutor._on_bwd,
+    "P2PSend": StageExecutor._on_send,
+    "P2PRecv": StageExecutor._on_recv,
+    "OffloadAct": StageExecutor._noop,
+    "LoadAct": StageExecutor._noop,
+    "FreeParams": StageExecutor._noop,
+}

@@ -1,0 +1,154 @@
+"""Executor host logic on CPU: plan walking, uneven shards, routing, boundary
+P2P and DP collectives (gloo, world_size 3), against the fp32 oracle.
+
+The arithmetic is the test-only torch twin of the kernels (tests/cpu_ops.py),
+so these tests pin the executor's data movement; the B200 kernels themselves
+are pinned by the gpu-marked tests.
+"""
+
+import os
+import socket
+import sys
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import cpu_ops  # noqa: E402
+
+from oracle import gpt_cpu  # noqa: E402
+from paper_2507_10392_b200 import plan as P  # noqa: E402
+from paper_2507_10392_b200.plan import emulated as E  # noqa: E402
+from paper_2507_10392_b200.runtime.data import synthetic_batch  # noqa: E402
+from paper_2507_10392_b200.runtime.trainer import ZorseTrainer  # noqa: E402
+
+CFG = E.ModelConfig("tiny-test", "gpt", n_layer=4, d_model=64, n_head=2, vocab=512, seq_len=64)
+GB = 8
+
+
+def _setup(nodes, groups, n_mb, counts, strategy):
+    prof = E.profile_from_json(E.profile_json(nodes))
+    rt = P.fit_runtime_model(prof)
+    ctx = P.CostContext(graph=P.build_cluster_graph(prof), runtime=rt, model=CFG.model_spec(),
+                        workload=P.WorkloadSpec(GB, CFG.seq_len))
+    part = P.make_partition(ctx.graph, groups)
+    plan = P.build_plan(ctx, prof, part, n_mb, counts, P.Strategy(strategy),
+                        P.cluster_fingerprint(prof), "transformer")
+    P.attach_routing(plan, rt, "transformer")
+    return plan, ctx
+
+
+def _oracle(steps):
+    batches = [synthetic_batch(CFG.vocab, CFG.seq_len, GB, s) for s in range(1, steps + 1)]
+    params = gpt_cpu.init_params(CFG, 1234)
+    state, losses, grads = {}, [], None
+    for step, b in enumerate(batches, start=1):
+        loss, grads = gpt_cpu.loss_and_grads(CFG, params, b)
+        losses.append(loss)
+        gpt_cpu.adamw(params, grads, state, step)
+    return losses, params, grads
+
+
+def _rel(a, b):
+    return ((a - b).norm() / (b.norm() + 1e-12)).item()
+
+
+def _run_rank(trainer, steps):
+    trainer.exec.capture_grads = True
+    losses = []
+    for s in range(1, steps + 1):
+        losses.append(trainer.step(synthetic_batch(CFG.vocab, CFG.seq_len, GB, s)))
+    ex = trainer.exec
+    return {"losses": losses,
+            "shards": {u: (pu.lo, pu.hi, pu.master.clone(), ex.captured[u].clone())
+                       for u, pu in ex.units.items()}}
+
+
+def _check(results, steps):
+    ref_losses, ref_params, ref_grads = _oracle(steps)
+    for r in results:
+        for got, want in zip(r["losses"], ref_losses):
+            assert abs(got - want) / abs(want) < 1e-2, (got, want)
+    covered = {}
+    for r in results:
+        for u, (lo, hi, master, grad) in r["shards"].items():
+            covered.setdefault(u, []).append((lo, hi))
+            assert _rel(grad, ref_grads[u][lo:hi]) < 3e-2, f"grad {u}[{lo}:{hi}]"
+            assert (master - ref_params[u][lo:hi]).abs().max().item() < 2.5e-3 * steps, f"param {u}"
+    for u, spans in covered.items():  # shards tile every flat buffer exactly once
+        spans.sort()
+        assert spans[0][0] == 0 and all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+        assert spans[-1][1] == ref_params[u].numel()
+
+
+@pytest.mark.parametrize("n_mb,counts,strategy", [(1, [1], "zorse"), (2, [4], "zorse"),
+                                                  (2, [2], "pp-zero3"), (4, [3], "pp-zero2")])
+def test_single_rank_matches_oracle(n_mb, counts, strategy):
+    plan, ctx = _setup([("n0", ["b200"])], [["n0-0"]], n_mb, counts, strategy)
+    tr = ZorseTrainer(plan, ctx, CFG, _ops=cpu_ops)
+    _check([_run_rank(tr, 2)], 2)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, spec, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan, ctx = _setup(*spec)
+        def comms(groups_ranks):
+            world_c = cpu_ops.GlooComm(list(range(world)), rank)
+            group = None
+            for ranks in groups_ranks:  # every rank must create every subgroup
+                c = cpu_ops.GlooComm(ranks, rank)
+                if rank in ranks and len(ranks) > 1:
+                    group = c
+            return world_c, group
+        tr = ZorseTrainer(plan, ctx, CFG, world_rank=rank, world_size=world, _ops=cpu_ops,
+                          _comms=comms)
+        res = _run_rank(tr, 2)
+        # ship plain numpy (tensors in a Queue are shared by fd and die with the worker)
+        res["shards"] = {u: (lo, hi, m.numpy(), g.numpy()) for u, (lo, hi, m, g) in res["shards"].items()}
+        q.put((rank, res))
+    except Exception as exc:  # surface worker failures to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("spec", [
+    # 2 asymmetric stages: [n1-0] (1 rank) then [n0-0, n0-1] (uneven 3:1 shares)
+    ([("n0", ["b200", "b200h"]), ("n1", ["b200"])], [["n0-0", "n0-1"], ["n1-0"]], 2, [1, 1], "zorse"),
+    # interleaved ministages: stages alternate groups (4 global stages)
+    ([("n0", ["b200", "b200h"]), ("n1", ["b200"])], [["n0-0", "n0-1"], ["n1-0"]], 2, [2, 2], "zorse"),
+    # one uneven DP group of 3 (ZeRO-3 per-microbatch gathers)
+    ([("n0", ["b200", "b200", "b200h"])], [["n0-0", "n0-1", "n0-2"]], 2, [2], "pp-zero3"),
+], ids=["2stage", "interleaved", "dp3-zero3"])
+def test_three_ranks_gloo_matches_oracle(spec):
+    world = 3
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    port = _free_port()
+    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, spec, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in range(world):
+        rank, res = q.get(timeout=300)
+        results[rank] = res
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r for r in results.values() if isinstance(r, str)]
+    assert not errs, errs[0]
+    for r in results.values():
+        r["shards"] = {u: (lo, hi, torch.from_numpy(m), torch.from_numpy(g))
+                       for u, (lo, hi, m, g) in r["shards"].items()}
+    _check(list(results.values()), 2)

@@ -45,6 +45,8 @@ def test_gemm_tn(cuda, M, N, Kd):
 
 @pytest.mark.parametrize("M,N,Kd", SHAPES)
 def test_gemm_dgrad_layout(cuda, M, N, Kd):
+    if N % 8:
+        pytest.skip("MN-major B needs a 16-byte row pitch (TMA)")
     # out = a @ w where w is stored [K, N] (N contiguous): B operand MN-major
     torch.manual_seed(1)
     a = _rand(M, Kd)
