@@ -1,0 +1,341 @@
+"""Benchmark: device-timed training tokens/s of the Zorse hot path on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 is launched by the driver with torchrun (one process per GPU).  The
+workload is BASELINE config 2 — GPT-2 small (124M), seq 1024, one pipeline
+stage x an N-rank uneven ZeRO-3 DP group whose per-device batch shares come
+from the planner on an emulated-heterogeneity profile (half b200, half
+half-speed b200h), 8 sequences per GPU on average (weak scaling; at N=8 this
+is exactly config 2: global batch 64, shares 11x4 / 5x4).
+
+ours      : the B200 executor (tcgen05 GEMMs, flash attention, fused AdamW,
+            NCCL AG-v/RS-v) — value = whole-job tokens/s, device-timed,
+            max over ranks; e2e = same metric through ZorseTrainer.step with
+            the batch in pinned host memory and the loss read back each step.
+reference : the reference has no training step (hetplan is a planner +
+            simulator); its CPU path for this metric is the oracle port
+            (oracle/gpt_cpu.py, fp32 torch on all host cores), timed on a
+            bounded sample of the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+def build_workload(n_gpus: int, per_gpu_batch: int = 8):
+    from paper_2507_10392_b200 import plan as P
+    from paper_2507_10392_b200.plan import emulated as E
+
+    cfg = E.GPT2_SMALL
+    prof = E.profile_from_json(E.profile_json(E.dp_group_nodes(n_gpus)))
+    rt = P.fit_runtime_model(prof)
+    gb = per_gpu_batch * n_gpus
+    ctx = P.CostContext(graph=P.build_cluster_graph(prof), runtime=rt, model=cfg.model_spec(),
+                        workload=P.WorkloadSpec(gb, cfg.seq_len))
+    part = P.make_partition(ctx.graph, [[d.id for d in prof.devices]])
+    plan = P.build_plan(ctx, prof, part, 1, [cfg.n_layer], P.Strategy.INTERLEAVED,
+                        P.cluster_fingerprint(prof), "transformer")
+    P.attach_routing(plan, rt, "transformer")
+    return cfg, plan, ctx, gb
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+class TimedOps:
+    """Wraps the kernel module: CUDA events around every GEMM launch (same stream)."""
+
+    def __init__(self, ops):
+        self.ops = ops
+        self.records = []
+
+    def __getattr__(self, name):
+        return getattr(self.ops, name)
+
+    def gemm(self, a, b, out, **kw):
+        a_t, b_t = kw.get("a_t", False), kw.get("b_t", False)
+        M = a.shape[1] if a_t else a.shape[0]
+        K = a.shape[0] if a_t else a.shape[1]
+        N = b.shape[1] if b_t else b.shape[0]
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        r = self.ops.gemm(a, b, out, **kw)
+        e.record()
+        self.records.append((s, e, 2.0 * M * N * K))
+        return r
+
+
+def cpu_reference_sample(cfg, seconds_budget: float = 20.0):
+    """Oracle port (fp32 torch CPU) on a bounded sample: steps of 1 sequence."""
+    from oracle import gpt_cpu
+
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    params = gpt_cpu.init_params(cfg, 1234)
+    state = {}
+    tokens = 0
+    t0 = time.perf_counter()
+    step = 0
+    while True:
+        step += 1
+        batch = gpt_cpu.synthetic_batch(cfg, 1, step)
+        _, grads = gpt_cpu.loss_and_grads(cfg, params, batch)
+        gpt_cpu.adamw(params, grads, state, step)
+        tokens += cfg.seq_len
+        el = time.perf_counter() - t0
+        if el > seconds_budget * 0.5 or step >= 3:
+            break
+    return {"value": tokens / el, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{step} oracle step(s) of 1 x {cfg.seq_len} tokens (fp32 fwd+bwd+AdamW, "
+                      f"{cfg.name}) on {threads} host threads, {el:.1f} s"}
+
+
+def run_reference(args):
+    from paper_2507_10392_b200.plan import emulated as E
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg, plan, ctx, gb = build_workload(args.gpus)
+    base = cpu_reference_sample(cfg, seconds_budget=30.0)
+    v = base["value"]
+    line = {
+        "impl": "reference", "metric": "training tokens/sec (device-timed)", "value": v,
+        "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": gb * cfg.seq_len / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} 1 stage x {args.gpus}-rank uneven ZeRO-3 DP",
+                   "global_batch": gb, "seq_len": cfg.seq_len, "parallelism": f"dp{args.gpus}"},
+        "cpu_baseline": dict(base, value=v),
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    from paper_2507_10392_b200 import kernels
+    from paper_2507_10392_b200.runtime.data import synthetic_batch
+    from paper_2507_10392_b200.runtime.trainer import ZorseTrainer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg, plan, ctx, gb = build_workload(args.gpus)
+    trainer = ZorseTrainer(plan, ctx, cfg, world_rank=rank, world_size=world)
+    ex = trainer.exec
+    batch = synthetic_batch(cfg.vocab, cfg.seq_len, gb, 1, pin=True)
+    h2d = trainer.load(batch)
+    tokens_per_step = gb * cfg.seq_len
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        trainer.run()
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---------------- device-timed region (inputs resident in HBM) ----------------
+    kernels.reset_launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        start.record()
+        for _ in range(args.steps):
+            trainer.run()
+        end.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = kernels.launch_count()
+    ms = start.elapsed_time(end)
+    t = torch.tensor([ms], device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    loss = trainer.loss_device().item()
+
+    # ---------------- e2e through the public API (pinned host batch, loss D2H) ----
+    e2e_steps = max(2, min(args.steps, 5))
+    barrier()
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es.record()
+    for i in range(e2e_steps):
+        trainer.step(batch)          # H2D of this rank's tokens/labels + step + loss D2H
+    ee.record()
+    torch.cuda.synchronize()
+    e2e_ms = es.elapsed_time(ee)
+    t = torch.tensor([e2e_ms], device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = t.item()
+
+    # ---------------- roofline of the dominant kernel (tcgen05 GEMM) ------------
+    timed = TimedOps(kernels)
+    ex.ops = timed
+    ex.model.ops = timed
+    torch.cuda.synchronize()
+    trainer.run()
+    torch.cuda.synchronize()
+    ex.ops = kernels
+    ex.model.ops = kernels
+    g_ms = sum(s.elapsed_time(e) for s, e, _ in timed.records)
+    g_flops = sum(f for _, _, f in timed.records)
+    n_launch = len(timed.records)
+    peaks, src = _peaks()
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    achieved = g_flops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+
+    if rank == 0:
+        step_flops = cfg.flops_per_token() * tokens_per_step
+        line = {
+            "metric": "training tokens/sec (device-timed)",
+            "value": tokens_per_step * args.steps / (ms * 1e-3),
+            "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random init)",
+            "config": {
+                "workload": f"{cfg.name} (L{cfg.n_layer} d{cfg.d_model} s{cfg.seq_len}) 1 stage x "
+                            f"{world}-rank uneven ZeRO-3 DP, planner shares",
+                "model": cfg.name, "global_batch": gb, "seq_len": cfg.seq_len,
+                "parallelism": f"dp{world}", "shares": [plan.groups[0].shares[d]
+                                                         for d in plan.groups[0].device_ids],
+                "n_microbatches": plan.n_microbatches, "ministages": len(plan.groups[0].ministage_sizes),
+                "l2": "per-step working set (params+grads+activations) >> 126 MB L2; no flush",
+            },
+            "loss": loss,
+            "model_tflops_per_gpu": step_flops * args.steps / (ms * 1e-3) / 1e12 / world,
+            "mfu_of_measured_sustained": step_flops * args.steps / (ms * 1e-3) / 1e12 / world / peak,
+            "e2e": {"value": tokens_per_step * e2e_steps / (e2e_ms * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 4 * world},
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "kernel": "zb_gemm_bf16 (tcgen05)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "peak_source": f"{src} bf16_tflops_sustained",
+                         "gemm_share_of_step": g_ms / (ms / args.steps),
+                         "launches_per_step": n_launch,
+                         "algorithmic_flops_per_step": g_flops},
+            "clocks": clocks.summary(),
+        }
+        if world == 1:
+            line["cpu_baseline"] = cpu_reference_sample(cfg)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

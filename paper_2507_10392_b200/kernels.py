@@ -9,7 +9,24 @@ from __future__ import annotations
 
 import torch
 
-from ._lib import call
+from ._lib import call as _call
+
+# Device kernel launches issued per C-ABI entry point (for the bench's gpu_launches).
+_LAUNCHES_PER_CALL = {"zb_attn_bwd": 3}
+_launches = [0]
+
+
+def call(name, *args):
+    _call(name, *args)
+    _launches[0] += _LAUNCHES_PER_CALL.get(name, 1)
+
+
+def reset_launch_count():
+    _launches[0] = 0
+
+
+def launch_count():
+    return _launches[0]
 
 # GEMM epilogues (csrc/gemm_sm100.cu)
 EPI_BF16 = 0

@@ -1,0 +1,43 @@
+"""The C-ABI library loads on a CPU-only host and exports every entry point
+declared in include/zorse_b200.h (no compute calls without a GPU)."""
+
+import ctypes
+import os
+import re
+
+from paper_2507_10392_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    with open(os.path.join(ROOT, "include", "zorse_b200.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(zb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for must in ("zb_gemm_bf16", "zb_attn_fwd", "zb_attn_bwd", "zb_adamw_shard",
+                 "zb_allgather_v", "zb_reduce_scatter_v", "zb_p2p_group", "zb_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_bindings_cover_the_header():
+    assert set(_declared()) <= set(_lib.SIGNATURES) | {"zb_last_error"}
+
+
+def test_error_path_without_gpu():
+    lib = _lib.lib()
+    # invalid shape is rejected before touching the device
+    rc = lib.zb_gemm_bf16(None, None, None, None, None, None, 0, 0, 0, 8, 8, 8, 0, 0, 0, 0, 0,
+                          0.0, None)
+    assert rc == 1001
+    assert b"bad shape" in lib.zb_last_error()
+    assert lib.zb_version() == 1

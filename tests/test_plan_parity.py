@@ -115,3 +115,14 @@ def test_device_streams_partition_the_events():
         assert all(e.group == gi for e in streams[0])
     total = sum(len(sched.stream_for(g.device_ids[0])) for g in plan.groups)
     assert total == len(sched.events)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "plan_training"],
+                         ids=lambda c: c["name"])
+def test_plan_training_bit_exact(case):
+    prof, ctx = _ctx(case)
+    plan, records = P.plan_training(prof, ctx.model, ctx.workload, ctx.runtime,
+                                    strategies=tuple(P.Strategy(s) for s in case["strategies"]),
+                                    k_max=case["k_max"])
+    assert len(records) == case["n_candidates"]
+    assert plan.dumps() == case["plan_json"]
