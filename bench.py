@@ -136,8 +136,9 @@ class TimedOps:
         M = a.shape[1] if a_t else a.shape[0]
         K = a.shape[0] if a_t else a.shape[1]
         N = b.shape[1] if b_t else b.shape[0]
-        s = torch.cuda.Event(enable_timing=True)
-        e = torch.cuda.Event(enable_timing=True)
+        kw_ev = {"external": True} if getattr(self, "external", False) else {}
+        s = torch.cuda.Event(enable_timing=True, **kw_ev)
+        e = torch.cuda.Event(enable_timing=True, **kw_ev)
         s.record()
         r = self.ops.gemm(a, b, out, **kw)
         e.record()
@@ -219,8 +220,11 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
-    for _ in range(args.warmup):
-        trainer.run()
+    for _ in range(max(1, args.warmup - 1)):
+        trainer.run()                 # eager warm-up (JIT-free: warms TMA maps, NCCL, allocs)
+    if not args.eager:
+        trainer.capture()             # whole step -> one CUDA graph
+    trainer.run()
     torch.cuda.synchronize()
     barrier()
 
@@ -266,7 +270,18 @@ def run_ours(args):
     ex.ops = timed
     ex.model.ops = timed
     torch.cuda.synchronize()
-    trainer.run()
+    try:  # time GEMMs inside a replayed graph of the step (no host gaps)
+        timed.external = True
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            ex.step()
+        g2.replay()
+        mode = "graph"
+    except Exception:
+        timed.records.clear()
+        timed.external = False
+        ex.step()
+        mode = "eager"
     torch.cuda.synchronize()
     ex.ops = kernels
     ex.model.ops = kernels
@@ -310,7 +325,7 @@ def run_ours(args):
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "peak_source": f"{src} bf16_tflops_sustained",
                          "gemm_share_of_step": g_ms / (ms / args.steps),
-                         "launches_per_step": n_launch,
+                         "launches_per_step": n_launch, "timing_mode": mode,
                          "algorithmic_flops_per_step": g_flops},
             "clocks": clocks.summary(),
         }
@@ -329,6 +344,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--eager", action="store_true", help="no CUDA-graph capture of the step")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

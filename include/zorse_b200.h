@@ -91,6 +91,14 @@ int zb_adamw_shard(void* master, void* exp_avg, void* exp_avg_sq, const void* gr
                    void* param_bf16, void* sumsq, int64_t n, float lr, float beta1, float beta2,
                    float eps, float weight_decay, float grad_scale, int step, zb_stream_t stream);
 
+/* Same, with the step number t read from device memory (*step_dev, int32) so a
+ * captured CUDA graph replays correct bias corrections; zb_step_increment adds 1. */
+int zb_adamw_shard_dstep(void* master, void* exp_avg, void* exp_avg_sq, const void* grad,
+                         void* param_bf16, void* sumsq, int64_t n, float lr, float beta1,
+                         float beta2, float eps, float weight_decay, float grad_scale,
+                         const void* step_dev, zb_stream_t stream);
+int zb_step_increment(void* step_dev, zb_stream_t stream);
+
 /* ---------------------------------------------------------------- collectives
  * Communicators are opaque NCCL handles owned by the executor. dtype: 0 bf16, 1 fp32. */
 int zb_nccl_unique_id_size(void);

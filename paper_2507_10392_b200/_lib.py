@@ -29,6 +29,8 @@ SIGNATURES = {
     "zb_attn_fwd": [P, P, P, I, I, I, I, I, F, P],
     "zb_attn_bwd": [P, P, P, P, P, P, P, I, I, I, I, I, F, P],
     "zb_adamw_shard": [P, P, P, P, P, P, I64, F, F, F, F, F, F, I, P],
+    "zb_adamw_shard_dstep": [P, P, P, P, P, P, I64, F, F, F, F, F, F, P, P],
+    "zb_step_increment": [P, P],
     "zb_cast_f32_bf16": [P, P, I64, P],
     "zb_fill_f32": [P, F, I64, P],
     "zb_add_bf16": [P, P, P, I64, P],

@@ -19,7 +19,17 @@ struct AdamParams {
   float step_size;      // lr / (1 - beta1^t)
   float inv_bc2_sqrt;   // 1 / sqrt(1 - beta2^t)
   float decay;          // 1 - lr * wd
+  const int* step_dev;  // if set: t is read on the device (CUDA-graph replay)
 };
+
+ZB_DEVICE void resolve_step(AdamParams& a) {
+  if (a.step_dev) {
+    const int t = *a.step_dev;
+    const double bc1 = 1.0 - pow((double)a.beta1, t), bc2 = 1.0 - pow((double)a.beta2, t);
+    a.step_size = (float)(a.lr / bc1);
+    a.inv_bc2_sqrt = (float)(1.0 / sqrt(bc2));
+  }
+}
 
 ZB_DEVICE void adam_elem(float& p, float& m, float& v, float g, const AdamParams& a) {
   p *= a.decay;
@@ -36,6 +46,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master,
                                                     __nv_bfloat16* __restrict__ param,
                                                     float* __restrict__ sumsq, int64_t n,
                                                     AdamParams a) {
+  resolve_step(a);
   float ss = 0.f;
   const int64_t n4 = n >> 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -84,12 +95,15 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master,
 
 using namespace zb;
 
-extern "C" int zb_adamw_shard(void* master, void* exp_avg, void* exp_avg_sq, const void* grad,
-                              void* param_bf16, void* sumsq, int64_t n, float lr, float beta1,
-                              float beta2, float eps, float weight_decay, float grad_scale,
-                              int step, cudaStream_t s) {
+__global__ void step_inc_kernel(int* step) { *step += 1; }
+
+// step <= 0 with step_dev != NULL: the step number is read from device memory.
+static int adamw_impl(void* master, void* exp_avg, void* exp_avg_sq, const void* grad,
+                      void* param_bf16, void* sumsq, int64_t n, float lr, float beta1,
+                      float beta2, float eps, float weight_decay, float grad_scale, int step,
+                      const int* step_dev, cudaStream_t s) {
   if (n <= 0) return 0;
-  if (step < 1) return set_error(ZB_ERR_INVALID, "adamw: step must be >= 1");
+  if (step < 1 && !step_dev) return set_error(ZB_ERR_INVALID, "adamw: step must be >= 1");
   const uintptr_t al = (uintptr_t)master | (uintptr_t)exp_avg | (uintptr_t)exp_avg_sq |
                        (uintptr_t)grad;
   if ((al & 15) || ((uintptr_t)param_bf16 & 7))
@@ -97,6 +111,8 @@ extern "C" int zb_adamw_shard(void* master, void* exp_avg, void* exp_avg_sq, con
   AdamParams a;
   a.lr = lr; a.beta1 = beta1; a.beta2 = beta2; a.eps = eps; a.wd = weight_decay;
   a.grad_scale = grad_scale;
+  a.step_dev = step_dev;
+  if (step < 1) step = 1;
   const double bc1 = 1.0 - pow((double)beta1, step), bc2 = 1.0 - pow((double)beta2, step);
   a.step_size = (float)(lr / bc1);
   a.inv_bc2_sqrt = (float)(1.0 / sqrt(bc2));
@@ -109,4 +125,28 @@ extern "C" int zb_adamw_shard(void* master, void* exp_avg, void* exp_avg_sq, con
                                     n, a);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_cuda_error(e, "adamw");
+}
+
+extern "C" int zb_adamw_shard(void* master, void* exp_avg, void* exp_avg_sq, const void* grad,
+                              void* param_bf16, void* sumsq, int64_t n, float lr, float beta1,
+                              float beta2, float eps, float weight_decay, float grad_scale,
+                              int step, cudaStream_t s) {
+  return adamw_impl(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, n, lr, beta1, beta2,
+                    eps, weight_decay, grad_scale, step, nullptr, s);
+}
+
+extern "C" int zb_adamw_shard_dstep(void* master, void* exp_avg, void* exp_avg_sq,
+                                    const void* grad, void* param_bf16, void* sumsq, int64_t n,
+                                    float lr, float beta1, float beta2, float eps,
+                                    float weight_decay, float grad_scale, const void* step_dev,
+                                    cudaStream_t s) {
+  if (!step_dev) return set_error(ZB_ERR_INVALID, "adamw: step_dev is NULL");
+  return adamw_impl(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, n, lr, beta1, beta2,
+                    eps, weight_decay, grad_scale, 0, (const int*)step_dev, s);
+}
+
+extern "C" int zb_step_increment(void* step_dev, cudaStream_t s) {
+  step_inc_kernel<<<1, 1, 0, s>>>((int*)step_dev);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "step_increment");
 }

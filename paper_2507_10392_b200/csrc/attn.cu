@@ -15,10 +15,13 @@
 namespace zb {
 namespace attn {
 
-constexpr int BM = 64;   // queries per block (4 warps x 16)
-constexpr int BN = 64;   // keys per block
+constexpr int BM = 64;    // queries per q-tile in the backward passes (4 warps x 16)
+constexpr int BN = 64;    // keys per k-tile
 constexpr int NW = 4;
 constexpr int NT = NW * 32;
+constexpr int FW = 8;     // forward / dQ: 8 warps x 16 = 128 queries per CTA
+constexpr int FT = FW * 32;
+constexpr int FBM = FW * 16;
 constexpr float LOG2E = 1.4426950408889634f;
 
 ZB_DEVICE void cp_async16(void* smem, const void* gmem) {
@@ -53,12 +56,12 @@ ZB_DEVICE uint32_t swz(int row, int col) {
   return row * (D * 2) + ((((col >> 3) ^ (row & 7))) << 4) + ((col & 7) << 1);
 }
 
-// Copy a [64][D] tile (rows r0.., columns c0.. of a row-major matrix with pitch ld).
-template <int D>
+// Copy a [ROWS][D] tile (row-major source with pitch ld) with THREADS threads.
+template <int D, int ROWS = 64, int THREADS = NT>
 ZB_DEVICE void load_tile(uint8_t* s, const __nv_bfloat16* g, int ld, int tid) {
   constexpr int CH = D / 8;  // 16-byte chunks per row
 #pragma unroll
-  for (int i = tid; i < 64 * CH; i += NT) {
+  for (int i = tid; i < ROWS * CH; i += THREADS) {
     const int r = i / CH, c = i % CH;
     cp_async16(s + swz<D>(r, c * 8), g + (size_t)r * ld + c * 8);
   }
@@ -90,27 +93,28 @@ ZB_DEVICE void ld_b_kn(const uint8_t* s, int k0, int n0, int lane, uint32_t& b00
 
 // ---------------------------------------------------------------- forward
 template <int D>
-__global__ void __launch_bounds__(NT) fwd_kernel(const __nv_bfloat16* __restrict__ qkv,
+__global__ void __launch_bounds__(FT) fwd_kernel(const __nv_bfloat16* __restrict__ qkv,
                                                 __nv_bfloat16* __restrict__ out,
                                                 float* __restrict__ lse, int S, int H, int ld,
                                                 float scale) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint8_t* sQ = sm;
-  uint8_t* sK = sQ + BM * D * 2;          // [2][BN][D]
+  uint8_t* sK = sQ + FBM * D * 2;         // [2][BN][D]
   uint8_t* sV = sK + 2 * BN * D * 2;      // [2][BN][D]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nqb = S / BM;
+  const int nqb = S / FBM;
   const int qb = nqb - 1 - blockIdx.x;  // heavy (late) query blocks first
   const int h = blockIdx.y, b = blockIdx.z;
   const int HD = H * D;
   const __nv_bfloat16* base = qkv + (size_t)b * S * ld;
-  const __nv_bfloat16* gQ = base + (size_t)qb * BM * ld + h * D;
+  const __nv_bfloat16* gQ = base + (size_t)qb * FBM * ld + h * D;
   const __nv_bfloat16* gK = base + HD + h * D;
   const __nv_bfloat16* gV = base + 2 * HD + h * D;
+  const int last_kb = ((qb + 1) * FBM - 1) / BN;  // last key block touching this query block
 
-  load_tile<D>(sQ, gQ, ld, tid);
-  load_tile<D>(sK, gK, ld, tid);
-  load_tile<D>(sV, gV, ld, tid);
+  load_tile<D, FBM, FT>(sQ, gQ, ld, tid);
+  load_tile<D, BN, FT>(sK, gK, ld, tid);
+  load_tile<D, BN, FT>(sV, gV, ld, tid);
   cp_commit();
 
   float o[D / 8][4];
@@ -119,21 +123,22 @@ __global__ void __launch_bounds__(NT) fwd_kernel(const __nv_bfloat16* __restrict
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   const float sl2 = scale * LOG2E;
   uint32_t qf[D / 16][4];
-  const int qrow0 = qb * BM + warp * 16 + (lane >> 2);  // this thread's rows: qrow0, qrow0+8
+  const int qrow0 = qb * FBM + warp * 16 + (lane >> 2);  // this thread's rows: qrow0, qrow0+8
 
-  for (int kb = 0; kb <= qb; ++kb) {
+  for (int kb = 0; kb <= last_kb; ++kb) {
     cp_wait_all();
     __syncthreads();
     if (kb == 0) {
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) ld_a<D>(sQ, warp * 16, kk * 16, lane, qf[kk]);
     }
-    if (kb + 1 <= qb) {
+    if (kb + 1 <= last_kb) {
       const int nb = (kb + 1) & 1;
-      load_tile<D>(sK + nb * BN * D * 2, gK + (size_t)(kb + 1) * BN * ld, ld, tid);
-      load_tile<D>(sV + nb * BN * D * 2, gV + (size_t)(kb + 1) * BN * ld, ld, tid);
+      load_tile<D, BN, FT>(sK + nb * BN * D * 2, gK + (size_t)(kb + 1) * BN * ld, ld, tid);
+      load_tile<D, BN, FT>(sV + nb * BN * D * 2, gV + (size_t)(kb + 1) * BN * ld, ld, tid);
     }
     cp_commit();
+    if (kb * BN > qb * FBM + warp * 16 + 15) continue;  // every key of this block is masked for this warp
     const uint8_t* cK = sK + (kb & 1) * BN * D * 2;
     const uint8_t* cV = sV + (kb & 1) * BN * D * 2;
     float s[BN / 8][4];
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(NT) fwd_kernel(const __nv_bfloat16* __restrict
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         float v = s[nt][e] * sl2;
-        if (kb == qb) {
+        if ((kb + 1) * BN > qb * FBM) {
           const int key = kb * BN + nt * 8 + 2 * (lane & 3) + (e & 1);
           const int q = qrow0 + (e >> 1) * 8;
           if (key > q) v = -INFINITY;
@@ -510,9 +515,9 @@ static int prep(K kern, size_t smem) {
 template <int D>
 static int run_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int ld,
                    float scale, cudaStream_t s) {
-  const size_t smem = (size_t)(BM + 4 * BN) * D * 2;
+  const size_t smem = (size_t)(FBM + 4 * BN) * D * 2;
   if (int rc = prep(fwd_kernel<D>, smem)) return rc;
-  fwd_kernel<D><<<dim3(S / BM, H, n_seq), NT, smem, s>>>(
+  fwd_kernel<D><<<dim3(S / FBM, H, n_seq), FT, smem, s>>>(
       (const __nv_bfloat16*)qkv, (__nv_bfloat16*)out, (float*)lse, S, H, ld, scale);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_fwd");
@@ -546,7 +551,7 @@ using namespace zb;
 
 extern "C" int zb_attn_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int D,
                            int ld, float scale, cudaStream_t s) {
-  if (S % 64) return set_error(ZB_ERR_INVALID, "attn: seq_len must be a multiple of 64");
+  if (S % 128) return set_error(ZB_ERR_INVALID, "attn: seq_len must be a multiple of 128");
   if (ld % 8) return set_error(ZB_ERR_INVALID, "attn: ld must be a multiple of 8");
   if (n_seq <= 0) return 0;
   if (D == 64) return attn::run_fwd<64>(qkv, out, lse, n_seq, S, H, ld, scale, s);
@@ -558,7 +563,7 @@ extern "C" int zb_attn_fwd(const void* qkv, void* out, void* lse, int n_seq, int
 extern "C" int zb_attn_bwd(const void* qkv, const void* out, const void* dout, const void* lse,
                            void* dqkv, void* /*dq_accum*/, void* delta, int n_seq, int S, int H,
                            int D, int ld, float scale, cudaStream_t s) {
-  if (S % 64) return set_error(ZB_ERR_INVALID, "attn: seq_len must be a multiple of 64");
+  if (S % 128) return set_error(ZB_ERR_INVALID, "attn: seq_len must be a multiple of 128");
   if (n_seq <= 0) return 0;
   if (D == 64) return attn::run_bwd<64>(qkv, out, dout, lse, dqkv, delta, n_seq, S, H, ld, scale, s);
   if (D == 128) return attn::run_bwd<128>(qkv, out, dout, lse, dqkv, delta, n_seq, S, H, ld, scale, s);

@@ -62,16 +62,18 @@ __global__ void layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
 }
 
 // dx = dres + rstd * (g - mean(g) - xhat * mean(g * xhat)),  g = dy * w
-// dw += sum_rows dy * xhat,  db += sum_rows dy   (block partials in smem, then
-// one fp32 atomic per column per block).
-__global__ void layernorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
-                                     const __nv_bfloat16* __restrict__ x,
-                                     const __nv_bfloat16* __restrict__ w,
-                                     const float* __restrict__ mean_in,
-                                     const float* __restrict__ rstd_in, __nv_bfloat16* dx,
-                                     float* __restrict__ dw, float* __restrict__ db,
-                                     const __nv_bfloat16* dres, int rows, int d) {
-  extern __shared__ float sh[];  // [2*d]: dw partial, db partial
+// dw += sum_rows dy * xhat,  db += sum_rows dy.
+// One warp per row; each lane owns the same MAXV 8-wide column vectors for
+// every row it visits, so dw/db partials stay in registers across rows and
+// the row data is read from HBM exactly once.  Per block: one smem reduction,
+// then one fp32 atomic per column.
+template <int MAXV>
+__global__ void __launch_bounds__(256) layernorm_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const __nv_bfloat16* __restrict__ w, const float* __restrict__ mean_in,
+    const float* __restrict__ rstd_in, __nv_bfloat16* dx, float* __restrict__ dw,
+    float* __restrict__ db, const __nv_bfloat16* dres, int rows, int d) {
+  extern __shared__ float sh[];  // [2*d]
   float* sdw = sh;
   float* sdb = sh + d;
   for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) sh[i] = 0.f;
@@ -80,47 +82,73 @@ __global__ void layernorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
   const int lane = threadIdx.x & 31;
   const int nv = d >> 3;
   const uint4* wr = reinterpret_cast<const uint4*>(w);
+  float adw[MAXV][8], adb[MAXV][8];
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) adw[j][k] = adb[j][k] = 0.f;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
     const uint4* dyr = reinterpret_cast<const uint4*>(dy + (size_t)row * d);
     const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * d);
     const float mean = mean_in[row], rstd = rstd_in[row];
+    uint4 qd[MAXV], qx[MAXV];
     float sg = 0.f, sgx = 0.f;
-    for (int v = lane; v < nv; v += 32) {
-      uint4 qd = dyr[v], qx = xr[v], qw = wr[v];
-      uint32_t *di = &qd.x, *xi = &qx.x, *wi = &qw.x;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
-        float g0 = dv.x * wv.x, g1 = dv.y * wv.y;
-        float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
-        sg += g0 + g1;
-        sgx += g0 * h0 + g1 * h1;
-        const int c = v * 8 + 2 * k;
-        atomicAdd(&sdw[c], dv.x * h0);
-        atomicAdd(&sdw[c + 1], dv.y * h1);
-        atomicAdd(&sdb[c], dv.x);
-        atomicAdd(&sdb[c + 1], dv.y);
+    for (int j = 0; j < MAXV; ++j) {
+      const int v = lane + 32 * j;
+      qd[j] = make_uint4(0, 0, 0, 0);
+      qx[j] = make_uint4(0, 0, 0, 0);
+      if (v < nv) {
+        qd[j] = dyr[v];
+        qx[j] = xr[v];
+        const uint4 qw = wr[v];
+        const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
+          const float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
+          const float g0 = dv.x * wv.x, g1 = dv.y * wv.y;
+          adw[j][2 * k] += dv.x * h0;
+          adw[j][2 * k + 1] += dv.y * h1;
+          adb[j][2 * k] += dv.x;
+          adb[j][2 * k + 1] += dv.y;
+          sg += g0 + g1;
+          sgx += g0 * h0 + g1 * h1;
+        }
       }
     }
     const float mg = warp_sum(sg) / d, mgx = warp_sum(sgx) / d;
     uint4* dxr = reinterpret_cast<uint4*>(dx + (size_t)row * d);
     const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + (size_t)row * d) : nullptr;
-    for (int v = lane; v < nv; v += 32) {
-      uint4 qd = dyr[v], qx = xr[v], qw = wr[v];
-      uint4 qr = rr ? rr[v] : make_uint4(0, 0, 0, 0);
-      uint32_t *di = &qd.x, *xi = &qx.x, *wi = &qw.x, *ri = &qr.x;
+#pragma unroll
+    for (int j = 0; j < MAXV; ++j) {
+      const int v = lane + 32 * j;
+      if (v >= nv) continue;
+      const uint4 qw = wr[v];
+      const uint4 qr = rr ? rr[v] : make_uint4(0, 0, 0, 0);
+      const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw.x, *ri = &qr.x;
       uint4 o;
       uint32_t* oi = &o.x;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
         float2 rv = rr ? unpack_bf16(ri[k]) : make_float2(0.f, 0.f);
-        float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
-        float o0 = rstd * (dv.x * wv.x - mg - h0 * mgx) + rv.x;
-        float o1 = rstd * (dv.y * wv.y - mg - h1 * mgx) + rv.y;
+        const float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
+        const float o0 = rstd * (dv.x * wv.x - mg - h0 * mgx) + rv.x;
+        const float o1 = rstd * (dv.y * wv.y - mg - h1 * mgx) + rv.y;
         oi[k] = pack_bf16(o0, o1);
       }
       dxr[v] = o;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    const int v = lane + 32 * j;
+    if (v >= nv) continue;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      atomicAdd(&sdw[v * 8 + k], adw[j][k]);
+      atomicAdd(&sdb[v * 8 + k], adb[j][k]);
     }
   }
   __syncthreads();
@@ -344,19 +372,28 @@ extern "C" int zb_layernorm_bwd(const void* dy, const void* x, const void* w, co
                                 const void* rstd, void* dx, void* dw, void* db, const void* dres,
                                 int rows, int d, cudaStream_t s) {
   if (d % 8) return set_error(ZB_ERR_INVALID, "layernorm: d must be a multiple of 8");
+  if (d > 5120) return set_error(ZB_ERR_UNSUPPORTED, "layernorm_bwd: d > 5120");
   if (rows <= 0) return 0;
   const int threads = 256, per = threads / 32;
-  int blocks = (rows + per * 4 - 1) / (per * 4);
+  int blocks = (rows + per * 8 - 1) / (per * 8);  // >= 8 rows per warp amortises the reduction
   if (blocks > 2 * num_sms()) blocks = 2 * num_sms();
-  size_t smem = 2 * (size_t)d * sizeof(float);
-  if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(layernorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  }
-  layernorm_bwd_kernel<<<blocks, threads, smem, s>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w,
-      (const float*)mean, (const float*)rstd, (__nv_bfloat16*)dx, (float*)dw, (float*)db,
-      (const __nv_bfloat16*)dres, rows, d);
+  const size_t smem = 2 * (size_t)d * sizeof(float);
+  const int vpl = (d / 8 + 31) / 32;  // column vectors per lane
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<blocks, threads, smem, s>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                                       (const __nv_bfloat16*)w, (const float*)mean,
+                                       (const float*)rstd, (__nv_bfloat16*)dx, (float*)dw,
+                                       (float*)db, (const __nv_bfloat16*)dres, rows, d);
+  };
+  if (vpl <= 1) go(layernorm_bwd_kernel<1>);
+  else if (vpl <= 2) go(layernorm_bwd_kernel<2>);
+  else if (vpl <= 3) go(layernorm_bwd_kernel<3>);
+  else if (vpl <= 4) go(layernorm_bwd_kernel<4>);
+  else if (vpl <= 7) go(layernorm_bwd_kernel<7>);
+  else if (vpl <= 10) go(layernorm_bwd_kernel<10>);
+  else if (vpl <= 20) go(layernorm_bwd_kernel<20>);
   return launched("layernorm_bwd");
 }
 

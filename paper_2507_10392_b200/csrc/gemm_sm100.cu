@@ -8,8 +8,11 @@
 // dgrad (B MN-major) and wgrad (A and B MN-major) run through the same pipeline
 // without any transpose pass.
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread),
-// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM -> registers -> global).
+// Roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread),
+// warp 2 = TMEM allocator, warps 4..11 = epilogue (TMEM -> registers -> global;
+// two warps per TMEM lane quarter, each draining half of the tile's columns).
+// Work units are (tile, K-split); with split-K (fp32-accumulate epilogue only)
+// partial tiles are combined with vectorised fp32 reductions (red.global.add.v4).
 // Pipelines: S-stage smem ring (full/empty mbarriers), 2-deep TMEM accumulator
 // ring (tmem_full/tmem_empty) so the epilogue of tile i overlaps the mainloop
 // of tile i+1. Tiles are BM=128 x BN (128|256), BK=64 (one 128-byte swizzle row).
@@ -40,19 +43,22 @@ struct GemmArgs {
   float beta;
   int vec;  // 16-byte vector access legal for C / R / aux rows
   int num_m_tiles, num_n_tiles;
+  int splits;      // K splits (1 unless EPI_F32 with beta == 1)
+  int kb_per_split;
 };
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;
 
 template <int BN>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
-  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 192 ? 5 : 6);
+  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;  // two accumulators, pow2 alloc
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -65,6 +71,18 @@ ZB_DEVICE void epilogue_chunk(const GemmArgs& args, const uint32_t (&r)[32], int
   const bool full = args.vec && (col0 + 32 <= args.N);
   if (EPI == EPI_F32) {
     float* C = reinterpret_cast<float*>(args.C) + (size_t)row * args.ldc + col0;
+    if (args.splits > 1) {  // beta == 1: accumulate partial sums in place
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(C + j), "f"(v[j]),
+                       "f"(v[j + 1]), "f"(v[j + 2]), "f"(v[j + 3])
+                       : "memory");
+      } else {
+        _Pragma("unroll") for (int j = 0; j < 32; ++j) if (col0 + j < args.N) atomicAdd(C + j, v[j]);
+      }
+      return;
+    }
     if (full) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
@@ -85,9 +103,21 @@ ZB_DEVICE void epilogue_chunk(const GemmArgs& args, const uint32_t (&r)[32], int
     return;
   }
   if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID) {
+    if (full) {
+      const uint4* bp = reinterpret_cast<const uint4*>(args.bias + col0);
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (full || col0 + j < args.N) v[j] += __bfloat162float(args.bias[col0 + j]);
+      for (int j = 0; j < 32; j += 8) {
+        const uint4 q = bp[j / 8];
+        float2 f0 = unpack_bf16(q.x), f1 = unpack_bf16(q.y), f2 = unpack_bf16(q.z),
+               f3 = unpack_bf16(q.w);
+        v[j] += f0.x; v[j + 1] += f0.y; v[j + 2] += f1.x; v[j + 3] += f1.y;
+        v[j + 4] += f2.x; v[j + 5] += f2.y; v[j + 6] += f3.x; v[j + 7] += f3.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < args.N) v[j] += __bfloat162float(args.bias[col0 + j]);
+    }
   }
   if (EPI == EPI_BIAS_RESID) {
     const __nv_bfloat16* Rp = args.R + (size_t)row * args.ldr + col0;
@@ -179,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = args.num_m_tiles * args.num_n_tiles;
+  const int num_units = num_tiles * args.splits;
   const int num_kb = (args.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -190,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty_bar[i], kEpiWarps);  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
@@ -205,10 +236,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+        const int tile = unit % num_tiles;
+        const int kb0 = (unit / num_tiles) * args.kb_per_split;
+        const int kb1 = min(num_kb, kb0 + args.kb_per_split);
         const int m0 = (tile % args.num_m_tiles) * BM;
         const int n0 = (tile / args.num_m_tiles) * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           uint8_t* a_dst = smA + stage * Cfg::A_BYTES;
@@ -242,13 +276,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
+        const int kb0 = (unit / num_tiles) * args.kb_per_split;
+        const int kb1 = min(num_kb, kb0 + args.kb_per_split);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smA + stage * Cfg::A_BYTES);
@@ -262,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                    : umma_desc_sw128(a_addr + k * 32, 16, 1024);
             uint64_t b_desc = B_MN ? umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024)
                                    : umma_desc_sw128(b_addr + k * 32, 16, 1024);
-            mma_bf16_ss(d_tmem, a_desc, b_desc, idesc, (kb | k) != 0);
+            mma_bf16_ss(d_tmem, a_desc, b_desc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty_bar[stage]);  // smem slot free once these MMAs retire
           if (++stage == S) {
@@ -275,9 +311,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 4;  // TMEM lane quarter this warp may access
+    const int ew = (warp - 4) & 3;     // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;  // which half of the tile's columns it drains
     int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
+      const int tile = unit % num_tiles;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const int m0 = (tile % args.num_m_tiles) * BM;
@@ -287,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = m0 + ew * 32 + lane;
       const bool row_ok = row < args.M;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
         __syncwarp();
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
@@ -338,8 +376,19 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs ar
   }
   args.num_m_tiles = (args.M + BM - 1) / BM;
   args.num_n_tiles = (args.N + BN - 1) / BN;
-  int tiles = args.num_m_tiles * args.num_n_tiles;
-  int grid = tiles < num_sms() ? tiles : num_sms();
+  const int tiles = args.num_m_tiles * args.num_n_tiles;
+  const int num_kb = (args.K + BK - 1) / BK;
+  int splits = 1;
+  if (EPI == EPI_F32 && args.beta == 1.f && tiles < num_sms()) {
+    // split K so that at least ~2 waves of (tile, split) units exist, >= 8 k-blocks each
+    splits = (2 * num_sms() + tiles - 1) / tiles;
+    int cap = num_kb / 8;
+    if (splits > cap) splits = cap > 1 ? cap : 1;
+  }
+  args.kb_per_split = (num_kb + splits - 1) / splits;
+  args.splits = (num_kb + args.kb_per_split - 1) / args.kb_per_split;
+  const int units = tiles * args.splits;
+  int grid = units < num_sms() ? units : num_sms();
   kern<<<grid, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, args);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
@@ -374,8 +423,26 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
   if (((uintptr_t)A & 15) || ((uintptr_t)B & 15))
     return set_error(ZB_ERR_INVALID, "gemm: A/B must be 16-byte aligned");
   CUtensorMap ta, tb;
-  // BN choice: 256-wide tiles unless N is small.
-  const int BN = (N <= 128) ? 128 : 256;
+  // BN choice: 256-wide tiles unless 128-wide ones fill the SMs in clearly fewer
+  // partial waves (N = 768-class layers) or N is small.
+  int BN = 256;
+  {
+    // cost ~ waves x per-tile time; per-tile time per k-block ~ max(MMA 2*BN cycles,
+    // smem (128+BN)*128 B at ~87% of 128 B/cycle).  Picks 192 for N = 768 / 3072-class layers.
+    const int sms = num_sms(), mt = (M + BM - 1) / BM;
+    double best = 1e30;
+    for (int bn : {256, 192, 128}) {
+      const long long t = (long long)mt * ((N + bn - 1) / bn);
+      const long long waves = (t + sms - 1) / sms;
+      const double per = 2.0 * bn > 1.15 * (128 + bn) ? 2.0 * bn : 1.15 * (128 + bn);
+      const double cost = waves * per;
+      if (cost < best - 1e-9) {
+        best = cost;
+        BN = bn;
+      }
+    }
+    if (N <= 128) BN = 128;
+  }
   int rc;
   if (a_mn_major)
     rc = make_tmap(&ta, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, BK);
@@ -400,6 +467,7 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
     bool v = (ldc % celem) == 0 && ((uintptr_t)C & 15) == 0;
     if (R) v = v && (ldr % 8) == 0 && ((uintptr_t)R & 15) == 0;
     if (aux) v = v && (ldaux % 8) == 0 && ((uintptr_t)aux & 15) == 0;
+    if (bias) v = v && ((uintptr_t)bias & 15) == 0;
     args.vec = v ? 1 : 0;
   }
   const int key = a_mn_major * 2 + b_mn_major;
@@ -408,6 +476,12 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
       case 0: return dispatch_epi<256, 0, 0>(epilogue, ta, tb, args, stream);
       case 1: return dispatch_epi<256, 0, 1>(epilogue, ta, tb, args, stream);
       case 3: return dispatch_epi<256, 1, 1>(epilogue, ta, tb, args, stream);
+    }
+  } else if (BN == 192) {
+    switch (key) {
+      case 0: return dispatch_epi<192, 0, 0>(epilogue, ta, tb, args, stream);
+      case 1: return dispatch_epi<192, 0, 1>(epilogue, ta, tb, args, stream);
+      case 3: return dispatch_epi<192, 1, 1>(epilogue, ta, tb, args, stream);
     }
   } else {
     switch (key) {

@@ -142,8 +142,15 @@ def attn_bwd(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, seq_len, n_head,
 
 def adamw_shard(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, lr, beta1, beta2, eps,
                 weight_decay, grad_scale, step):
+    """step: python int, or an int32 CUDA tensor holding t (read on the device)."""
     _need_cuda(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq)
     n = master.numel()
+    if isinstance(step, torch.Tensor):
+        _need_cuda(step)
+        call("zb_adamw_shard_dstep", _ptr(master), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(grad),
+             _ptr(param_bf16), _ptr(sumsq), n, float(lr), float(beta1), float(beta2), float(eps),
+             float(weight_decay), float(grad_scale), _ptr(step), _stream())
+        return
     call("zb_adamw_shard", _ptr(master), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(grad),
          _ptr(param_bf16), _ptr(sumsq), n, float(lr), float(beta1), float(beta2), float(eps),
          float(weight_decay), float(grad_scale), int(step), _stream())
@@ -162,3 +169,9 @@ def fill_f32(t, value):
 def add_bf16(a, b, out):
     _need_cuda(a, b, out)
     call("zb_add_bf16", _ptr(a), _ptr(b), _ptr(out), a.numel(), _stream())
+
+
+def step_increment(step_dev):
+    """step_dev (int32 CUDA tensor) += 1 on the device."""
+    _need_cuda(step_dev)
+    call("zb_step_increment", _ptr(step_dev), _stream())

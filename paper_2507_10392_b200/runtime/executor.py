@@ -169,6 +169,7 @@ class StageExecutor:
         self.tokens = torch.zeros(self.M, n, device=device, dtype=torch.int32)
         self.labels = torch.zeros(self.M, n, device=device, dtype=torch.int32)
         self.loss_sum = torch.zeros(1, device=device, dtype=torch.float32)
+        self.step_dev = torch.zeros(1, device=device, dtype=torch.int32)  # Adam t on the device
         self.gsumsq = torch.zeros(1, device=device, dtype=torch.float32)
 
         # ---------------- sample ranges and boundary transfer lists ----------
@@ -259,6 +260,7 @@ class StageExecutor:
         """One training iteration (data must be loaded).  Enqueues everything on
         the current stream; does not synchronise."""
         self.step_count += 1
+        self.ops.step_increment(self.step_dev)
         for u in self.units.values():
             u.grad.zero_()
         self.loss_sum.zero_()
@@ -315,7 +317,7 @@ class StageExecutor:
                 self.captured[u] = pu.grad[pu.lo:pu.hi].clone()
             self.ops.adamw_shard(pu.master, pu.exp_avg, pu.exp_avg_sq, pu.grad[pu.lo:pu.hi],
                                  pu.full[pu.lo:pu.hi], self.gsumsq, a.lr, a.beta1, a.beta2, a.eps,
-                                 a.weight_decay, 1.0, self.step_count)
+                                 a.weight_decay, 1.0, self.step_dev)
 
     def _on_fwd(self, ev: Event) -> None:
         s, m = ev.key[1], ev.key[2]
@@ -343,7 +345,7 @@ class StageExecutor:
         n = self.n_tok
         for j, layer in enumerate(range(lo, hi)):
             self.model.layer_fwd(self.units[layer].p, self.act[(layer, m)][:n], self.fwd_out[:n],
-                                 self.acts[j], n)
+                                 self.acts[j], n, need_out=False)
 
     def _on_bwd(self, ev: Event) -> None:
         s, m = ev.key[1], ev.key[2]

@@ -158,8 +158,10 @@ class GptOps:
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
 
     def layer_fwd(self, p: Dict[str, torch.Tensor], x: torch.Tensor, out: torch.Tensor,
-                  a: LayerActs, n_tok: int) -> None:
-        """out = block(x); fills ``a`` (the recompute set)."""
+                  a: LayerActs, n_tok: int, need_out: bool = True) -> None:
+        """out = block(x); fills ``a`` (the recompute set).  ``need_out=False``
+        (activation recompute) skips the fc2 GEMM: backward never reads the
+        block output, only its internals."""
         o, cfg = self.ops, self.cfg
         n_seq = n_tok // cfg.seq_len
         o.layernorm_fwd(x, p["ln1_w"], p["ln1_b"], a.h1[:n_tok], a.mean1[:n_tok], a.rstd1[:n_tok])
@@ -172,8 +174,9 @@ class GptOps:
                         a.rstd2[:n_tok])
         o.gemm(a.h2[:n_tok], p["fc1_w"], a.g[:n_tok], epilogue=EPI_BIAS_GELU, bias=p["fc1_b"],
                aux=a.u[:n_tok])
-        o.gemm(a.g[:n_tok], p["fc2_w"], out, epilogue=EPI_BIAS_RESID, bias=p["fc2_b"],
-               resid=a.x_mid[:n_tok])
+        if need_out:
+            o.gemm(a.g[:n_tok], p["fc2_w"], out, epilogue=EPI_BIAS_RESID, bias=p["fc2_b"],
+                   resid=a.x_mid[:n_tok])
 
     def layer_bwd(self, p: Dict[str, torch.Tensor], gr: Dict[str, torch.Tensor], x: torch.Tensor,
                   dy: torch.Tensor, dx: torch.Tensor, a: LayerActs, s: BwdScratch,

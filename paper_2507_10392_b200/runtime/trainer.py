@@ -58,13 +58,32 @@ class ZorseTrainer:
                                   device, seed=seed, adam=adam, init_device=init_device)
         self.loss_buf = torch.zeros(1, device=device, dtype=torch.float32)
 
+        self.graph = None
+
+    def capture(self) -> None:
+        """Capture one whole training step (every kernel, collective and P2P of
+        this rank) into a CUDA graph; ``run``/``step`` then replay it.  Must be
+        called after at least one eager step (it warms every code path)."""
+        if self.device.type != "cuda":
+            raise RuntimeError("CUDA-graph capture needs the B200 path")
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.exec.step()
+        self.exec.step_count -= 1   # capture recorded the step, it did not run it
+        self.graph = g
+
     def load(self, batch: torch.Tensor) -> int:
         """Host->device copy of this rank's slices of the global batch."""
         return self.exec.load_batch(batch)
 
     def run(self) -> None:
         """Enqueue one training step (no host synchronisation)."""
-        self.exec.step()
+        if self.graph is not None:
+            self.exec.step_count += 1
+            self.graph.replay()
+        else:
+            self.exec.step()
 
     def loss_device(self) -> torch.Tensor:
         """Global mean loss of the last step as a device scalar (all ranks)."""

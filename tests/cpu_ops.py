@@ -123,6 +123,8 @@ def attn_bwd(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, seq_len, n_head,
 
 def adamw_shard(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, lr, beta1, beta2, eps,
                 weight_decay, grad_scale, step):
+    if isinstance(step, torch.Tensor):
+        step = int(step.item())
     g = grad.float() * grad_scale
     if sumsq is not None:
         sumsq += (g * g).sum()
@@ -180,3 +182,7 @@ class GlooComm:
 
     def allreduce_sum(self, buf):
         self.dist.all_reduce(buf, group=self.pg)
+
+
+def step_increment(step_dev):
+    step_dev += 1
