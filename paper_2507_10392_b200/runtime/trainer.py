@@ -59,6 +59,7 @@ class ZorseTrainer:
         self.loss_buf = torch.zeros(1, device=device, dtype=torch.float32)
 
         self.graph = None
+        self.launches_per_step = None   # kernel launches recorded in the captured step
 
     def capture(self) -> None:
         """Capture one whole training step (every kernel, collective and P2P of
@@ -68,8 +69,11 @@ class ZorseTrainer:
             raise RuntimeError("CUDA-graph capture needs the B200 path")
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
+        counter = getattr(self.ops, "launch_count", None)
+        before = counter() if counter else 0
         with torch.cuda.graph(g):
             self.exec.step()
+        self.launches_per_step = (counter() - before) if counter else None
         self.exec.step_count -= 1   # capture recorded the step, it did not run it
         self.graph = g
 

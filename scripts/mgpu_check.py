@@ -1,0 +1,82 @@
+"""Multi-GPU parity run (torchrun, one process per GPU): executes a small GPT
+through the product path (NCCL AG-v/RS-v, many-to-many P2P) for LAYOUT and
+checks every rank's loss, reduced gradient shards and updated master shards
+against the CPU fp32 oracle.  Prints one JSON line per rank; exits 1 on failure.
+
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/mgpu_check.py LAYOUT
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch
+import torch.distributed as dist
+
+from oracle import gpt_cpu
+from paper_2507_10392_b200 import plan as P
+from paper_2507_10392_b200.plan import emulated as E
+from paper_2507_10392_b200.runtime.data import synthetic_batch
+from paper_2507_10392_b200.runtime.trainer import ZorseTrainer
+
+CFG = E.ModelConfig("mgpu-gpt", "gpt", n_layer=4, d_model=256, n_head=4, vocab=2048, seq_len=128)
+LAYOUTS = {
+    # name: (nodes, groups, n_microbatches, ministage counts, strategy, global batch)
+    "dp2": ([("n0", ["b200", "b200h"])], [["n0-0", "n0-1"]], 2, [2], "zorse", 8),
+    "pp2": ([("n0", ["b200"]), ("n1", ["b200h"])], [["n0-0"], ["n1-0"]], 2, [2, 2], "zorse", 8),
+    "pp1+3": ([("n0", ["b200"]), ("n1", ["b200", "b200h", "b200h"])],
+              [["n0-0"], ["n1-0", "n1-1", "n1-2"]], 2, [1, 1], "zorse", 8),
+    "dp4z3": ([("n0", ["b200", "b200", "b200h", "b200h"])], [[f"n0-{i}" for i in range(4)]], 2,
+              [2], "pp-zero3", 12),
+    "pp2x2": ([("n0", ["b200", "b200h"]), ("n1", ["b200", "b200"])],
+              [["n0-0", "n0-1"], ["n1-0", "n1-1"]], 2, [2, 2], "zorse", 8),
+}
+
+
+def main():
+    name = sys.argv[1]
+    nodes, groups, M, counts, strategy, gb = LAYOUTS[name]
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+    prof = E.profile_from_json(E.profile_json(nodes))
+    rt = P.fit_runtime_model(prof)
+    ctx = P.CostContext(graph=P.build_cluster_graph(prof), runtime=rt, model=CFG.model_spec(),
+                        workload=P.WorkloadSpec(gb, CFG.seq_len))
+    plan = P.build_plan(ctx, prof, P.make_partition(ctx.graph, groups), M, counts,
+                        P.Strategy(strategy), P.cluster_fingerprint(prof), "transformer")
+    P.attach_routing(plan, rt, "transformer")
+    tr = ZorseTrainer(plan, ctx, CFG, world_rank=rank, world_size=world)
+    tr.exec.capture_grads = True
+    params = gpt_cpu.init_params(CFG, 1234)
+    state = {}
+    ok = True
+    worst = {"loss": 0.0, "grad": 0.0, "param": 0.0}
+    for step in (1, 2):
+        batch = synthetic_batch(CFG.vocab, CFG.seq_len, gb, step)
+        loss = tr.step(batch.pin_memory())
+        ref_loss, grads = gpt_cpu.loss_and_grads(CFG, params, batch)
+        gpt_cpu.adamw(params, grads, state, step)
+        worst["loss"] = max(worst["loss"], abs(loss - ref_loss) / ref_loss)
+        for u, g in tr.exec.captured.items():
+            pu = tr.exec.units[u]
+            ref = grads[u][pu.lo:pu.hi]
+            rel = ((g.cpu() - ref).norm() / (ref.norm() + 1e-12)).item()
+            worst["grad"] = max(worst["grad"], rel)
+    for u, pu in tr.exec.units.items():
+        err = (pu.master.cpu() - params[u][pu.lo:pu.hi]).abs().max().item()
+        worst["param"] = max(worst["param"], err)
+    ok = worst["loss"] < 1e-2 and worst["grad"] < 3e-2 and worst["param"] < 5e-3
+    print(json.dumps({"layout": name, "rank": rank, "dev": tr.dev_id, "group": tr.exec.gi,
+                      "share": tr.exec.share, "units": len(tr.exec.units), "ok": ok, **worst}),
+          flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
