@@ -53,6 +53,10 @@ int zb_gemm_bf16(const void* A, const void* B, void* C, const void* bias, const 
  * out [n_seq*S, H*D] bf16; lse [n_seq, H, S] fp32.  Same tasks as above. */
 int zb_attn_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int D, int ld,
                 float scale, zb_stream_t stream);
+/* Same contract on 5th-gen tensor cores: S and O accumulate in TMEM, K/V streamed
+ * by TMA, one softmax thread per query row.  S % 128 == 0. */
+int zb_attn_fwd_tc(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int D, int ld,
+                   float scale, zb_stream_t stream);
 /* Writes dQ, dK, dV into the matching columns of dqkv (pitch ld).
  * delta: fp32 scratch [n_seq, H, S].  dq_accum: reserved (may be NULL). */
 int zb_attn_bwd(const void* qkv, const void* out, const void* dout, const void* lse, void* dqkv,

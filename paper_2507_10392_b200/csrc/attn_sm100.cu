@@ -1,0 +1,307 @@
+// Causal flash attention on 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// Forward, one CTA per (128-query tile, head, sequence):
+//   warp 0      TMA producer: Q once, then K/V tiles of 128 keys into a 2-stage ring
+//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into a double-buffered TMEM
+//               S tile, O += P_j V_j into a TMEM O accumulator (P from smem)
+//   warp 2      TMEM allocator
+//   warps 4..7  softmax: thread r owns query row r — reads its whole S row from
+//               TMEM (no cross-thread reductions), online max/sum, writes the bf16
+//               P row into a swizzled smem tile, rescales its O row in TMEM
+//               (tcgen05.ld/st) only when its running max moved, then the
+//               normalised O row + lse to global.
+// The MMA warp issues S_{j+1} before waiting for P_j, so the tensor core computes
+// the next scores while the softmax warps work.
+//
+// Layout as in attn.cu: qkv rows [q|k|v] (pitch ld), sequence b = rows [b*S, (b+1)*S).
+#include "common.cuh"
+#include "zb_internal.h"
+
+namespace zb {
+namespace fa {
+
+constexpr int BQ = 128;   // queries per CTA (= TMEM lanes = softmax threads)
+constexpr int BKV = 128;  // keys per block
+constexpr int NST = 2;    // K/V pipeline stages
+constexpr int kThreads = 256;
+constexpr float LOG2E = 1.4426950408889634f;
+
+template <int D>
+struct FwdSmem {
+  static constexpr int Q_BYTES = BQ * D * 2;
+  static constexpr int K_BYTES = BKV * D * 2;
+  static constexpr int V_BYTES = BKV * D * 2;
+  static constexpr int P_BYTES = BQ * BKV * 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + NST * K_BYTES;
+  static constexpr int OFF_P = OFF_V + NST * V_BYTES;
+  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  static constexpr int TOTAL = OFF_BAR + 256 + 1024;  // barriers + alignment slack
+};
+
+// K-major SW128 descriptor for a [rows][64*nblk] tile stored as nblk 64-column
+// blocks of rows*128 bytes each; kk = 16-element K step.
+ZB_DEVICE uint64_t desc_kmajor(uint32_t base, int kk, int rows) {
+  return umma_desc_sw128(base + (kk >> 2) * rows * 128 + (kk & 3) * 32, 16, 1024);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_kernel(const __grid_constant__ CUtensorMap tm_rows128,
+               const __grid_constant__ CUtensorMap tm_rows64, __nv_bfloat16* __restrict__ out,
+               float* __restrict__ lse, int S, int H, float scale) {
+  using L = FwdSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;        // [NST]
+  uint64_t* kv_empty = bar + 3;       // [NST]
+  uint64_t* s_full = bar + 5;         // [2]
+  uint64_t* s_empty = bar + 7;        // [2]
+  uint64_t* p_full = bar + 9;         // [2]
+  uint64_t* p_empty = bar + 11;       // [2]
+  uint64_t* o_bar = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqt = S / BQ;
+  const int qt = nqt - 1 - blockIdx.x;  // heavy (late) query tiles first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int HD = H * D;
+  const int row0 = b * S;               // first qkv row of this sequence
+  const int nblk = qt + 1;              // causal: key blocks 0..qt
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_rows128);
+    tma_prefetch_desc(&tm_rows64);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+    }
+    mbar_init(o_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s[2] = {tmem, tmem + 128};
+  const uint32_t t_o = tmem + 256;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, L::Q_BYTES);
+#pragma unroll
+      for (int kc = 0; kc < D / 64; ++kc)
+        tma_load_2d(sm + L::OFF_Q + kc * BQ * 128, &tm_rows128, q_full, h * D + kc * 64,
+                    row0 + qt * BQ);
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % NST;
+        mbar_wait(&kv_empty[st], ((j / NST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], L::K_BYTES + L::V_BYTES);
+        uint8_t* kd = sm + L::OFF_K + st * L::K_BYTES;
+        uint8_t* vd = sm + L::OFF_V + st * L::V_BYTES;
+        const int kr = row0 + j * BKV;
+#pragma unroll
+        for (int kc = 0; kc < D / 64; ++kc)
+          tma_load_2d(kd + kc * BKV * 128, &tm_rows128, &kv_full[st], HD + h * D + kc * 64, kr);
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (int dc = 0; dc < D / 64; ++dc)
+            tma_load_2d(vd + (kb * (D / 64) + dc) * 8192, &tm_rows64, &kv_full[st],
+                        2 * HD + h * D + dc * 64, kr + kb * 64);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(BQ, BKV, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(BQ, D, 0, 1);
+      const uint32_t q_base = smem_u32(sm + L::OFF_Q);
+      auto issue_s = [&](int j) {
+        const int st = j % NST, sb = j & 1;
+        mbar_wait(&kv_full[st], (j / NST) & 1);
+        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sm + L::OFF_K + st * L::K_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16_ss(t_s[sb], desc_kmajor(q_base, kk, BQ), desc_kmajor(k_base, kk, BKV),
+                      idesc_s, kk > 0 ? 1u : 0u);
+        mma_commit(&s_full[sb]);
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      issue_s(0);
+      for (int j = 0; j < nblk; ++j) {
+        if (j + 1 < nblk) issue_s(j + 1);
+        const int st = j % NST, sb = j & 1;
+        mbar_wait(&p_full[sb], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t p_base = smem_u32(sm + L::OFF_P + sb * L::P_BYTES);
+        const uint32_t v_base = smem_u32(sm + L::OFF_V + st * L::V_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint64_t a = desc_kmajor(p_base, kk, BQ);
+          const uint64_t bdesc =
+              umma_desc_sw128(v_base + (kk >> 2) * (D / 64) * 8192 + (kk & 3) * 2048, 8192, 1024);
+          mma_bf16_ss(t_o, a, bdesc, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&kv_empty[st]);
+        mma_commit(&p_empty[sb]);
+        mma_commit(o_bar);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax
+    const int wq = warp - 4;                 // TMEM lane quarter
+    const int r = wq * 32 + lane;            // query row in the tile
+    const int q = qt * BQ + r;               // query position in the sequence
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const float sl2 = scale * LOG2E;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      float s[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_s[sb] + lane_off + c * 32, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[sb]);
+      float mx = m;
+      const bool diag = (j == qt);
+#pragma unroll
+      for (int c = 0; c < BKV; ++c) {
+        float x = s[c] * sl2;
+        if (diag && j * BKV + c > q) x = -INFINITY;
+        s[c] = x;
+        mx = fmaxf(mx, x);
+      }
+      const float corr = exp2_fast(m - mx);  // 0 on the first block (m = -inf)
+      m = mx;
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < BKV; ++c) {
+        s[c] = exp2_fast(s[c] - m);
+        rs += s[c];
+      }
+      l = l * corr + rs;
+      // P row -> smem (bf16, K-major SW128: two 64-key blocks of [128 rows][128 B])
+      mbar_wait(&p_empty[sb], ((j >> 1) & 1) ^ 1);
+      uint8_t* prow = sm + L::OFF_P + sb * L::P_BYTES + r * 128;
+#pragma unroll
+      for (int ch = 0; ch < BKV / 8; ++ch) {
+        uint4 pk;
+        pk.x = pack_bf16(s[ch * 8 + 0], s[ch * 8 + 1]);
+        pk.y = pack_bf16(s[ch * 8 + 2], s[ch * 8 + 3]);
+        pk.z = pack_bf16(s[ch * 8 + 4], s[ch * 8 + 5]);
+        pk.w = pack_bf16(s[ch * 8 + 6], s[ch * 8 + 7]);
+        const int kb = ch >> 3, cc = ch & 7;
+        *reinterpret_cast<uint4*>(prow + kb * (BQ * 128) + ((cc ^ (r & 7)) << 4)) = pk;
+      }
+      fence_proxy_async_smem();
+      // rescale O once the previous P V has landed (skip when no row's max moved)
+      if (j > 0) {
+        mbar_wait(o_bar, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st_32x32b_x32(t_o + lane_off + c * 32, v);
+          }
+          tmem_st_wait();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[sb]);
+    }
+    // epilogue: O / l -> bf16 row, lse
+    mbar_wait(o_bar, (nblk - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 pk;
+        pk.x = pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
+        pk.y = pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
+        pk.z = pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
+        pk.w = pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
+        *reinterpret_cast<uint4*>(orow + c * 32 + i) = pk;
+      }
+    }
+    lse[((size_t)b * H + h) * S + q] = (m + __log2f(l)) / LOG2E;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+template <int D>
+static int run_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int ld,
+                   float scale, cudaStream_t s) {
+  CUtensorMap m128, m64;
+  const uint64_t T = (uint64_t)n_seq * S;
+  if (int rc = make_tmap_bf16_2d(&m128, qkv, (uint64_t)3 * H * D, T, ld, 64, 128)) return rc;
+  if (int rc = make_tmap_bf16_2d(&m64, qkv, (uint64_t)3 * H * D, T, ld, 64, 64)) return rc;
+  const int smem = FwdSmem<D>::TOTAL;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_sm100: cudaFuncSetAttribute");
+    configured = true;
+  }
+  fwd_kernel<D><<<dim3(S / BQ, H, n_seq), kThreads, smem, s>>>(m128, m64, (__nv_bfloat16*)out,
+                                                               (float*)lse, S, H, scale);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_sm100 fwd launch");
+}
+
+}  // namespace fa
+}  // namespace zb
+
+using namespace zb;
+
+extern "C" int zb_attn_fwd_tc(const void* qkv, void* out, void* lse, int n_seq, int S, int H,
+                              int D, int ld, float scale, cudaStream_t s) {
+  if (S % 128) return set_error(ZB_ERR_INVALID, "attn_fwd_tc: seq_len must be a multiple of 128");
+  if (ld % 8 || ((uintptr_t)qkv & 15)) return set_error(ZB_ERR_INVALID, "attn_fwd_tc: bad ld/alignment");
+  if (n_seq <= 0) return 0;
+  if (D == 64) return fa::run_fwd<64>(qkv, out, lse, n_seq, S, H, ld, scale, s);
+  if (D == 128) return fa::run_fwd<128>(qkv, out, lse, n_seq, S, H, ld, scale, s);
+  return set_error(ZB_ERR_UNSUPPORTED, "attn_fwd_tc: head_dim %d unsupported (64, 128)", D);
+}

@@ -21,4 +21,7 @@ int tensor_map_encode(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, v
                       const cuuint32_t* estrides, CUtensorMapInterleave il,
                       CUtensorMapSwizzle sw, CUtensorMapL2promotion l2,
                       CUtensorMapFloatOOBfill oob);
+// 2-D bf16 tensor map, 128-byte swizzle, box {box_inner, box_outer}.
+int make_tmap_bf16_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                      uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer);
 }  // namespace zb

@@ -127,9 +127,10 @@ def bias_grad(dy, db, beta=1.0):
     call("zb_bias_grad", _ptr(dy), _ptr(db), rows, n, dy.stride(0), _stream())
 
 
-def attn_fwd(qkv, out, lse, n_seq, seq_len, n_head, head_dim, scale):
+def attn_fwd(qkv, out, lse, n_seq, seq_len, n_head, head_dim, scale, impl="tc"):
+    """impl "tc": tcgen05/TMEM kernel (default); "mma": legacy mma.sync kernel."""
     _need_cuda(qkv, out, lse)
-    call("zb_attn_fwd", _ptr(qkv), _ptr(out), _ptr(lse), n_seq, seq_len, n_head, head_dim,
+    call("zb_attn_fwd_tc" if impl == "tc" else "zb_attn_fwd", _ptr(qkv), _ptr(out), _ptr(lse), n_seq, seq_len, n_head, head_dim,
          qkv.stride(0), float(scale), _stream())
 
 

@@ -1,0 +1,31 @@
+"""Time attention kernels (tcgen05 vs mma.sync) at GPT-2 / Llama shapes."""
+import sys, os, json, math
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2507_10392_b200 import kernels as K
+
+def t_ms(fn, iters=20):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters): fn()
+    e.record(); torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+for (n, S, H, D) in [(8, 1024, 12, 64), (11, 1024, 12, 64), (2, 2048, 32, 128), (8, 1024, 25, 64)]:
+    T = n * S
+    qkv = torch.randn(T, 3 * H * D, device="cuda").bfloat16()
+    out = torch.empty(T, H * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(n, H, S, device="cuda")
+    dout = torch.randn(T, H * D, device="cuda").bfloat16()
+    dqkv = torch.empty_like(qkv); delta = torch.empty(n, H, S, device="cuda")
+    sc = 1 / math.sqrt(D)
+    fl = 4.0 * n * H * S * S * D / 2
+    r = {"shape": [n, S, H, D]}
+    for impl in ("tc", "mma"):
+        ms = t_ms(lambda: K.attn_fwd(qkv, out, lse, n, S, H, D, sc, impl=impl))
+        r[f"fwd_{impl}_ms"] = ms; r[f"fwd_{impl}_tflops"] = fl / ms / 1e9
+    ms = t_ms(lambda: K.attn_bwd(qkv, out, dout, lse, dqkv, None, delta, n, S, H, D, sc))
+    r["bwd_ms"] = ms; r["bwd_tflops(2.5x fwd flops)"] = 2.5 * fl / ms / 1e9
+    print(json.dumps(r), flush=True)

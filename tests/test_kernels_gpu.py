@@ -103,15 +103,17 @@ def _attn_ref(qkv, n_seq, S, H, D):
     return o.transpose(1, 2).reshape(n_seq * S, H * D), lse
 
 
-@pytest.mark.parametrize("n_seq,S,H,D", [(2, 128, 4, 64), (1, 1024, 3, 64), (2, 256, 2, 128)])
-def test_attention_fwd_bwd(cuda, n_seq, S, H, D):
+@pytest.mark.parametrize("impl", ["tc", "mma"])
+@pytest.mark.parametrize("n_seq,S,H,D", [(2, 128, 4, 64), (1, 1024, 3, 64), (2, 256, 2, 128),
+                                         (1, 2048, 2, 128)])
+def test_attention_fwd_bwd(cuda, n_seq, S, H, D, impl):
     torch.manual_seed(4)
     T = n_seq * S
     qkv = torch.randn(T, 3 * H * D, device="cuda").bfloat16()
     out = torch.empty(T, H * D, device="cuda", dtype=torch.bfloat16)
     lse = torch.empty(n_seq, H, S, device="cuda")
     scale = 1.0 / math.sqrt(D)
-    K.attn_fwd(qkv, out, lse, n_seq, S, H, D, scale)
+    K.attn_fwd(qkv, out, lse, n_seq, S, H, D, scale, impl=impl)
     qf = qkv.float().requires_grad_()
     ro, rlse = _attn_ref(qf, n_seq, S, H, D)
     torch.cuda.synchronize()
