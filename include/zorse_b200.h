@@ -40,7 +40,7 @@ int zb_device_sync(void);
  * a_mn_major: A stored [K][lda] (M contiguous) instead of [M][lda].
  * b_mn_major: B stored [K][ldb] (N contiguous) instead of [N][ldb].
  * epilogue: 0 C=acc | 1 C=acc+bias | 2 aux=acc+bias, C=gelu(aux) | 3 C=acc+bias+R
- *           4 C=acc*gelu'(aux) | 5 C(fp32)=beta*C+acc
+ *           4 C=acc*gelu'(aux) | 5 C(fp32)=beta*C+acc | 6 C=acc+R
  * Replaces the modelled per-layer compute of Fwd / Recompute / Bwd tasks
  * (simulate.py:330-367, 469-505; compute_time simulate.py:177-195). */
 int zb_gemm_bf16(const void* A, const void* B, void* C, const void* bias, const void* R,
@@ -71,7 +71,7 @@ int zb_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void*
 int zb_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mean,
                      const void* rstd, void* dx, void* dw, void* db, const void* dres, int rows,
                      int d, zb_stream_t stream);
-/* out[t] = wte[tok[t]] + wpe[t % seq]  (tok: int32). */
+/* out[t] = wte[tok[t]] + wpe[t % seq]  (tok: int32; wpe may be NULL). */
 int zb_embedding_fwd(const void* tok, const void* wte, const void* wpe, void* out, int rows, int d,
                      int seq, zb_stream_t stream);
 /* dwte[tok[t]] += dout[t]; dwpe[t % seq] += dout[t]  (fp32 accumulators). */
@@ -83,6 +83,19 @@ int zb_xent_fwd_bwd(const void* logits, const void* labels, void* loss_sum, void
                     int rows, int V, int ld, float scale, zb_stream_t stream);
 /* db[n] (fp32) += sum_rows dy[row, n]. */
 int zb_bias_grad(const void* dy, void* db, int rows, int n, int ld, zb_stream_t stream);
+/* Llama family: RMSNorm (rstd fp32 [rows]); dw (fp32) += grad; dres may be NULL. */
+int zb_rmsnorm_fwd(const void* x, const void* w, void* y, void* rstd, int rows, int d, float eps,
+                   zb_stream_t stream);
+int zb_rmsnorm_bwd(const void* dy, const void* x, const void* w, const void* rstd, void* dx,
+                   void* dw, const void* dres, int rows, int d, zb_stream_t stream);
+/* Rotary embedding in place on the q and k parts of fused QKV rows (pitch ld,
+ * rotate-half pairs (i, i+D/2), angle pos*theta^(-2i/D), pos = row % S);
+ * inverse=1 applies the transpose rotation (gradient). */
+int zb_rope(void* qkv, int rows, int S, int H, int D, int ld, float theta, int inverse,
+            zb_stream_t stream);
+/* gu rows = [gate(f) | up(f)]: out = silu(gate)*up; backward writes [dgate | dup] (may alias gu). */
+int zb_swiglu_fwd(const void* gu, void* out, int rows, int f, zb_stream_t stream);
+int zb_swiglu_bwd(const void* gu, const void* dout, void* dgu, int rows, int f, zb_stream_t stream);
 int zb_cast_f32_bf16(const void* src, void* dst, int64_t n, zb_stream_t stream);
 int zb_fill_f32(void* p, float value, int64_t n, zb_stream_t stream);
 int zb_add_bf16(const void* a, const void* b, void* out, int64_t n, zb_stream_t stream);

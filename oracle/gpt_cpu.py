@@ -36,7 +36,41 @@ def _gelu(x):
     return 0.5 * x * (1 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
 
 
+def _rope(t, S, theta=10000.0):
+    """t: [n_seq, H, S, D]; rotate-half pairs (i, i+D/2), angle pos*theta^(-2i/D)."""
+    D = t.shape[-1]
+    half = D // 2
+    inv = theta ** (-(2.0 * torch.arange(half, dtype=torch.float32)) / D)
+    ang = torch.arange(S, dtype=torch.float32)[:, None] * inv[None, :]
+    sn, cs = torch.sin(ang), torch.cos(ang)
+    a, b = t[..., :half], t[..., half:]
+    return torch.cat([a * cs - b * sn, a * sn + b * cs], -1)
+
+
+def _attention(q, k, v, n_seq, S, H, D):
+    s = (q @ k.transpose(-1, -2)) / math.sqrt(D)
+    s = s.masked_fill(torch.ones(S, S, dtype=torch.bool).triu(1), float("-inf"))
+    return (torch.softmax(s, -1) @ v).transpose(1, 2).reshape(n_seq * S, H * D)
+
+
+def _rmsnorm(x, w, eps=1e-5):
+    return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps) * w
+
+
+def _llama_block(cfg: ModelConfig, w, x, n_seq):
+    S, H, D, f = cfg.seq_len, cfg.n_head, cfg.head_dim, cfg.ffn
+    h = _rmsnorm(x, w["attn_norm"])
+    q, k, v = (h @ w["qkv_w"].t()).view(n_seq, S, 3, H, D).unbind(2)
+    q, k, v = (t.transpose(1, 2) for t in (q, k, v))
+    q, k = _rope(q, S), _rope(k, S)
+    x = x + _attention(q, k, v, n_seq, S, H, D) @ w["o_w"].t()
+    gu = _rmsnorm(x, w["mlp_norm"]) @ w["gu_w"].t()
+    return x + (F.silu(gu[:, :f]) * gu[:, f:]) @ w["down_w"].t()
+
+
 def _block(cfg: ModelConfig, w, x, n_seq):
+    if cfg.family == "llama":
+        return _llama_block(cfg, w, x, n_seq)
     S, H, D, d = cfg.seq_len, cfg.n_head, cfg.head_dim, cfg.d_model
     h = F.layer_norm(x, (d,), w["ln1_w"], w["ln1_b"], 1e-5)
     qkv = h @ w["qkv_w"].t() + w["qkv_b"]
@@ -62,11 +96,16 @@ def loss_and_grads(cfg: ModelConfig, params: Dict[object, torch.Tensor], batch: 
     tok = batch[:, :S].reshape(-1).long()
     lab = batch[:, 1:].reshape(-1).long()
     e = views["embed"]
-    x = e["wte"][tok] + e["wpe"][torch.arange(B * S) % S]
+    x = e["wte"][tok]
+    if "wpe" in e:
+        x = x + e["wpe"][torch.arange(B * S) % S]
     for i in range(cfg.n_layer):
         x = _block(cfg, views[i], x, B)
     h = views["head"]
-    xf = F.layer_norm(x, (cfg.d_model,), h["lnf_w"], h["lnf_b"], 1e-5)
+    if cfg.family == "llama":
+        xf = _rmsnorm(x, h["norm_w"])
+    else:
+        xf = F.layer_norm(x, (cfg.d_model,), h["lnf_w"], h["lnf_b"], 1e-5)
     logits = xf @ h["head_w"].t()
     loss = F.cross_entropy(logits, lab, reduction="sum") / (B * S)
     loss.backward()

@@ -32,6 +32,11 @@ SIGNATURES = {
     "zb_adamw_shard": [P, P, P, P, P, P, I64, F, F, F, F, F, F, I, P],
     "zb_adamw_shard_dstep": [P, P, P, P, P, P, I64, F, F, F, F, F, F, P, P],
     "zb_step_increment": [P, P],
+    "zb_rmsnorm_fwd": [P, P, P, P, I, I, F, P],
+    "zb_rmsnorm_bwd": [P, P, P, P, P, P, P, I, I, P],
+    "zb_rope": [P, I, I, I, I, I, F, I, P],
+    "zb_swiglu_fwd": [P, P, I, I, P],
+    "zb_swiglu_bwd": [P, P, P, I, I, P],
     "zb_cast_f32_bf16": [P, P, I64, P],
     "zb_fill_f32": [P, F, I64, P],
     "zb_add_bf16": [P, P, P, I64, P],

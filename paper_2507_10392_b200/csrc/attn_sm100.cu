@@ -172,7 +172,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = qt * BQ + r;               // query position in the sequence
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const float sl2 = scale * LOG2E;
+    // Running max in the scaled log2 domain.  It is only moved when a row's new
+    // max exceeds it by more than RESCALE_T (P stays <= 2^RESCALE_T, exact in
+    // fp32/bf16), so O is rarely rescaled and the softmax warps normally hand P_j
+    // to the MMA warp without waiting for P_{j-1} V_{j-1}.
+    constexpr float RESCALE_T = 8.f;
     float m = -INFINITY, l = 0.f;
+    int o_seen = 0;  // o_bar completions consumed (= PV blocks known complete)
     for (int j = 0; j < nblk; ++j) {
       const int sb = j & 1;
       mbar_wait(&s_full[sb], (j >> 1) & 1);
@@ -189,21 +195,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[sb]);
-      float mx = m;
-      const bool diag = (j == qt);
+      if (j == qt) {  // diagonal block: keys after the query are masked
 #pragma unroll
-      for (int c = 0; c < BKV; ++c) {
-        float x = s[c] * sl2;
-        if (diag && j * BKV + c > q) x = -INFINITY;
-        s[c] = x;
-        mx = fmaxf(mx, x);
+        for (int c = 0; c < BKV; ++c)
+          if (c > r) s[c] = -INFINITY;
       }
-      const float corr = exp2_fast(m - mx);  // 0 on the first block (m = -inf)
-      m = mx;
+      float mx = s[0];
+#pragma unroll
+      for (int c = 1; c < BKV; ++c) mx = fmaxf(mx, s[c]);
+      mx *= sl2;
+      const bool move = mx > m + RESCALE_T;
+      const float m_new = move ? mx : m;
+      const float corr = move ? exp2_fast(m - m_new) : 1.f;  // 0 on the first block
+      m = m_new;
       float rs = 0.f;
 #pragma unroll
       for (int c = 0; c < BKV; ++c) {
-        s[c] = exp2_fast(s[c] - m);
+        s[c] = exp2_fast(fmaf(s[c], sl2, -m));
         rs += s[c];
       }
       l = l * corr + rs;
@@ -221,29 +229,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<uint4*>(prow + kb * (BQ * 128) + ((cc ^ (r & 7)) << 4)) = pk;
       }
       fence_proxy_async_smem();
-      // rescale O once the previous P V has landed (skip when no row's max moved)
-      if (j > 0) {
-        mbar_wait(o_bar, (j - 1) & 1);
+      const bool rescale = j > 0 && __any_sync(0xffffffffu, move);
+      if (rescale) {  // O must hold P_{j-1} V_{j-1} before it is rescaled
+        mbar_wait(o_bar, o_seen & 1);
+        ++o_seen;
         tc_fence_after();
-        if (__any_sync(0xffffffffu, corr != 1.f)) {
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
-            tmem_ld_wait();
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+          tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
-            tmem_st_32x32b_x32(t_o + lane_off + c * 32, v);
-          }
-          tmem_st_wait();
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+          tmem_st_32x32b_x32(t_o + lane_off + c * 32, v);
         }
+        tmem_st_wait();
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[sb]);
+      // keep o_bar consumption in step (never more than one completion behind)
+      if (j > 0 && o_seen < j) {
+        mbar_wait(o_bar, o_seen & 1);
+        ++o_seen;
+      }
     }
     // epilogue: O / l -> bf16 row, lse
-    mbar_wait(o_bar, (nblk - 1) & 1);
+    while (o_seen < nblk) {
+      mbar_wait(o_bar, o_seen & 1);
+      ++o_seen;
+    }
     tc_fence_after();
     const float inv = 1.f / l;
     __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D;

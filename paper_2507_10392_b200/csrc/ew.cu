@@ -169,7 +169,8 @@ __global__ void embedding_fwd_kernel(const int* __restrict__ tok,
        i += (size_t)gridDim.x * blockDim.x) {
     const int row = (int)(i / nv), v = (int)(i % nv);
     const uint4 a = reinterpret_cast<const uint4*>(wte + (size_t)tok[row] * d)[v];
-    const uint4 p = reinterpret_cast<const uint4*>(wpe + (size_t)(row % seq) * d)[v];
+    const uint4 p = wpe ? reinterpret_cast<const uint4*>(wpe + (size_t)(row % seq) * d)[v]
+                        : make_uint4(0, 0, 0, 0);  // no learned positions (Llama: RoPE)
     const uint32_t *ai = &a.x, *pi = &p.x;
     uint4 o;
     uint32_t* oi = &o.x;
@@ -194,14 +195,16 @@ __global__ void embedding_bwd_kernel(const int* __restrict__ tok,
     const uint4 g = reinterpret_cast<const uint4*>(dout + (size_t)row * d)[v];
     const uint32_t* gi = &g.x;
     float* te = dwte + (size_t)tok[row] * d + v * 8;
-    float* pe = dwpe + (size_t)(row % seq) * d + v * 8;
+    float* pe = dwpe ? dwpe + (size_t)(row % seq) * d + v * 8 : nullptr;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       float2 x = unpack_bf16(gi[k]);
       atomicAdd(te + 2 * k, x.x);
       atomicAdd(te + 2 * k + 1, x.y);
-      atomicAdd(pe + 2 * k, x.x);
-      atomicAdd(pe + 2 * k + 1, x.y);
+      if (pe) {
+        atomicAdd(pe + 2 * k, x.x);
+        atomicAdd(pe + 2 * k + 1, x.y);
+      }
     }
   }
 }

@@ -31,6 +31,7 @@ enum Epilogue : int {
   EPI_BIAS_RESID = 3,  // C = acc + bias[n] + R[m,n]
   EPI_GELU_BWD = 4,    // C = acc * gelu'(AUX[m,n])
   EPI_F32 = 5,         // C(fp32) = beta * C + acc
+  EPI_RESID = 6,       // C = acc + R[m,n]            (bias-free residual, Llama)
 };
 
 struct GemmArgs {
@@ -119,7 +120,7 @@ ZB_DEVICE void epilogue_chunk(const GemmArgs& args, const uint32_t (&r)[32], int
         if (col0 + j < args.N) v[j] += __bfloat162float(args.bias[col0 + j]);
     }
   }
-  if (EPI == EPI_BIAS_RESID) {
+  if (EPI == EPI_BIAS_RESID || EPI == EPI_RESID) {
     const __nv_bfloat16* Rp = args.R + (size_t)row * args.ldr + col0;
     if (full) {
 #pragma unroll
@@ -405,6 +406,7 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, G
     case EPI_BIAS_RESID: return launch_gemm<BN, A_MN, B_MN, EPI_BIAS_RESID>(ta, tb, args, s);
     case EPI_GELU_BWD: return launch_gemm<BN, A_MN, B_MN, EPI_GELU_BWD>(ta, tb, args, s);
     case EPI_F32: return launch_gemm<BN, A_MN, B_MN, EPI_F32>(ta, tb, args, s);
+    case EPI_RESID: return launch_gemm<BN, A_MN, B_MN, EPI_RESID>(ta, tb, args, s);
   }
   return set_error(ZB_ERR_INVALID, "gemm: unknown epilogue %d", epi);
 }

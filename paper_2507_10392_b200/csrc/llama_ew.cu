@@ -1,0 +1,255 @@
+// Llama-family elementwise kernels (BASELINE configs 4 and 5): RMSNorm fwd/bwd,
+// rotary position embedding applied in place on the fused QKV rows (and its
+// inverse on the gradients), SwiGLU fwd/bwd.  HBM-bound; 16-byte accesses,
+// fp32 math, warp-shuffle reductions.
+#include "common.cuh"
+#include "zb_internal.h"
+
+namespace zb {
+
+// ------------------------------------------------------------------ RMSNorm
+// y = x * rstd * w,  rstd = 1/sqrt(mean(x^2) + eps).  One warp per row.
+__global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                   const __nv_bfloat16* __restrict__ w,
+                                   __nv_bfloat16* __restrict__ y, float* __restrict__ rstd_out,
+                                   int rows, int d, float eps) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * d);
+  const int nv = d >> 3;
+  float ss = 0.f;
+  for (int v = lane; v < nv; v += 32) {
+    uint4 q = xr[v];
+    const uint32_t* qi = &q.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = unpack_bf16(qi[k]);
+      ss += f.x * f.x + f.y * f.y;
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(ss) / d + eps);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4* yr = reinterpret_cast<uint4*>(y + (size_t)row * d);
+  for (int v = lane; v < nv; v += 32) {
+    uint4 q = xr[v], qw = wr[v], o;
+    const uint32_t *qi = &q.x, *wi = &qw.x;
+    uint32_t* oi = &o.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = unpack_bf16(qi[k]), g = unpack_bf16(wi[k]);
+      oi[k] = pack_bf16(f.x * rstd * g.x, f.y * rstd * g.y);
+    }
+    yr[v] = o;
+  }
+  if (lane == 0) rstd_out[row] = rstd;
+}
+
+// dx = dres + rstd * (g - xhat * mean(g * xhat)),  g = dy * w,  xhat = x * rstd
+// dw += sum_rows dy * xhat  (smem per-block partials, one atomic per column per block)
+__global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                   const __nv_bfloat16* __restrict__ x,
+                                   const __nv_bfloat16* __restrict__ w,
+                                   const float* __restrict__ rstd_in, __nv_bfloat16* dx,
+                                   float* __restrict__ dw, const __nv_bfloat16* dres, int rows,
+                                   int d) {
+  extern __shared__ float sdw[];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) sdw[i] = 0.f;
+  __syncthreads();
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nv = d >> 3;
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + (size_t)row * d);
+    const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * d);
+    const float rstd = rstd_in[row];
+    float sgx = 0.f;
+    for (int v = lane; v < nv; v += 32) {
+      uint4 qd = dyr[v], qx = xr[v], qw = wr[v];
+      const uint32_t *di = &qd.x, *xi = &qx.x, *wi = &qw.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
+        const float h0 = xv.x * rstd, h1 = xv.y * rstd;
+        sgx += dv.x * wv.x * h0 + dv.y * wv.y * h1;
+        atomicAdd(&sdw[v * 8 + 2 * k], dv.x * h0);
+        atomicAdd(&sdw[v * 8 + 2 * k + 1], dv.y * h1);
+      }
+    }
+    const float mgx = warp_sum(sgx) / d;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + (size_t)row * d);
+    const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + (size_t)row * d) : nullptr;
+    for (int v = lane; v < nv; v += 32) {
+      uint4 qd = dyr[v], qx = xr[v], qw = wr[v];
+      uint4 qr = rr ? rr[v] : make_uint4(0, 0, 0, 0);
+      const uint32_t *di = &qd.x, *xi = &qx.x, *wi = &qw.x, *ri = &qr.x;
+      uint4 o;
+      uint32_t* oi = &o.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
+        float2 rv = rr ? unpack_bf16(ri[k]) : make_float2(0.f, 0.f);
+        const float o0 = rstd * (dv.x * wv.x - xv.x * rstd * mgx) + rv.x;
+        const float o1 = rstd * (dv.y * wv.y - xv.y * rstd * mgx) + rv.y;
+        oi[k] = pack_bf16(o0, o1);
+      }
+      dxr[v] = o;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < d; i += blockDim.x) atomicAdd(&dw[i], sdw[i]);
+}
+
+// ------------------------------------------------------------------ RoPE
+// In place on the q and k parts of fused QKV rows (pitch ld): for each head and
+// i < D/2:  (a, b) = (x[i], x[i + D/2]) -> (a cos - b sin, a sin + b cos),
+// angle = pos * theta^(-2i/D), pos = row % S.  inverse=1 rotates by -angle
+// (the gradient of the rotation).
+__global__ void rope_kernel(__nv_bfloat16* qkv, int rows, int S, int H, int D, int ld,
+                            float theta, int inverse) {
+  const int half = D / 2;
+  const long long total = (long long)rows * 2 * H * half;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % half);
+    long long t = i / half;
+    const int hh = (int)(t % (2 * H));  // 0..H-1: q heads, H..2H-1: k heads
+    const int row = (int)(t / (2 * H));
+    const int pos = row % S;
+    const float inv_freq = exp2f(-(2.f * c / D) * log2f(theta));
+    float sn, cs;
+    sincosf(pos * inv_freq, &sn, &cs);
+    if (inverse) sn = -sn;
+    __nv_bfloat16* p = qkv + (size_t)row * ld + hh * D;
+    const float a = __bfloat162float(p[c]), b = __bfloat162float(p[c + half]);
+    p[c] = __float2bfloat16(a * cs - b * sn);
+    p[c + half] = __float2bfloat16(a * sn + b * cs);
+  }
+}
+
+// ------------------------------------------------------------------ SwiGLU
+// gu rows = [gate(f) | up(f)];  out = silu(gate) * up.
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
+                                  __nv_bfloat16* __restrict__ out, int rows, int f) {
+  const int nv = f >> 3;
+  const long long total = (long long)rows * nv;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(i / nv), v = (int)(i % nv);
+    const __nv_bfloat16* r = gu + (size_t)row * 2 * f;
+    const uint4 g = reinterpret_cast<const uint4*>(r)[v];
+    const uint4 u = reinterpret_cast<const uint4*>(r + f)[v];
+    const uint32_t *gi = &g.x, *ui = &u.x;
+    uint4 o;
+    uint32_t* oi = &o.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 a = unpack_bf16(gi[k]), b = unpack_bf16(ui[k]);
+      const float s0 = a.x / (1.f + __expf(-a.x)), s1 = a.y / (1.f + __expf(-a.y));
+      oi[k] = pack_bf16(s0 * b.x, s1 * b.y);
+    }
+    reinterpret_cast<uint4*>(out + (size_t)row * f)[v] = o;
+  }
+}
+
+// dgu = [dgate | dup]:  dgate = dout * up * silu'(gate), dup = dout * silu(gate).
+// May run in place (dgu == gu).
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* gu, const __nv_bfloat16* __restrict__ dout,
+                                  __nv_bfloat16* dgu, int rows, int f) {
+  const int nv = f >> 3;
+  const long long total = (long long)rows * nv;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(i / nv), v = (int)(i % nv);
+    const __nv_bfloat16* r = gu + (size_t)row * 2 * f;
+    const uint4 g = reinterpret_cast<const uint4*>(r)[v];
+    const uint4 u = reinterpret_cast<const uint4*>(r + f)[v];
+    const uint4 d = reinterpret_cast<const uint4*>(dout + (size_t)row * f)[v];
+    const uint32_t *gi = &g.x, *ui = &u.x, *di = &d.x;
+    uint4 og, ou;
+    uint32_t *ogi = &og.x, *oui = &ou.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 a = unpack_bf16(gi[k]), b = unpack_bf16(ui[k]), dd = unpack_bf16(di[k]);
+      const float sg0 = 1.f / (1.f + __expf(-a.x)), sg1 = 1.f / (1.f + __expf(-a.y));
+      const float si0 = a.x * sg0, si1 = a.y * sg1;
+      const float ds0 = sg0 * (1.f + a.x * (1.f - sg0)), ds1 = sg1 * (1.f + a.y * (1.f - sg1));
+      ogi[k] = pack_bf16(dd.x * b.x * ds0, dd.y * b.y * ds1);
+      oui[k] = pack_bf16(dd.x * si0, dd.y * si1);
+    }
+    __nv_bfloat16* w = dgu + (size_t)row * 2 * f;
+    reinterpret_cast<uint4*>(w)[v] = og;
+    reinterpret_cast<uint4*>(w + f)[v] = ou;
+  }
+}
+
+static int grid_for2(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  long long cap = (long long)num_sms() * 16;
+  return (int)(g < 1 ? 1 : (g < cap ? g : cap));
+}
+
+static int launched2(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, what);
+}
+
+}  // namespace zb
+
+using namespace zb;
+
+extern "C" int zb_rmsnorm_fwd(const void* x, const void* w, void* y, void* rstd, int rows, int d,
+                              float eps, cudaStream_t s) {
+  if (d % 8) return set_error(ZB_ERR_INVALID, "rmsnorm: d must be a multiple of 8");
+  if (rows <= 0) return 0;
+  rmsnorm_fwd_kernel<<<(rows + 7) / 8, 256, 0, s>>>((const __nv_bfloat16*)x,
+                                                     (const __nv_bfloat16*)w, (__nv_bfloat16*)y,
+                                                     (float*)rstd, rows, d, eps);
+  return launched2("rmsnorm_fwd");
+}
+
+extern "C" int zb_rmsnorm_bwd(const void* dy, const void* x, const void* w, const void* rstd,
+                              void* dx, void* dw, const void* dres, int rows, int d,
+                              cudaStream_t s) {
+  if (d % 8) return set_error(ZB_ERR_INVALID, "rmsnorm: d must be a multiple of 8");
+  if (rows <= 0) return 0;
+  int blocks = (rows + 63) / 64;
+  if (blocks > 2 * num_sms()) blocks = 2 * num_sms();
+  const size_t smem = (size_t)d * sizeof(float);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  rmsnorm_bwd_kernel<<<blocks, 256, smem, s>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                                               (const __nv_bfloat16*)w, (const float*)rstd,
+                                               (__nv_bfloat16*)dx, (float*)dw,
+                                               (const __nv_bfloat16*)dres, rows, d);
+  return launched2("rmsnorm_bwd");
+}
+
+extern "C" int zb_rope(void* qkv, int rows, int S, int H, int D, int ld, float theta, int inverse,
+                       cudaStream_t s) {
+  if (D % 2) return set_error(ZB_ERR_INVALID, "rope: head_dim must be even");
+  if (rows <= 0) return 0;
+  long long n = (long long)rows * 2 * H * (D / 2);
+  rope_kernel<<<grid_for2(n, 256), 256, 0, s>>>((__nv_bfloat16*)qkv, rows, S, H, D, ld, theta,
+                                                inverse);
+  return launched2("rope");
+}
+
+extern "C" int zb_swiglu_fwd(const void* gu, void* out, int rows, int f, cudaStream_t s) {
+  if (f % 8) return set_error(ZB_ERR_INVALID, "swiglu: f must be a multiple of 8");
+  if (rows <= 0) return 0;
+  swiglu_fwd_kernel<<<grid_for2((long long)rows * (f / 8), 256), 256, 0, s>>>(
+      (const __nv_bfloat16*)gu, (__nv_bfloat16*)out, rows, f);
+  return launched2("swiglu_fwd");
+}
+
+extern "C" int zb_swiglu_bwd(const void* gu, const void* dout, void* dgu, int rows, int f,
+                             cudaStream_t s) {
+  if (f % 8) return set_error(ZB_ERR_INVALID, "swiglu: f must be a multiple of 8");
+  if (rows <= 0) return 0;
+  swiglu_bwd_kernel<<<grid_for2((long long)rows * (f / 8), 256), 256, 0, s>>>(
+      (const __nv_bfloat16*)gu, (const __nv_bfloat16*)dout, (__nv_bfloat16*)dgu, rows, f);
+  return launched2("swiglu_bwd");
+}

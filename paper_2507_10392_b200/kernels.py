@@ -35,6 +35,7 @@ EPI_BIAS_GELU = 2
 EPI_BIAS_RESID = 3
 EPI_GELU_BWD = 4
 EPI_F32 = 5
+EPI_RESID = 6
 
 
 def _stream():
@@ -176,3 +177,32 @@ def step_increment(step_dev):
     """step_dev (int32 CUDA tensor) += 1 on the device."""
     _need_cuda(step_dev)
     call("zb_step_increment", _ptr(step_dev), _stream())
+
+
+def rmsnorm_fwd(x, w, y, rstd, eps=1e-5):
+    _need_cuda(x, w, y, rstd)
+    rows, d = x.shape
+    call("zb_rmsnorm_fwd", _ptr(x), _ptr(w), _ptr(y), _ptr(rstd), rows, d, float(eps), _stream())
+
+
+def rmsnorm_bwd(dy, x, w, rstd, dx, dw, dx_accum=None):
+    _need_cuda(dy, x, w, rstd, dx, dw, dx_accum)
+    rows, d = x.shape
+    call("zb_rmsnorm_bwd", _ptr(dy), _ptr(x), _ptr(w), _ptr(rstd), _ptr(dx), _ptr(dw),
+         _ptr(dx_accum), rows, d, _stream())
+
+
+def rope(qkv, seq_len, n_head, head_dim, theta=10000.0, inverse=False):
+    _need_cuda(qkv)
+    call("zb_rope", _ptr(qkv), qkv.shape[0], seq_len, n_head, head_dim, qkv.stride(0),
+         float(theta), int(inverse), _stream())
+
+
+def swiglu_fwd(gu, out):
+    _need_cuda(gu, out)
+    call("zb_swiglu_fwd", _ptr(gu), _ptr(out), out.shape[0], out.shape[1], _stream())
+
+
+def swiglu_bwd(gu, dout, dgu):
+    _need_cuda(gu, dout, dgu)
+    call("zb_swiglu_bwd", _ptr(gu), _ptr(dout), _ptr(dgu), dout.shape[0], dout.shape[1], _stream())

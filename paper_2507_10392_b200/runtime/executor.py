@@ -40,7 +40,7 @@ from ..plan.costs import CostContext
 from ..plan.emulated import ModelConfig
 from ..plan.schedule import Event, build_schedule
 from ..plan.shard import ShardSpec, split_flat
-from .model import (FlatLayout, GptOps, alloc_acts, alloc_bwd_scratch, embed_layout,
+from .model import (FlatLayout, make_model_ops, alloc_acts, alloc_bwd_scratch, embed_layout,
                     head_layout, init_flat, layer_layout)
 
 
@@ -96,7 +96,7 @@ class StageExecutor:
         self.rank_of = rank_of
         self.world, self.group_comm, self.ops, self.device = world_comm, group_comm, ops, device
         self.adam = adam
-        self.model = GptOps(cfg, ops)
+        self.model = make_model_ops(cfg, ops)
         self.schedule = build_schedule(ctx, plan)
         self.events: List[Event] = self.schedule.stream_for(dev_id)
         self.order = plan.global_order()

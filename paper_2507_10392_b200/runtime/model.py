@@ -30,7 +30,7 @@ import torch
 
 from ..plan.emulated import ModelConfig
 
-EPI_BF16, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_GELU_BWD, EPI_F32 = range(6)
+EPI_BF16, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_GELU_BWD, EPI_F32, EPI_RESID = range(7)
 
 
 class FlatLayout:
@@ -61,17 +61,25 @@ class FlatLayout:
 
 def layer_layout(cfg: ModelConfig) -> FlatLayout:
     d, f = cfg.d_model, cfg.ffn
+    if cfg.family == "llama":
+        # 4d^2 + 3df + 2d (SURVEY §8 notation); gate and up projections fused [2f, d]
+        return FlatLayout([("attn_norm", (d,)), ("qkv_w", (3 * d, d)), ("o_w", (d, d)),
+                           ("mlp_norm", (d,)), ("gu_w", (2 * f, d)), ("down_w", (d, f))])
     return FlatLayout([("ln1_w", (d,)), ("ln1_b", (d,)), ("qkv_w", (3 * d, d)), ("qkv_b", (3 * d,)),
                        ("proj_w", (d, d)), ("proj_b", (d,)), ("ln2_w", (d,)), ("ln2_b", (d,)),
                        ("fc1_w", (f, d)), ("fc1_b", (f,)), ("fc2_w", (d, f)), ("fc2_b", (d,))])
 
 
 def embed_layout(cfg: ModelConfig) -> FlatLayout:
+    if cfg.family == "llama":
+        return FlatLayout([("wte", (cfg.vocab, cfg.d_model))])
     return FlatLayout([("wte", (cfg.vocab, cfg.d_model)), ("wpe", (cfg.seq_len, cfg.d_model))])
 
 
 def head_layout(cfg: ModelConfig) -> FlatLayout:
     d = cfg.d_model
+    if cfg.family == "llama":
+        return FlatLayout([("norm_w", (d,)), ("head_w", (cfg.vocab, d))])
     return FlatLayout([("lnf_w", (d,)), ("lnf_b", (d,)), ("head_w", (cfg.vocab, d))])
 
 
@@ -88,7 +96,7 @@ def init_flat(layout: FlatLayout, kind: str, index: int, cfg: ModelConfig, seed:
         v = views[name]
         if name.endswith("_b"):
             v.zero_()
-        elif name.startswith("ln"):
+        elif name.startswith("ln") or name.endswith("norm") or name == "norm_w":
             v.fill_(1.0)
         else:
             std = resid_std if name in ("proj_w", "fc2_w") else 0.02
@@ -117,7 +125,35 @@ class LayerActs:
     g: torch.Tensor       # gelu(u)            [n, f]
 
 
-def alloc_acts(cfg: ModelConfig, n_tok: int, device) -> LayerActs:
+@dataclass
+class LlamaActs:
+    h1: torch.Tensor      # RMSNorm1(x)       [n, d]
+    rstd1: torch.Tensor
+    qkv: torch.Tensor     # post-RoPE q,k | v  [n, 3d]
+    attn: torch.Tensor    # [n, d]
+    lse: torch.Tensor
+    x_mid: torch.Tensor   # [n, d]
+    h2: torch.Tensor      # RMSNorm2(x_mid)
+    rstd2: torch.Tensor
+    gu: torch.Tensor      # [gate | up]       [n, 2f]
+    m: torch.Tensor       # silu(gate) * up   [n, f]
+
+
+def alloc_acts(cfg: ModelConfig, n_tok: int, device):
+    if cfg.family == "llama":
+        d, f, H, S = cfg.d_model, cfg.ffn, cfg.n_head, cfg.seq_len
+        n = max(n_tok, 1)
+        bf = dict(device=device, dtype=torch.bfloat16)
+        return LlamaActs(h1=torch.empty(n, d, **bf), rstd1=torch.empty(n, device=device),
+                         qkv=torch.empty(n, 3 * d, **bf), attn=torch.empty(n, d, **bf),
+                         lse=torch.empty(max(n_tok // S, 1), H, S, device=device),
+                         x_mid=torch.empty(n, d, **bf), h2=torch.empty(n, d, **bf),
+                         rstd2=torch.empty(n, device=device), gu=torch.empty(n, 2 * f, **bf),
+                         m=torch.empty(n, f, **bf))
+    return _alloc_gpt_acts(cfg, n_tok, device)
+
+
+def _alloc_gpt_acts(cfg: ModelConfig, n_tok: int, device) -> LayerActs:
     d, f, H, S = cfg.d_model, cfg.ffn, cfg.n_head, cfg.seq_len
     seqs = max(n_tok // S, 1)
     bf = dict(device=device, dtype=torch.bfloat16)
@@ -224,3 +260,76 @@ class GptOps:
         o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         o.gemm(logits[:n], p["head_w"], dhf[:n], b_t=True)
         o.layernorm_bwd(dhf[:n], x, p["lnf_w"], mean[:n], rstd[:n], dx, gr["lnf_w"], gr["lnf_b"])
+
+
+class LlamaOps:
+    """Llama block (pre-RMSNorm, RoPE, SwiGLU, no biases) as kernel calls; same
+    interface as GptOps."""
+
+    ROPE_THETA = 10000.0
+
+    def __init__(self, cfg: ModelConfig, ops):
+        self.cfg, self.ops = cfg, ops
+        self.scale = 1.0 / math.sqrt(cfg.head_dim)
+
+    def layer_fwd(self, p, x, out, a: LlamaActs, n_tok: int, need_out: bool = True) -> None:
+        o, cfg = self.ops, self.cfg
+        n = n_tok
+        n_seq = n // cfg.seq_len
+        o.rmsnorm_fwd(x, p["attn_norm"], a.h1[:n], a.rstd1[:n])
+        o.gemm(a.h1[:n], p["qkv_w"], a.qkv[:n])
+        o.rope(a.qkv[:n], cfg.seq_len, cfg.n_head, cfg.head_dim, self.ROPE_THETA)
+        o.attn_fwd(a.qkv[:n], a.attn[:n], a.lse[:n_seq], n_seq, cfg.seq_len, cfg.n_head,
+                   cfg.head_dim, self.scale)
+        o.gemm(a.attn[:n], p["o_w"], a.x_mid[:n], epilogue=EPI_RESID, resid=x)
+        o.rmsnorm_fwd(a.x_mid[:n], p["mlp_norm"], a.h2[:n], a.rstd2[:n])
+        o.gemm(a.h2[:n], p["gu_w"], a.gu[:n])
+        o.swiglu_fwd(a.gu[:n], a.m[:n])
+        if need_out:
+            o.gemm(a.m[:n], p["down_w"], out, epilogue=EPI_RESID, resid=a.x_mid[:n])
+
+    def layer_bwd(self, p, gr, x, dy, dx, a: LlamaActs, s: BwdScratch, n_tok: int) -> None:
+        o, cfg = self.ops, self.cfg
+        n = n_tok
+        n_seq = n // cfg.seq_len
+        o.gemm(dy, a.m[:n], gr["down_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        o.gemm(dy, p["down_w"], a.m[:n], b_t=True)                 # dm (m no longer needed)
+        o.swiglu_bwd(a.gu[:n], a.m[:n], a.gu[:n])                  # d[gate|up] in place
+        o.gemm(a.gu[:n], a.h2[:n], gr["gu_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        o.gemm(a.gu[:n], p["gu_w"], s.dh[:n], b_t=True)
+        o.rmsnorm_bwd(s.dh[:n], a.x_mid[:n], p["mlp_norm"], a.rstd2[:n], s.dx_mid[:n],
+                      gr["mlp_norm"], dx_accum=dy)
+        o.gemm(s.dx_mid[:n], a.attn[:n], gr["o_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        o.gemm(s.dx_mid[:n], p["o_w"], s.da[:n], b_t=True)
+        o.attn_bwd(a.qkv[:n], a.attn[:n], s.da[:n], a.lse[:n_seq], s.dqkv[:n], None,
+                   s.delta[:n_seq], n_seq, cfg.seq_len, cfg.n_head, cfg.head_dim, self.scale)
+        o.rope(s.dqkv[:n], cfg.seq_len, cfg.n_head, cfg.head_dim, self.ROPE_THETA, inverse=True)
+        o.gemm(s.dqkv[:n], a.h1[:n], gr["qkv_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        o.gemm(s.dqkv[:n], p["qkv_w"], s.dh[:n], b_t=True)
+        o.rmsnorm_bwd(s.dh[:n], x, p["attn_norm"], a.rstd1[:n], dx, gr["attn_norm"],
+                      dx_accum=s.dx_mid[:n])
+
+    def embed_fwd(self, p, tokens, out, n_tok):
+        self.ops.embedding_fwd(tokens[:n_tok], p["wte"], None, out, self.cfg.seq_len)
+
+    def embed_bwd(self, gr, tokens, dx, n_tok):
+        self.ops.embedding_bwd(tokens[:n_tok], dx, gr["wte"], None, self.cfg.seq_len)
+
+    def head_fwd_bwd(self, p, gr, x, labels, dx, logits, hf, mean, rstd, dhf, loss_sum, scale,
+                     n_tok):
+        o = self.ops
+        n = n_tok
+        o.rmsnorm_fwd(x, p["norm_w"], hf[:n], rstd[:n])
+        o.gemm(hf[:n], p["head_w"], logits[:n])
+        o.xent_fwd_bwd(logits[:n], labels[:n], loss_sum, logits[:n], scale)
+        o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        o.gemm(logits[:n], p["head_w"], dhf[:n], b_t=True)
+        o.rmsnorm_bwd(dhf[:n], x, p["norm_w"], rstd[:n], dx, gr["norm_w"])
+
+
+def make_model_ops(cfg: ModelConfig, ops):
+    if cfg.family == "gpt":
+        return GptOps(cfg, ops)
+    if cfg.family == "llama":
+        return LlamaOps(cfg, ops)
+    raise NotImplementedError(f"model family {cfg.family!r}")

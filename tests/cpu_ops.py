@@ -11,7 +11,7 @@ import math
 
 import torch
 
-EPI_BF16, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_GELU_BWD, EPI_F32 = range(6)
+EPI_BF16, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_GELU_BWD, EPI_F32, EPI_RESID = range(7)
 
 
 def _gelu(x):
@@ -34,7 +34,7 @@ def gemm(a, b, out, *, a_t=False, b_t=False, epilogue=EPI_BF16, bias=None, resid
         return out
     if epilogue in (EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID):
         acc = acc + bias.float()
-    if epilogue == EPI_BIAS_RESID:
+    if epilogue in (EPI_BIAS_RESID, EPI_RESID):
         acc = acc + resid.float()
     if epilogue == EPI_BIAS_GELU:
         aux.copy_(acc)
@@ -70,13 +70,17 @@ def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None):
 
 def embedding_fwd(tokens, wte, wpe, out, seq_len):
     pos = torch.arange(out.shape[0]) % seq_len
-    out.copy_(wte.float()[tokens.long()] + wpe.float()[pos])
+    x = wte.float()[tokens.long()]
+    if wpe is not None:
+        x = x + wpe.float()[pos]
+    out.copy_(x)
 
 
 def embedding_bwd(tokens, dout, dwte, dwpe, seq_len):
     pos = torch.arange(dout.shape[0]) % seq_len
     dwte.index_add_(0, tokens.long(), dout.float())
-    dwpe.index_add_(0, pos, dout.float())
+    if dwpe is not None:
+        dwpe.index_add_(0, pos, dout.float())
 
 
 def xent_fwd_bwd(logits, labels, loss_sum, dlogits, scale):
@@ -186,3 +190,52 @@ class GlooComm:
 
 def step_increment(step_dev):
     step_dev += 1
+
+
+def rmsnorm_fwd(x, w, y, rstd, eps=1e-5):
+    xf = x.float()
+    rs = torch.rsqrt((xf * xf).mean(-1) + eps)
+    y.copy_(xf * rs[:, None] * w.float())
+    rstd.copy_(rs)
+
+
+def rmsnorm_bwd(dy, x, w, rstd, dx, dw, dx_accum=None):
+    xh = x.float() * rstd[:, None]
+    g = dy.float() * w.float()
+    out = rstd[:, None] * (g - xh * (g * xh).mean(-1, keepdim=True))
+    if dx_accum is not None:
+        out = out + dx_accum.float()
+    dw += (dy.float() * xh).sum(0)
+    dx.copy_(out)
+
+
+def rope(qkv, seq_len, n_head, head_dim, theta=10000.0, inverse=False):
+    rows = qkv.shape[0]
+    half = head_dim // 2
+    pos = (torch.arange(rows) % seq_len).float()
+    inv = theta ** (-(2.0 * torch.arange(half).float()) / head_dim)
+    ang = pos[:, None] * inv[None, :]
+    sn, cs = torch.sin(ang), torch.cos(ang)
+    if inverse:
+        sn = -sn
+    x = qkv[:, :2 * n_head * head_dim].float().view(rows, 2 * n_head, head_dim)
+    a, b = x[..., :half], x[..., half:]
+    na = a * cs[:, None, :] - b * sn[:, None, :]
+    nb = a * sn[:, None, :] + b * cs[:, None, :]
+    qkv[:, :2 * n_head * head_dim].copy_(torch.cat([na, nb], -1).view(rows, -1))
+
+
+def swiglu_fwd(gu, out):
+    f = out.shape[1]
+    g, u = gu[:, :f].float(), gu[:, f:].float()
+    out.copy_(torch.nn.functional.silu(g) * u)
+
+
+def swiglu_bwd(gu, dout, dgu):
+    f = dout.shape[1]
+    g, u, d = gu[:, :f].float(), gu[:, f:].float(), dout.float()
+    sg = torch.sigmoid(g)
+    dg = d * u * sg * (1 + g * (1 - sg))
+    du = d * g * sg
+    dgu[:, :f].copy_(dg)
+    dgu[:, f:].copy_(du)

@@ -24,13 +24,16 @@ from paper_2507_10392_b200.runtime.data import synthetic_batch  # noqa: E402
 from paper_2507_10392_b200.runtime.trainer import ZorseTrainer  # noqa: E402
 
 CFG = E.ModelConfig("tiny-test", "gpt", n_layer=4, d_model=64, n_head=2, vocab=512, seq_len=64)
+LLAMA = E.ModelConfig("tiny-llama", "llama", n_layer=4, d_model=64, n_head=2, vocab=512,
+                      seq_len=64, d_ff=176)
 GB = 8
 
 
-def _setup(nodes, groups, n_mb, counts, strategy):
+def _setup(nodes, groups, n_mb, counts, strategy, cfg=None):
+    cfg = cfg or CFG
     prof = E.profile_from_json(E.profile_json(nodes))
     rt = P.fit_runtime_model(prof)
-    ctx = P.CostContext(graph=P.build_cluster_graph(prof), runtime=rt, model=CFG.model_spec(),
+    ctx = P.CostContext(graph=P.build_cluster_graph(prof), runtime=rt, model=cfg.model_spec(),
                         workload=P.WorkloadSpec(GB, CFG.seq_len))
     part = P.make_partition(ctx.graph, groups)
     plan = P.build_plan(ctx, prof, part, n_mb, counts, P.Strategy(strategy),
@@ -39,12 +42,13 @@ def _setup(nodes, groups, n_mb, counts, strategy):
     return plan, ctx
 
 
-def _oracle(steps):
-    batches = [synthetic_batch(CFG.vocab, CFG.seq_len, GB, s) for s in range(1, steps + 1)]
-    params = gpt_cpu.init_params(CFG, 1234)
+def _oracle(steps, cfg=None):
+    cfg = cfg or CFG
+    batches = [synthetic_batch(cfg.vocab, cfg.seq_len, GB, s) for s in range(1, steps + 1)]
+    params = gpt_cpu.init_params(cfg, 1234)
     state, losses, grads = {}, [], None
     for step, b in enumerate(batches, start=1):
-        loss, grads = gpt_cpu.loss_and_grads(CFG, params, b)
+        loss, grads = gpt_cpu.loss_and_grads(cfg, params, b)
         losses.append(loss)
         gpt_cpu.adamw(params, grads, state, step)
     return losses, params, grads
@@ -56,17 +60,18 @@ def _rel(a, b):
 
 def _run_rank(trainer, steps):
     trainer.exec.capture_grads = True
+    cfg = trainer.exec.cfg
     losses = []
     for s in range(1, steps + 1):
-        losses.append(trainer.step(synthetic_batch(CFG.vocab, CFG.seq_len, GB, s)))
+        losses.append(trainer.step(synthetic_batch(cfg.vocab, cfg.seq_len, GB, s)))
     ex = trainer.exec
     return {"losses": losses,
             "shards": {u: (pu.lo, pu.hi, pu.master.clone(), ex.captured[u].clone())
                        for u, pu in ex.units.items()}}
 
 
-def _check(results, steps):
-    ref_losses, ref_params, ref_grads = _oracle(steps)
+def _check(results, steps, cfg=None):
+    ref_losses, ref_params, ref_grads = _oracle(steps, cfg)
     for r in results:
         for got, want in zip(r["losses"], ref_losses):
             assert abs(got - want) / abs(want) < 1e-2, (got, want)
@@ -88,6 +93,13 @@ def test_single_rank_matches_oracle(n_mb, counts, strategy):
     plan, ctx = _setup([("n0", ["b200"])], [["n0-0"]], n_mb, counts, strategy)
     tr = ZorseTrainer(plan, ctx, CFG, _ops=cpu_ops)
     _check([_run_rank(tr, 2)], 2)
+
+
+@pytest.mark.parametrize("n_mb,counts,strategy", [(2, [2], "zorse"), (2, [4], "pp-zero3")])
+def test_single_rank_llama_matches_oracle(n_mb, counts, strategy):
+    plan, ctx = _setup([("n0", ["b200"])], [["n0-0"]], n_mb, counts, strategy, cfg=LLAMA)
+    tr = ZorseTrainer(plan, ctx, LLAMA, _ops=cpu_ops)
+    _check([_run_rank(tr, 2)], 2, LLAMA)
 
 
 def _free_port():
