@@ -308,6 +308,98 @@ class TaskGraph:
         return self.tasks
 
 
+class OneFOneBGraph(TaskGraph):
+    """1F1B microbatch schedule (BASELINE config 4) over the same plan types.
+
+    The reference has no 1F1B (SPEC.md:477 lists it as a non-goal), so this
+    schedule has no reference oracle.  It keeps the reference's task kinds,
+    keys and cost model, and uses PP_ZERO3 collective semantics — one
+    AllGather per layer per microbatch per pass — because 1F1B interleaves the
+    forward and backward of different microbatches (SURVEY §7 hard part 7);
+    the per-group AG/RS counts therefore still equal count_collectives
+    (costs.py:189-201).  Each group owns exactly one ministage (one pipeline
+    stage); its compute lane runs min(k-s-1, M) warm-up forwards, then
+    alternates one forward / one (recompute + backward), then drains.
+    """
+
+    def build(self) -> List[Task]:
+        plan, ctx = self.plan, self.ctx
+        if not plan.strategy.gathers_per_microbatch:
+            raise SimulationError("1F1B needs per-microbatch gathers (strategy pp-zero3)")
+        if any(len(g.ministage_sizes) != 1 for g in plan.groups):
+            raise SimulationError("1F1B here supports one ministage per group")
+        M, k = plan.n_microbatches, self.n
+        link: Dict[Tuple[int, str], Tuple[str, str, float]] = {}
+        for b in range(k - 1):
+            lo, hi = self.group_of(b), self.group_of(b + 1)
+            link[(b, "f")] = best_cross_link(ctx, self.ids(lo), self.ids(hi))
+            link[(b, "b")] = best_cross_link(ctx, self.ids(hi), self.ids(lo))
+        boundary_bytes = (plan.microbatch_size * ctx.workload.seq_len * ctx.model.hidden_size
+                          * ctx.model.bytes_per_element)
+        for s in range(k):
+            gi = self.group_of(s)
+            lays = self.layers(s)
+            coll = self.lanes(gi, "collective")
+            comp = self.lanes(gi, "compute")
+            warm = min(k - s - 1, M)
+            seq = [("F", m) for m in range(warm)]
+            nf, nb = warm, 0
+            while nb < M:
+                if nf < M:
+                    seq.append(("F", nf))
+                    nf += 1
+                seq.append(("B", nb))
+                nb += 1
+            fwd_t, rc_t, bwd_t = (self.compute_time(s, "fwd"), self.compute_time(s, "fwd"),
+                                  self.compute_time(s, "bwd"))
+            prev = None  # previous compute task on this stage's lane
+            for op, m in seq:
+                tag = "AGf" if op == "F" else "AGb"
+                for i, layer in enumerate(lays):
+                    deps = [(tag, s, i - 1, m)] if i > 0 else ([prev] if prev else [])
+                    self.add((tag, s, i, m), "AllGather", s, m, layer,
+                             duration=self.ag_time(s, layer), lanes=coll, deps=deps)
+                gathers = [(tag, s, i, m) for i in range(len(lays))]
+                if op == "F":
+                    deps = gathers + ([prev] if prev else [])
+                    if s > 0:
+                        deps.append(("PRf", s - 1, m))
+                    self.add(("F", s, m), "Fwd", s, m, duration=fwd_t, lanes=comp, deps=deps)
+                    prev = ("F", s, m)
+                    if s + 1 < k:
+                        src, dst, bw = link[(s, "f")]
+                        self.add(("PSf", s, m), "P2PSend", s, m, duration=boundary_bytes / bw,
+                                 lanes=((src, "p2p"),), deps=[("F", s, m)])
+                        self.add(("PRf", s, m), "P2PRecv", s + 1, m,
+                                 duration=ctx.comm.p2p_latency, lanes=((dst, "p2p"),),
+                                 deps=[("PSf", s, m)])
+                else:
+                    deps = gathers + [("F", s, m)] + ([prev] if prev else [])
+                    self.add(("RC", s, m), "Recompute", s, m, duration=rc_t, lanes=comp, deps=deps)
+                    deps = [("RC", s, m)] + ([("PRb", s, m)] if s + 1 < k else [])
+                    self.add(("B", s, m), "Bwd", s, m, duration=bwd_t, lanes=comp, deps=deps)
+                    prev = ("B", s, m)
+                    if s > 0:
+                        src, dst, bw = link[(s - 1, "b")]
+                        self.add(("PSb", s - 1, m), "P2PSend", s, m, duration=boundary_bytes / bw,
+                                 lanes=((src, "p2p"),), deps=[("B", s, m)])
+                        self.add(("PRb", s - 1, m), "P2PRecv", s - 1, m,
+                                 duration=ctx.comm.p2p_latency, lanes=((dst, "p2p"),),
+                                 deps=[("PSb", s - 1, m)])
+            for i, layer in enumerate(lays):
+                deps = [prev] + ([("RS", s, i - 1)] if i > 0 else [])
+                self.add(("RS", s, i), "ReduceScatter", s, -1, layer,
+                         duration=self.rs_time(s, layer), lanes=coll, deps=deps)
+            local = sum(ctx.model.params_of(layer) for layer in lays) / plan.groups[gi].d_dp
+            self.add(("OPT", s), "OptimStep", s, duration=local * ctx.optim_update_per_param,
+                     lanes=comp, deps=[("RS", s, i) for i in range(len(lays))])
+        for t in self.tasks:
+            for dep in t.deps:
+                if dep not in self.by_key:
+                    raise SimulationError(f"task {t.key} depends on unknown {dep}")
+        return self.tasks
+
+
 def list_schedule(tasks: Sequence[Task], plan: TrainingPlan) -> List[Event]:
     """Greedy list scheduling: repeatedly start the ready task with the least
     (earliest start, priority); a task occupies all its lanes."""
@@ -381,16 +473,32 @@ class Schedule:
     def stream_for(self, dev_id: str) -> List[Event]:
         """Events device ``dev_id`` executes, in global order.
 
-        Every task is tagged with the group of its stage (simulate.py:236), so
-        P2PSend belongs to the sending group and P2PRecv to the receiving one.
-        On B200 a boundary transfer is many-to-many — every member of the
-        sending group holds part of the microbatch and every member of the
-        receiving group needs part of it — so all members of the group execute
-        the event, not only the single best link the reference charges.
+        Every task is tagged with the group of its stage (simulate.py:236).  On
+        B200 a boundary transfer is many-to-many — every member of the sending
+        group holds part of the microbatch and every member of the receiving
+        group needs part of it — and it is ONE global operation: the receiving
+        group posts its receives at the P2PSend event (its P2PRecv event only
+        marks arrival).  With every NCCL operation (group collective or
+        transfer) at a single position of one global order, the earliest
+        unfinished operation always has all its participants' earlier work
+        done, so blocking sends can never form a cycle.
         """
         gi = self.group_of_device(dev_id)
-        return [e for e in self.events if e.group == gi]
+        order = self.plan.global_order()
+        out = []
+        for e in self.events:
+            if e.group == gi:
+                out.append(e)
+            elif e.kind == "P2PSend":
+                b = e.key[1]  # boundary between global stages b and b+1
+                peer_stage = b + 1 if e.key[0] == "PSf" else b
+                if order[peer_stage][0] == gi:
+                    out.append(e)  # receiving side of the transfer
+        return out
 
 
-def build_schedule(ctx: CostContext, plan: TrainingPlan) -> Schedule:
-    return Schedule(plan=plan, events=list_schedule(TaskGraph(ctx, plan).build(), plan))
+def build_schedule(ctx: CostContext, plan: TrainingPlan, kind: str = "gpipe") -> Schedule:
+    """kind "gpipe": the reference's ministage-interleaved GPipe schedule
+    (simulate.py:256-558, bit-exact); "1f1b": OneFOneBGraph."""
+    graph = {"gpipe": TaskGraph, "1f1b": OneFOneBGraph}[kind](ctx, plan)
+    return Schedule(plan=plan, events=list_schedule(graph.build(), plan))

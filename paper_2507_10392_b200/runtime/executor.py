@@ -87,7 +87,8 @@ class StageExecutor:
 
     def __init__(self, plan: TrainingPlan, ctx: CostContext, cfg: ModelConfig, dev_id: str,
                  rank_of: Dict[str, int], world_comm, group_comm, ops, device,
-                 seed: int = 1234, adam: AdamConfig = AdamConfig(), init_device="cpu"):
+                 seed: int = 1234, adam: AdamConfig = AdamConfig(), init_device="cpu",
+                 schedule: str = "gpipe"):
         if plan.routing is None:
             raise ValueError("plan has no routing; attach it (configure.attach_routing) first")
         if ctx.model.num_layers != cfg.n_layer:
@@ -97,7 +98,7 @@ class StageExecutor:
         self.world, self.group_comm, self.ops, self.device = world_comm, group_comm, ops, device
         self.adam = adam
         self.model = make_model_ops(cfg, ops)
-        self.schedule = build_schedule(ctx, plan)
+        self.schedule = build_schedule(ctx, plan, schedule)
         self.events: List[Event] = self.schedule.stream_for(dev_id)
         self.order = plan.global_order()
         self.ranges = plan.stage_layer_ranges()
@@ -365,24 +366,23 @@ class StageExecutor:
             self.model.embed_bwd(self.units["embed"].g, self.tokens[m], self.gbuf[(lo, m)][:n], n)
 
     def _on_send(self, ev: Event) -> None:
+        """One global transfer: the sending group sends, the receiving group
+        receives (see Schedule.stream_for)."""
         kind, b, m = ev.key
-        if kind == "PSf":
-            buf = self.act[(self.ranges[b][1], m)]
-            lst = self.transfers[("f", b, m)]
-        else:  # PSb: gradient of stage b+1's input goes to group of stage b
-            buf = self.gbuf[(self.ranges[b + 1][0], m)]
-            lst = self.transfers[("b", b, m)]
-        self.world.p2p([(peer, buf[lo:hi], True) for peer, lo, hi, snd in lst if snd])
+        direction = "f" if kind == "PSf" else "b"
+        lst = self.transfers[(direction, b, m)]
+        if ev.group == self.gi:  # sender
+            # PSf: output of stage b; PSb: gradient of stage b+1's input
+            buf = self.act[(self.ranges[b][1], m)] if kind == "PSf" else \
+                self.gbuf[(self.ranges[b + 1][0], m)]
+            self.world.p2p([(peer, buf[lo:hi], True) for peer, lo, hi, snd in lst if snd])
+        else:                    # receiver
+            buf = self.act[(self.ranges[b + 1][0], m)] if kind == "PSf" else \
+                self.gbuf[(self.ranges[b][1], m)]
+            self.world.p2p([(peer, buf[lo:hi], False) for peer, lo, hi, snd in lst if not snd])
 
     def _on_recv(self, ev: Event) -> None:
-        kind, b, m = ev.key
-        if kind == "PRf":
-            buf = self.act[(self.ranges[b + 1][0], m)]
-            lst = self.transfers[("f", b, m)]
-        else:  # PRb
-            buf = self.gbuf[(self.ranges[b][1], m)]
-            lst = self.transfers[("b", b, m)]
-        self.world.p2p([(peer, buf[lo:hi], False) for peer, lo, hi, snd in lst if not snd])
+        return None  # data was received at the matching P2PSend event
 
     def _noop(self, ev: Event) -> None:
         return None

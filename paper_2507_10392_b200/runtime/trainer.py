@@ -26,7 +26,7 @@ class ZorseTrainer:
     def __init__(self, plan: TrainingPlan, ctx: CostContext, cfg: ModelConfig, *,
                  world_rank: int = 0, world_size: int = 1, seed: int = 1234,
                  adam: AdamConfig = AdamConfig(), init_device: str = "cpu",
-                 _ops=None, _comms=None, _device=None):
+                 schedule: str = "gpipe", _ops=None, _comms=None, _device=None):
         devices = list(ctx.graph.vertices)
         if len(devices) != world_size:
             raise ValueError(f"cluster profile has {len(devices)} devices but world size is "
@@ -55,7 +55,8 @@ class ZorseTrainer:
         self.ops = ops
         self.device = device
         self.exec = StageExecutor(plan, ctx, cfg, self.dev_id, self.rank_of, world, group, ops,
-                                  device, seed=seed, adam=adam, init_device=init_device)
+                                  device, seed=seed, adam=adam, init_device=init_device,
+                                  schedule=schedule)
         self.loss_buf = torch.zeros(1, device=device, dtype=torch.float32)
 
         self.graph = None

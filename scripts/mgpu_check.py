@@ -22,6 +22,10 @@ from paper_2507_10392_b200.runtime.data import synthetic_batch
 from paper_2507_10392_b200.runtime.trainer import ZorseTrainer
 
 CFG = E.ModelConfig("mgpu-gpt", "gpt", n_layer=4, d_model=256, n_head=4, vocab=2048, seq_len=128)
+LLAMA = E.ModelConfig("mgpu-llama", "llama", n_layer=4, d_model=512, n_head=4, vocab=4096,
+                      seq_len=256, d_ff=1376)
+XLW = E.ModelConfig("mgpu-xl-width", "gpt", n_layer=4, d_model=1600, n_head=25, vocab=4096,
+                    seq_len=256)
 LAYOUTS = {
     # name: (nodes, groups, n_microbatches, ministage counts, strategy, global batch)
     "dp2": ([("n0", ["b200", "b200h"])], [["n0-0", "n0-1"]], 2, [2], "zorse", 8),
@@ -32,12 +36,21 @@ LAYOUTS = {
               [2], "pp-zero3", 12),
     "pp2x2": ([("n0", ["b200", "b200h"]), ("n1", ["b200", "b200"])],
               [["n0-0", "n0-1"], ["n1-0", "n1-1"]], 2, [2, 2], "zorse", 8),
+    # Llama, 1F1B, 2 stages x 2-way ZeRO-3 DP (config 4 in miniature)
+    "llama1f1b2x2": ([("n0", ["b200", "b200"]), ("n1", ["b200", "b200"])],
+                     [["n0-0", "n0-1"], ["n1-0", "n1-1"]], 4, [1, 1], "pp-zero3", 8),
+    # GPT-2-XL widths, asymmetric 1 + 3 stages (config 3 in miniature)
+    "xl1+3": ([("n0", ["b200"]), ("n1", ["b200", "b200", "b200h"])],
+              [["n0-0"], ["n1-0", "n1-1", "n1-2"]], 4, [1, 1], "zorse", 8),
 }
+CFGS = {"llama1f1b2x2": LLAMA, "xl1+3": XLW}
+SCHED = {"llama1f1b2x2": "1f1b"}
 
 
 def main():
     name = sys.argv[1]
     nodes, groups, M, counts, strategy, gb = LAYOUTS[name]
+    CFG = CFGS.get(name, globals()["CFG"])
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
@@ -49,7 +62,8 @@ def main():
     plan = P.build_plan(ctx, prof, P.make_partition(ctx.graph, groups), M, counts,
                         P.Strategy(strategy), P.cluster_fingerprint(prof), "transformer")
     P.attach_routing(plan, rt, "transformer")
-    tr = ZorseTrainer(plan, ctx, CFG, world_rank=rank, world_size=world)
+    tr = ZorseTrainer(plan, ctx, CFG, world_rank=rank, world_size=world,
+                      schedule=SCHED.get(name, "gpipe"))
     tr.exec.capture_grads = True
     params = gpt_cpu.init_params(CFG, 1234)
     state = {}

@@ -108,13 +108,13 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, spec, q):
+def _worker(rank, world, port, spec, q, cfg=None, schedule="gpipe"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        plan, ctx = _setup(*spec)
+        plan, ctx = _setup(*spec, cfg=cfg)
         def comms(groups_ranks):
             world_c = cpu_ops.GlooComm(list(range(world)), rank)
             group = None
@@ -123,8 +123,8 @@ def _worker(rank, world, port, spec, q):
                 if rank in ranks and len(ranks) > 1:
                     group = c
             return world_c, group
-        tr = ZorseTrainer(plan, ctx, CFG, world_rank=rank, world_size=world, _ops=cpu_ops,
-                          _comms=comms)
+        tr = ZorseTrainer(plan, ctx, cfg or CFG, world_rank=rank, world_size=world, _ops=cpu_ops,
+                          _comms=comms, schedule=schedule)
         res = _run_rank(tr, 2)
         # ship plain numpy (tensors in a Queue are shared by fd and die with the worker)
         res["shards"] = {u: (lo, hi, m.numpy(), g.numpy()) for u, (lo, hi, m, g) in res["shards"].items()}
@@ -145,11 +145,15 @@ def _worker(rank, world, port, spec, q):
     ([("n0", ["b200", "b200", "b200h"])], [["n0-0", "n0-1", "n0-2"]], 2, [2], "pp-zero3"),
 ], ids=["2stage", "interleaved", "dp3-zero3"])
 def test_three_ranks_gloo_matches_oracle(spec):
-    world = 3
+    _run_gloo(spec, 3)
+
+
+def _run_gloo(spec, world, cfg=None, schedule="gpipe"):
     ctx_mp = mp.get_context("spawn")
     q = ctx_mp.Queue()
     port = _free_port()
-    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, spec, q)) for r in range(world)]
+    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, spec, q, cfg, schedule))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = {}
@@ -163,4 +167,33 @@ def test_three_ranks_gloo_matches_oracle(spec):
     for r in results.values():
         r["shards"] = {u: (lo, hi, torch.from_numpy(m), torch.from_numpy(g))
                        for u, (lo, hi, m, g) in r["shards"].items()}
-    _check(list(results.values()), 2)
+    _check(list(results.values()), 2, cfg)
+
+
+def test_1f1b_three_stages_llama_gloo():
+    """BASELINE config 4 shape in miniature: Llama, 1F1B, 3 pipeline stages."""
+    spec = ([("n0", ["b200"]), ("n1", ["b200"]), ("n2", ["b200h"])],
+            [["n0-0"], ["n1-0"], ["n2-0"]], 4, [1, 1, 1], "pp-zero3")
+    _run_gloo(spec, 3, LLAMA, "1f1b")
+
+
+def test_1f1b_two_stages_with_dp_gloo():
+    spec = ([("n0", ["b200", "b200h"]), ("n1", ["b200"])], [["n0-0", "n0-1"], ["n1-0"]], 4,
+            [1, 1], "pp-zero3")
+    _run_gloo(spec, 3, CFG, "1f1b")
+
+
+def test_1f1b_schedule_shape():
+    plan, ctx = _setup([("n0", ["b200"]), ("n1", ["b200"]), ("n2", ["b200"])],
+                       [["n0-0"], ["n1-0"], ["n2-0"]], 4, [1, 1, 1], "pp-zero3")
+    sched = P.build_schedule(ctx, plan, "1f1b")
+    for gi in range(3):
+        comp = [(e.kind[0], e.microbatch) for e in sched.stream_for(plan.groups[gi].device_ids[0])
+                if e.kind in ("Fwd", "Bwd") and e.group == gi]
+        s = plan.global_order().index((gi, 0))
+        warm = min(3 - s - 1, 4)
+        assert [c for c in comp[:warm]] == [("F", m) for m in range(warm)]
+        assert comp[warm:warm + 2] == [("F", warm), ("B", 0)] or warm == 4
+        counts = sched.collective_counts()[gi]
+        assert counts == {"allgather": 2 * plan.groups[gi].layers_assigned * 4,
+                          "reduce_scatter": plan.groups[gi].layers_assigned}

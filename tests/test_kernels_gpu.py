@@ -151,3 +151,75 @@ def test_adamw_matches_torch(cuda):
     assert (p - ref.detach()).abs().max().item() < 1e-6
     assert rel(pb, ref.detach()) < 1e-2
     assert abs(ss.item() - sum(((g * s) ** 2).sum().item() for s in (1, 2, 3))) / ss.item() < 1e-4
+
+
+@pytest.mark.parametrize("rows,d", [(300, 512), (64, 4096), (17, 5120)])
+def test_rmsnorm(cuda, rows, d):
+    torch.manual_seed(6)
+    x = torch.randn(rows, d, device="cuda").bfloat16()
+    w = (1 + 0.1 * torch.randn(d, device="cuda")).bfloat16()
+    y = torch.empty_like(x)
+    rstd = torch.empty(rows, device="cuda")
+    K.rmsnorm_fwd(x, w, y, rstd)
+    xf = x.float().requires_grad_()
+    wf = w.float().requires_grad_()
+    ref = xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-5) * wf
+    assert rel(y, ref) < 1e-2
+    dy = torch.randn(rows, d, device="cuda").bfloat16()
+    dres = torch.randn(rows, d, device="cuda").bfloat16()
+    ref.backward(dy.float())
+    dx = torch.empty_like(x)
+    dw = torch.zeros(d, device="cuda")
+    K.rmsnorm_bwd(dy, x, w, rstd, dx, dw, dx_accum=dres)
+    torch.cuda.synchronize()
+    assert rel(dx, xf.grad + dres.float()) < 1e-2
+    assert rel(dw, wf.grad) < 1e-3
+
+
+def test_rope_roundtrip_and_reference(cuda):
+    torch.manual_seed(7)
+    n, S, H, D = 2, 128, 4, 128
+    qkv = torch.randn(n * S, 3 * H * D, device="cuda").bfloat16()
+    orig = qkv.clone()
+    K.rope(qkv, S, H, D)
+    half = D // 2
+    inv = 10000.0 ** (-(2.0 * torch.arange(half, device="cuda").float()) / D)
+    ang = (torch.arange(n * S, device="cuda") % S).float()[:, None] * inv[None]
+    x = orig[:, :2 * H * D].float().view(n * S, 2 * H, D)
+    a, b = x[..., :half], x[..., half:]
+    sn, cs = torch.sin(ang)[:, None], torch.cos(ang)[:, None]
+    ref = torch.cat([a * cs - b * sn, a * sn + b * cs], -1).view(n * S, -1)
+    torch.cuda.synchronize()
+    assert rel(qkv[:, :2 * H * D], ref) < 1e-2
+    assert torch.equal(qkv[:, 2 * H * D:], orig[:, 2 * H * D:])  # v untouched
+    K.rope(qkv, S, H, D, inverse=True)
+    torch.cuda.synchronize()
+    assert rel(qkv, orig) < 1e-2
+
+
+def test_swiglu(cuda):
+    torch.manual_seed(8)
+    rows, f = 257, 1376
+    gu = torch.randn(rows, 2 * f, device="cuda").bfloat16()
+    out = torch.empty(rows, f, device="cuda", dtype=torch.bfloat16)
+    K.swiglu_fwd(gu, out)
+    g = gu.float().requires_grad_()
+    ref = torch.nn.functional.silu(g[:, :f]) * g[:, f:]
+    assert rel(out, ref) < 1e-2
+    d = torch.randn(rows, f, device="cuda").bfloat16()
+    ref.backward(d.float())
+    dgu = gu.clone()
+    K.swiglu_bwd(dgu, d, dgu)  # in place
+    torch.cuda.synchronize()
+    assert rel(dgu, g.grad) < 1e-2
+
+
+def test_gemm_resid_epilogue(cuda):
+    torch.manual_seed(9)
+    a = torch.randn(384, 512, device="cuda").bfloat16()
+    b = (0.05 * torch.randn(640, 512, device="cuda")).bfloat16()
+    r = torch.randn(384, 640, device="cuda").bfloat16()
+    out = torch.empty(384, 640, device="cuda", dtype=torch.bfloat16)
+    K.gemm(a, b, out, epilogue=K.EPI_RESID, resid=r)
+    torch.cuda.synchronize()
+    assert rel(out, a.float() @ b.float().t() + r.float()) < 1e-2

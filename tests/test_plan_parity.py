@@ -109,12 +109,21 @@ def test_device_streams_partition_the_events():
     prof, ctx = _ctx(case)
     plan = P.TrainingPlan.from_json_dict(json.loads(case["plan_json"]), prof)
     sched = P.build_schedule(ctx, plan)
+    order = plan.global_order()
+    seen = set()
     for gi, g in enumerate(plan.groups):
         streams = [sched.stream_for(d) for d in g.device_ids]
         assert all(s == streams[0] for s in streams)  # group members run one program
-        assert all(e.group == gi for e in streams[0])
-    total = sum(len(sched.stream_for(g.device_ids[0])) for g in plan.groups)
-    assert total == len(sched.events)
+        for e in streams[0]:
+            if e.group != gi:  # only the receiving side of a boundary transfer
+                peer = e.key[1] + 1 if e.key[0] == "PSf" else e.key[1]
+                assert e.kind == "P2PSend" and order[peer][0] == gi
+        seen |= {e.key for e in streams[0]}
+        # streams keep the global order
+        pos = {e.key: i for i, e in enumerate(sched.events)}
+        idx = [pos[e.key] for e in streams[0]]
+        assert idx == sorted(idx)
+    assert seen == {e.key for e in sched.events}
 
 
 @pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "plan_training"],

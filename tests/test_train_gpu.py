@@ -34,6 +34,8 @@ def _rel(a, b):
     (E.TINY_GPT, 8, 2, [1], "zorse"),                  # BASELINE config 1 model
     (E.TINY_GPT, 8, 2, [4], "pp-zero3"),
     (E.ModelConfig("mid", "gpt", 2, 768, 12, 4096, 1024), 2, 1, [2], "zorse"),  # GPT-2 widths
+    (E.ModelConfig("llama-tiny", "llama", 2, 512, 4, 4096, 256, d_ff=1376), 4, 2, [2], "zorse"),
+    (E.ModelConfig("llama-hd128", "llama", 2, 1024, 8, 4096, 512, d_ff=2752), 2, 1, [1], "pp-zero3"),
 ])
 def test_training_steps_match_oracle(cuda, cfg, gb, n_mb, counts, strategy):
     plan, ctx = _setup(cfg, gb, n_mb, counts, strategy)
