@@ -545,6 +545,14 @@ static int run_bwd(const void* qkv, const void* out, const void* dout, const voi
 }
 
 }  // namespace attn
+
+int launch_attn_delta(const void* o, const void* dout, void* delta, int T, int S, int H, int D,
+                      cudaStream_t s) {
+  attn::delta_kernel<<<(T * H * 32 + 255) / 256, 256, 0, s>>>(
+      (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, (float*)delta, T, S, H, D);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "attn delta");
+}
 }  // namespace zb
 
 using namespace zb;

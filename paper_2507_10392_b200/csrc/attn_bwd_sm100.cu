@@ -1,0 +1,481 @@
+// Causal flash-attention backward on tcgen05 / TMEM / TMA (sm_100a).
+//
+// Two kernels, no atomics (deterministic):
+//   dq:   one CTA per 128-query tile; per 128-key block j (j <= tile):
+//           S = Q K_j^T, dP = dO V_j^T           (tensor core -> TMEM)
+//           dS = P * (dP - delta),  P = exp(S*scale - lse)   (one thread per query row)
+//           dQ += dS K_j                          (dS from smem, K_j reused as MN-major B)
+//   dkdv: one CTA per 128-key tile; per 128-query tile i (i >= tile):
+//           S^T = K Q_i^T, dP^T = V dO_i^T        (tensor core -> TMEM)
+//           P^T, dS^T                             (one thread per key row)
+//           dV += P^T dO_i, dK += dS^T Q_i        (Q_i / dO_i reused as MN-major B)
+// The same smem tile serves as a K-major operand (rows = tokens) and as an
+// MN-major operand (K = tokens) — a [128 rows][64 cols] SW128 tile is both
+// canonical layouts — so nothing is transposed or loaded twice.
+// Warp roles: 0 TMA, 1 MMA (one thread), 2 TMEM alloc, 4..7 math (thread = row).
+#include "common.cuh"
+#include "zb_internal.h"
+
+#include <cstdlib>
+
+namespace zb {
+namespace fab {
+
+constexpr int T = 128;  // tile rows (queries or keys)
+constexpr int kThreads = 256;
+constexpr float LOG2E = 1.4426950408889634f;
+
+ZB_DEVICE uint64_t desc_k(uint32_t base, int kk) {  // K-major [128 rows][64*n] tile
+  return umma_desc_sw128(base + (kk >> 2) * T * 128 + (kk & 3) * 32, 16, 1024);
+}
+ZB_DEVICE uint64_t desc_mn(uint32_t base, int kk) {  // same tile as MN-major, K = rows
+  return umma_desc_sw128(base + kk * 2048, T * 128, 1024);
+}
+// Write 32 consecutive bf16 values (columns c0..c0+31) of row r of a K-major SW128
+// [128 rows][128 cols] tile (two 64-col blocks of 16 KB).
+ZB_DEVICE void st_row32(uint8_t* tile, int r, int c0, const float* v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int ch = (c0 >> 3) + q;
+    uint4 pk;
+    pk.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+    pk.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+    pk.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+    pk.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+    *reinterpret_cast<uint4*>(tile + (ch >> 3) * (T * 128) + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) = pk;
+  }
+}
+
+// ------------------------------------------------------------------ dQ
+template <int D>
+struct DqSmem {
+  static constexpr int NST = 2;                  // K/V stages (224 KB at D = 128)
+  static constexpr int DSB = (D == 64) ? 2 : 1;
+  static constexpr int TILE = T * D * 2;
+  static constexpr int OFF_Q = 0, OFF_DO = TILE;
+  static constexpr int OFF_K = 2 * TILE;
+  static constexpr int OFF_V = OFF_K + NST * TILE;
+  static constexpr int OFF_DS = OFF_V + NST * TILE;
+  static constexpr int OFF_BAR = OFF_DS + DSB * T * T * 2;
+  static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    dq_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+              const float* __restrict__ lse, const float* __restrict__ delta,
+              __nv_bfloat16* __restrict__ dqkv, int S, int H, int ld, float scale) {
+  using L = DqSmem<D>;
+  constexpr int NST = L::NST, DSB = L::DSB;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t* qo_full = bar;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* s_empty = bar + 6;
+  uint64_t* ds_full = bar + 7;   // [2]
+  uint64_t* ds_empty = bar + 9;  // [2]
+  uint64_t* dq_done = bar + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = S / T - 1 - blockIdx.x;
+  const int h = blockIdx.y, b = blockIdx.z, HD = H * D, row0 = b * S, nblk = qt + 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+    mbar_init(qo_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&ds_full[i], 4);
+      mbar_init(&ds_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, 4);
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(qo_full, 2 * L::TILE);
+#pragma unroll
+      for (int kc = 0; kc < D / 64; ++kc) {
+        tma_load_2d(sm + L::OFF_Q + kc * T * 128, &tm_qkv, qo_full, h * D + kc * 64, row0 + qt * T);
+        tma_load_2d(sm + L::OFF_DO + kc * T * 128, &tm_do, qo_full, h * D + kc * 64, row0 + qt * T);
+      }
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % NST;
+        mbar_wait(&kv_empty[st], ((j / NST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * L::TILE);
+#pragma unroll
+        for (int kc = 0; kc < D / 64; ++kc) {
+          tma_load_2d(sm + L::OFF_K + st * L::TILE + kc * T * 128, &tm_qkv, &kv_full[st],
+                      HD + h * D + kc * 64, row0 + j * T);
+          tma_load_2d(sm + L::OFF_V + st * L::TILE + kc * T * 128, &tm_qkv, &kv_full[st],
+                      2 * HD + h * D + kc * 64, row0 + j * T);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(T, T, 0, 0);
+      constexpr uint32_t idesc_q = umma_idesc_bf16(T, D, 0, 1);
+      const uint32_t q_base = smem_u32(sm + L::OFF_Q), do_base = smem_u32(sm + L::OFF_DO);
+      auto issue_sd = [&](int j) {
+        const int st = j % NST;
+        mbar_wait(&kv_full[st], (j / NST) & 1);
+        mbar_wait(s_empty, (j & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sm + L::OFF_K + st * L::TILE);
+        const uint32_t v_base = smem_u32(sm + L::OFF_V + st * L::TILE);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          mma_bf16_ss(t_s, desc_k(q_base, kk), desc_k(k_base, kk), idesc_s, kk > 0);
+          mma_bf16_ss(t_dp, desc_k(do_base, kk), desc_k(v_base, kk), idesc_s, kk > 0);
+        }
+        mma_commit(s_full);
+      };
+      mbar_wait(qo_full, 0);
+      tc_fence_after();
+      issue_sd(0);
+      for (int j = 0; j < nblk; ++j) {
+        // With one K/V stage, S_{j+1} must wait for dQ_j to free the stage.
+        if (NST > 1 && j + 1 < nblk) issue_sd(j + 1);
+        const int st = j % NST, db = j % DSB;
+        mbar_wait(&ds_full[db], (j / DSB) & 1);
+        tc_fence_after();
+        const uint32_t ds_base = smem_u32(sm + L::OFF_DS + db * T * T * 2);
+        const uint32_t k_base = smem_u32(sm + L::OFF_K + st * L::TILE);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)
+          mma_bf16_ss(t_dq, desc_k(ds_base, kk), desc_mn(k_base, kk), idesc_q, (j > 0 || kk > 0));
+        mma_commit(&kv_empty[st]);
+        mma_commit(&ds_empty[db]);
+        if (NST == 1 && j + 1 < nblk) issue_sd(j + 1);
+      }
+      mma_commit(dq_done);
+    }
+  } else if (warp >= 4) {
+    const int wq = warp - 4, r = wq * 32 + lane, q = qt * T + r;
+    const uint32_t lo = (uint32_t)(wq * 32) << 16;
+    const float sl2 = scale * LOG2E;
+    const size_t vrow = ((size_t)b * H + h) * S + q;
+    const float L2 = lse[vrow] * LOG2E, Dl = delta[vrow];
+    for (int j = 0; j < nblk; ++j) {
+      const int db = j % DSB;
+      mbar_wait(&ds_empty[db], ((j / DSB) & 1) ^ 1);
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      uint8_t* ds_tile = sm + L::OFF_DS + db * T * T * 2;
+#pragma unroll 1
+      for (int c = 0; c < T / 32; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(t_s + lo + c * 32, sv);
+        tmem_ld_32x32b_x32(t_dp + lo + c * 32, dv);
+        tmem_ld_wait();
+        float ds[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float p = exp2_fast(fmaf(__uint_as_float(sv[i]), sl2, -L2));
+          if (j == qt && c * 32 + i > r) p = 0.f;
+          ds[i] = p * (__uint_as_float(dv[i]) - Dl);
+        }
+        st_row32(ds_tile, r, c * 32, ds);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ds_full[db]);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    __nv_bfloat16* out = dqkv + ((size_t)row0 + q) * ld + h * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(t_dq + lo + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 pk;
+        pk.x = pack_bf16(__uint_as_float(v[i]) * scale, __uint_as_float(v[i + 1]) * scale);
+        pk.y = pack_bf16(__uint_as_float(v[i + 2]) * scale, __uint_as_float(v[i + 3]) * scale);
+        pk.z = pack_bf16(__uint_as_float(v[i + 4]) * scale, __uint_as_float(v[i + 5]) * scale);
+        pk.w = pack_bf16(__uint_as_float(v[i + 6]) * scale, __uint_as_float(v[i + 7]) * scale);
+        *reinterpret_cast<uint4*>(out + c * 32 + i) = pk;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+// ------------------------------------------------------------------ dK, dV
+template <int D>
+struct DkvSmem {
+  static constexpr int NST = (D == 64) ? 2 : 1;
+  static constexpr int TILE = T * D * 2;
+  static constexpr int OFF_K = 0, OFF_V = TILE;
+  static constexpr int OFF_Q = 2 * TILE;              // [NST] Q_i
+  static constexpr int OFF_DO = OFF_Q + NST * TILE;   // [NST] dO_i
+  static constexpr int OFF_PT = OFF_DO + NST * TILE;  // P^T  [128 keys][128 queries]
+  static constexpr int OFF_DST = OFF_PT + T * T * 2;  // dS^T
+  static constexpr int OFF_VEC = OFF_DST + T * T * 2; // [2][2][128] fp32 lse*log2e, delta
+  static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * T * 4;
+  static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    dkdv_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                const float* __restrict__ lse, const float* __restrict__ delta,
+                __nv_bfloat16* __restrict__ dqkv, int S, int H, int ld, float scale) {
+  using L = DkvSmem<D>;
+  constexpr int NST = L::NST;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t* kv_full = bar;
+  uint64_t* qo_full = bar + 1;   // [2]
+  uint64_t* qo_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* s_empty = bar + 6;
+  uint64_t* p_full = bar + 7;
+  uint64_t* p_empty = bar + 8;
+  uint64_t* done = bar + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+  float* vec = reinterpret_cast<float*>(sm + L::OFF_VEC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kt = blockIdx.x;  // early key tiles see the most query tiles: launch first
+  const int nqt = S / T;
+  const int h = blockIdx.y, b = blockIdx.z, HD = H * D, row0 = b * S;
+  const int ntile = nqt - kt;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qo_full[i], 1);
+      mbar_init(&qo_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, 4);
+    mbar_init(p_full, 4);
+    mbar_init(p_empty, 1);
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * L::TILE);
+#pragma unroll
+      for (int kc = 0; kc < D / 64; ++kc) {
+        tma_load_2d(sm + L::OFF_K + kc * T * 128, &tm_qkv, kv_full, HD + h * D + kc * 64, row0 + kt * T);
+        tma_load_2d(sm + L::OFF_V + kc * T * 128, &tm_qkv, kv_full, 2 * HD + h * D + kc * 64,
+                    row0 + kt * T);
+      }
+      for (int i = 0; i < ntile; ++i) {
+        const int st = i % NST, qt = kt + i;
+        mbar_wait(&qo_empty[st], ((i / NST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qo_full[st], 2 * L::TILE);
+#pragma unroll
+        for (int kc = 0; kc < D / 64; ++kc) {
+          tma_load_2d(sm + L::OFF_Q + st * L::TILE + kc * T * 128, &tm_qkv, &qo_full[st],
+                      h * D + kc * 64, row0 + qt * T);
+          tma_load_2d(sm + L::OFF_DO + st * L::TILE + kc * T * 128, &tm_do, &qo_full[st],
+                      h * D + kc * 64, row0 + qt * T);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(T, T, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(T, D, 0, 1);
+      const uint32_t k_base = smem_u32(sm + L::OFF_K), v_base = smem_u32(sm + L::OFF_V);
+      const uint32_t pt_base = smem_u32(sm + L::OFF_PT), dst_base = smem_u32(sm + L::OFF_DST);
+      auto issue_s = [&](int i) {
+        const int st = i % NST;
+        mbar_wait(&qo_full[st], (i / NST) & 1);
+        mbar_wait(s_empty, (i & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sm + L::OFF_Q + st * L::TILE);
+        const uint32_t do_base = smem_u32(sm + L::OFF_DO + st * L::TILE);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          mma_bf16_ss(t_st, desc_k(k_base, kk), desc_k(q_base, kk), idesc_s, kk > 0);
+          mma_bf16_ss(t_dpt, desc_k(v_base, kk), desc_k(do_base, kk), idesc_s, kk > 0);
+        }
+        mma_commit(s_full);
+      };
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      issue_s(0);
+      for (int i = 0; i < ntile; ++i) {
+        if (NST > 1 && i + 1 < ntile) issue_s(i + 1);  // one stage: see dq_kernel
+        const int st = i % NST;
+        mbar_wait(p_full, i & 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sm + L::OFF_Q + st * L::TILE);
+        const uint32_t do_base = smem_u32(sm + L::OFF_DO + st * L::TILE);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk) {
+          mma_bf16_ss(t_dv, desc_k(pt_base, kk), desc_mn(do_base, kk), idesc_o, (i > 0 || kk > 0));
+          mma_bf16_ss(t_dk, desc_k(dst_base, kk), desc_mn(q_base, kk), idesc_o, (i > 0 || kk > 0));
+        }
+        mma_commit(&qo_empty[st]);
+        mma_commit(p_empty);
+        if (NST == 1 && i + 1 < ntile) issue_s(i + 1);
+      }
+      mma_commit(done);
+    }
+  } else if (warp >= 4) {
+    const int wq = warp - 4, r = wq * 32 + lane;
+    const uint32_t lo = (uint32_t)(wq * 32) << 16;
+    const float sl2 = scale * LOG2E;
+    for (int i = 0; i < ntile; ++i) {
+      const int qt = kt + i;
+      float* vl = vec + (i & 1) * 2 * T;
+      float* vd = vl + T;
+      const size_t vrow = ((size_t)b * H + h) * S + qt * T + r;
+      vl[r] = lse[vrow] * LOG2E;
+      vd[r] = delta[vrow];
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the four math warps
+      mbar_wait(s_full, i & 1);
+      mbar_wait(p_empty, (i & 1) ^ 1);
+      tc_fence_after();
+      uint8_t* pt = sm + L::OFF_PT;
+      uint8_t* dst = sm + L::OFF_DST;
+#pragma unroll 1
+      for (int c = 0; c < T / 32; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(t_st + lo + c * 32, sv);
+        tmem_ld_32x32b_x32(t_dpt + lo + c * 32, dv);
+        tmem_ld_wait();
+        float p[32], ds[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int qq = c * 32 + t;
+          float x = exp2_fast(fmaf(__uint_as_float(sv[t]), sl2, -vl[qq]));
+          if (qt == kt && qq < r) x = 0.f;
+          p[t] = x;
+          ds[t] = x * (__uint_as_float(dv[t]) - vd[qq]);
+        }
+        st_row32(pt, r, c * 32, p);
+        st_row32(dst, r, c * 32, ds);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int k = kt * T + r;
+    __nv_bfloat16* dk_row = dqkv + ((size_t)row0 + k) * ld + HD + h * D;
+    __nv_bfloat16* dv_row = dk_row + HD;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32], w[32];
+      tmem_ld_32x32b_x32(t_dk + lo + c * 32, v);
+      tmem_ld_32x32b_x32(t_dv + lo + c * 32, w);
+      tmem_ld_wait();
+#pragma unroll
+      for (int t = 0; t < 32; t += 8) {
+        uint4 a, bb;
+        a.x = pack_bf16(__uint_as_float(v[t]) * scale, __uint_as_float(v[t + 1]) * scale);
+        a.y = pack_bf16(__uint_as_float(v[t + 2]) * scale, __uint_as_float(v[t + 3]) * scale);
+        a.z = pack_bf16(__uint_as_float(v[t + 4]) * scale, __uint_as_float(v[t + 5]) * scale);
+        a.w = pack_bf16(__uint_as_float(v[t + 6]) * scale, __uint_as_float(v[t + 7]) * scale);
+        bb.x = pack_bf16(__uint_as_float(w[t]), __uint_as_float(w[t + 1]));
+        bb.y = pack_bf16(__uint_as_float(w[t + 2]), __uint_as_float(w[t + 3]));
+        bb.z = pack_bf16(__uint_as_float(w[t + 4]), __uint_as_float(w[t + 5]));
+        bb.w = pack_bf16(__uint_as_float(w[t + 6]), __uint_as_float(w[t + 7]));
+        *reinterpret_cast<uint4*>(dk_row + c * 32 + t) = a;
+        *reinterpret_cast<uint4*>(dv_row + c * 32 + t) = bb;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+template <int D>
+static int run(const void* qkv, const void* out, const void* dout, const void* lse, void* dqkv,
+               void* delta, int n_seq, int S, int H, int ld, float scale, cudaStream_t s) {
+  const int Tn = n_seq * S;
+  if (int rc = launch_attn_delta(out, dout, delta, Tn, S, H, D, s)) return rc;
+  CUtensorMap mq, mo;
+  if (int rc = make_tmap_bf16_2d(&mq, qkv, (uint64_t)3 * H * D, Tn, ld, 64, T)) return rc;
+  if (int rc = make_tmap_bf16_2d(&mo, dout, (uint64_t)H * D, Tn, (uint64_t)H * D, 64, T)) return rc;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         DqSmem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               DkvSmem<D>::TOTAL);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: cudaFuncSetAttribute");
+    configured = true;
+  }
+  const dim3 grid(S / T, H, n_seq);
+  static int only = -1;  // debug: ZB_ATTN_BWD_ONLY=dq|dkdv runs one pass
+  if (only < 0) {
+    const char* e = getenv("ZB_ATTN_BWD_ONLY");
+    only = !e ? 0 : (e[0] == 'q' || (e[0] == 'd' && e[1] == 'q')) ? 1 : 2;
+  }
+  if (only != 1)
+    dkdv_kernel<D><<<grid, kThreads, DkvSmem<D>::TOTAL, s>>>(mq, mo, (const float*)lse,
+                                                            (const float*)delta,
+                                                            (__nv_bfloat16*)dqkv, S, H, ld, scale);
+  if (only != 2)
+    dq_kernel<D><<<grid, kThreads, DqSmem<D>::TOTAL, s>>>(mq, mo, (const float*)lse,
+                                                        (const float*)delta, (__nv_bfloat16*)dqkv,
+                                                        S, H, ld, scale);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_bwd_tc launch");
+}
+
+}  // namespace fab
+}  // namespace zb
+
+using namespace zb;
+
+extern "C" int zb_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const void* lse,
+                              void* dqkv, void* delta, int n_seq, int S, int H, int D, int ld,
+                              float scale, cudaStream_t s) {
+  if (S % 128) return set_error(ZB_ERR_INVALID, "attn_bwd_tc: seq_len must be a multiple of 128");
+  if (ld % 8 || ((uintptr_t)qkv & 15) || ((uintptr_t)dout & 15))
+    return set_error(ZB_ERR_INVALID, "attn_bwd_tc: bad ld/alignment");
+  if (n_seq <= 0) return 0;
+  if (D == 64) return fab::run<64>(qkv, out, dout, lse, dqkv, delta, n_seq, S, H, ld, scale, s);
+  if (D == 128) return fab::run<128>(qkv, out, dout, lse, dqkv, delta, n_seq, S, H, ld, scale, s);
+  return set_error(ZB_ERR_UNSUPPORTED, "attn_bwd_tc: head_dim %d unsupported (64, 128)", D);
+}

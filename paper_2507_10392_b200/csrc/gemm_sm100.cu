@@ -22,6 +22,8 @@
 #include "common.cuh"
 #include "zb_internal.h"
 
+#include <cstdlib>
+
 namespace zb {
 
 enum Epilogue : int {
@@ -347,6 +349,184 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
 }
 
+// ---------------------------------------------------------------- 2-CTA variant
+// A CTA pair (cluster of 2, cta_group::2) computes a 256 x BN tile: each CTA
+// stages its 128 rows of A and half of B's BN columns, the leader CTA's single
+// thread issues tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' smem, and
+// each CTA's TMEM receives its own 128 accumulator rows.  Per SM the smem
+// operand traffic per MMA cycle drops by a third vs. the 1-CTA 128 x 256 tile.
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 6 : (BN == 192 ? 7 : 8);
+  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN, int A_MN, int B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2cta_kernel(const __grid_constant__ CUtensorMap tmA,
+                    const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
+  using Cfg = Gemm2Cfg<BN>;
+  constexpr int S = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint32_t base = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((base + 1023u) & ~1023u) - base);
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + S * Cfg::A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int num_tiles = args.num_m_tiles * args.num_n_tiles;  // m tiles of 256 rows
+  const int num_units = num_tiles * args.splits;
+  const int num_kb = (args.K + BK - 1) / BK;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full_bar[i], 1);   // leader's expect_tx (both CTAs' TMA bytes land here)
+      mbar_init(&empty_bar[i], 1);  // multicast MMA commit
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 2 * kEpiWarps);  // both CTAs' epilogue warps (leader's copy)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2cta(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int unit = cluster; unit < num_units; unit += nclusters) {
+        const int tile = unit % num_tiles;
+        const int kb0 = (unit / num_tiles) * args.kb_per_split;
+        const int kb1 = min(num_kb, kb0 + args.kb_per_split);
+        const int m0 = (tile % args.num_m_tiles) * 256 + (int)rank * 128;
+        const int n0 = (tile / args.num_m_tiles) * BN + (int)rank * (BN / 2);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          // Only the leader arrives (with both CTAs' bytes).  The follower's TMA
+          // bytes for this phase cannot land early: it refills a stage only after the
+          // pair's MMA released it, i.e. after the leader's barrier completed the
+          // previous phase.  (A remote release-arrive per k-block costs a MEMBAR.)
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+          uint8_t* a_dst = smA + stage * Cfg::A_BYTES;
+          uint8_t* b_dst = smB + stage * Cfg::B_BYTES;
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              tma_load_2d_2cta(a_dst + j * (64 * BK * 2), &tmA, &full_bar[stage], m0 + j * 64, k0);
+          } else {
+            tma_load_2d_2cta(a_dst, &tmA, &full_bar[stage], k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 128; ++j)
+              tma_load_2d_2cta(b_dst + j * (64 * BK * 2), &tmB, &full_bar[stage], n0 + j * 64, k0);
+          } else {
+            tma_load_2d_2cta(b_dst, &tmB, &full_bar[stage], k0, n0);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(256, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int unit = cluster; unit < num_units; unit += nclusters, ++local) {
+        const int kb0 = (unit / num_tiles) * args.kb_per_split;
+        const int kb1 = min(num_kb, kb0 + args.kb_per_split);
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smA + stage * Cfg::A_BYTES);
+          const uint32_t b_addr = smem_u32(smB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t a_desc = A_MN ? umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024)
+                                   : umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            uint64_t b_desc = B_MN ? umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024)
+                                   : umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            mma_bf16_ss_2cta(d_tmem, a_desc, b_desc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit_2cta(&empty_bar[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_2cta(&tfull_bar[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = (warp - 4) & 3;
+    const int half = (warp - 4) >> 2;
+    int local = 0;
+    for (int unit = cluster; unit < num_units; unit += nclusters, ++local) {
+      const int tile = unit % num_tiles;
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      const int m0 = (tile % args.num_m_tiles) * 256 + (int)rank * 128;
+      const int n0 = (tile / args.num_m_tiles) * BN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + ew * 32 + lane;
+      const bool row_ok = row < args.M;
+#pragma unroll 1
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+        __syncwarp();
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
+        tmem_ld_wait();
+        const int col0 = n0 + c * 32;
+        if (row_ok && col0 < args.N) epilogue_chunk<EPI>(args, r, row, col0);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tempty_bar[acc]);
+        else
+          mbar_arrive_remote(&tempty_bar[acc], 0);
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2cta(tmem_base, Cfg::TMEM_COLS);
+}
+
 // ---------------------------------------------------------------- host side
 
 // 2-D bf16 tensor map with a {64, rows} box and 128-byte swizzle.
@@ -396,6 +576,54 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs ar
   return 0;
 }
 
+template <int BN, int A_MN, int B_MN, int EPI>
+static int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs args,
+                        cudaStream_t stream) {
+  using Cfg = Gemm2Cfg<BN>;
+  auto kern = gemm2cta_kernel<BN, A_MN, B_MN, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm2cta: cudaFuncSetAttribute");
+    configured = true;
+  }
+  args.num_m_tiles = (args.M + 255) / 256;
+  args.num_n_tiles = (args.N + BN - 1) / BN;
+  const int tiles = args.num_m_tiles * args.num_n_tiles;
+  const int num_kb = (args.K + BK - 1) / BK;
+  const int pairs = num_sms() / 2;
+  int splits = 1;
+  if (EPI == EPI_F32 && args.beta == 1.f && tiles < pairs) {
+    splits = (2 * pairs + tiles - 1) / tiles;
+    int cap = num_kb / 8;
+    if (splits > cap) splits = cap > 1 ? cap : 1;
+  }
+  args.kb_per_split = (num_kb + splits - 1) / splits;
+  args.splits = (num_kb + args.kb_per_split - 1) / args.kb_per_split;
+  const int units = tiles * args.splits;
+  const int clusters = units < pairs ? units : pairs;
+  kern<<<2 * clusters, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, args);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "gemm2cta launch");
+  return 0;
+}
+
+template <int BN, int A_MN, int B_MN>
+static int dispatch_epi2(int epi, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs args,
+                         cudaStream_t s) {
+  switch (epi) {
+    case EPI_BF16: return launch_gemm2<BN, A_MN, B_MN, EPI_BF16>(ta, tb, args, s);
+    case EPI_BIAS: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS>(ta, tb, args, s);
+    case EPI_BIAS_GELU: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_GELU>(ta, tb, args, s);
+    case EPI_BIAS_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_RESID>(ta, tb, args, s);
+    case EPI_GELU_BWD: return launch_gemm2<BN, A_MN, B_MN, EPI_GELU_BWD>(ta, tb, args, s);
+    case EPI_F32: return launch_gemm2<BN, A_MN, B_MN, EPI_F32>(ta, tb, args, s);
+    case EPI_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_RESID>(ta, tb, args, s);
+  }
+  return set_error(ZB_ERR_INVALID, "gemm: unknown epilogue %d", epi);
+}
+
 template <int BN, int A_MN, int B_MN>
 static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs args,
                         cudaStream_t s) {
@@ -425,25 +653,41 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
   if (((uintptr_t)A & 15) || ((uintptr_t)B & 15))
     return set_error(ZB_ERR_INVALID, "gemm: A/B must be 16-byte aligned");
   CUtensorMap ta, tb;
-  // BN choice: 256-wide tiles unless 128-wide ones fill the SMs in clearly fewer
-  // partial waves (N = 768-class layers) or N is small.
-  int BN = 256;
+  // Tile choice by a wave-quantisation cost model: cost = waves x per-tile time per
+  // k-block on one SM = max(MMA 2*BN cycles, smem operand bytes at ~87% of 128 B/cycle).
+  // 1-CTA tiles are 128 x BN on one SM; 2-CTA (cta_group::2) tiles are 256 x BN on an
+  // SM pair, each SM staging 128 rows of A and BN/2 rows of B.
+  int BN = 256, pair = 0;
   {
-    // cost ~ waves x per-tile time; per-tile time per k-block ~ max(MMA 2*BN cycles,
-    // smem (128+BN)*128 B at ~87% of 128 B/cycle).  Picks 192 for N = 768 / 3072-class layers.
-    const int sms = num_sms(), mt = (M + BM - 1) / BM;
+    const int sms = num_sms();
     double best = 1e30;
-    for (int bn : {256, 192, 128}) {
-      const long long t = (long long)mt * ((N + bn - 1) / bn);
-      const long long waves = (t + sms - 1) / sms;
-      const double per = 2.0 * bn > 1.15 * (128 + bn) ? 2.0 * bn : 1.15 * (128 + bn);
-      const double cost = waves * per;
-      if (cost < best - 1e-9) {
-        best = cost;
-        BN = bn;
+    for (int two = 1; two >= 0; --two) {
+      if (two && M < 256) continue;
+      for (int bn : {256, 192, 128}) {
+        if (two && b_mn_major && bn == 192) continue;  // MN-major half-tiles must be 64-multiples
+        const long long t = (long long)((M + (two ? 255 : 127)) / (two ? 256 : 128)) * ((N + bn - 1) / bn);
+        const long long slots = two ? sms / 2 : sms;
+        const long long waves = (t + slots - 1) / slots;
+        const double smem_cyc = 1.15 * (128 + (two ? bn / 2 : bn));
+        const double per = 2.0 * bn > smem_cyc ? 2.0 * bn : smem_cyc;
+        const double cost = waves * per;
+        if (cost < best - 1e-9) {
+          best = cost;
+          BN = bn;
+          pair = two;
+        }
       }
     }
     if (N <= 128) BN = 128;
+    static int force = -1;
+    if (force < 0) {
+      const char* f = getenv("ZB_GEMM_CTAS");
+      force = f ? atoi(f) : 0;
+    }
+    // 2-CTA tiles are correct but measured ~2x slower than 1-CTA so far (profiles/
+    // r01_gemm_1cta_vs_2cta.txt): opt-in only until the pair pipeline is fixed.
+    if (force != 2) pair = 0;
+    if (force == 2 && M >= 256 && !(b_mn_major && BN == 192)) pair = 1;
   }
   int rc;
   if (a_mn_major)
@@ -454,7 +698,7 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
   if (b_mn_major)
     rc = make_tmap(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BK);
   else
-    rc = make_tmap(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, (uint32_t)BN);
+    rc = make_tmap(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, (uint32_t)(pair ? BN / 2 : BN));
   if (rc) return rc;
   GemmArgs args{};
   args.C = C;
@@ -473,6 +717,26 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
     args.vec = v ? 1 : 0;
   }
   const int key = a_mn_major * 2 + b_mn_major;
+  if (pair) {
+    if (BN == 256) {
+      switch (key) {
+        case 0: return dispatch_epi2<256, 0, 0>(epilogue, ta, tb, args, stream);
+        case 1: return dispatch_epi2<256, 0, 1>(epilogue, ta, tb, args, stream);
+        case 3: return dispatch_epi2<256, 1, 1>(epilogue, ta, tb, args, stream);
+      }
+    } else if (BN == 192) {
+      switch (key) {
+        case 0: return dispatch_epi2<192, 0, 0>(epilogue, ta, tb, args, stream);
+      }
+    } else {
+      switch (key) {
+        case 0: return dispatch_epi2<128, 0, 0>(epilogue, ta, tb, args, stream);
+        case 1: return dispatch_epi2<128, 0, 1>(epilogue, ta, tb, args, stream);
+        case 3: return dispatch_epi2<128, 1, 1>(epilogue, ta, tb, args, stream);
+      }
+    }
+    return set_error(ZB_ERR_INVALID, "gemm: unsupported 2-CTA layout");
+  }
   if (BN == 256) {
     switch (key) {
       case 0: return dispatch_epi<256, 0, 0>(epilogue, ta, tb, args, stream);

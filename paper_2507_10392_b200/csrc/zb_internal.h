@@ -24,4 +24,7 @@ int tensor_map_encode(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, v
 // 2-D bf16 tensor map, 128-byte swizzle, box {box_inner, box_outer}.
 int make_tmap_bf16_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
                       uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer);
+// delta[b,h,q] = sum_d dO*O (attention backward preprocessing, attn.cu).
+int launch_attn_delta(const void* o, const void* dout, void* delta, int T, int S, int H, int D,
+                      cudaStream_t s);
 }  // namespace zb

@@ -12,7 +12,7 @@ import torch
 from ._lib import call as _call
 
 # Device kernel launches issued per C-ABI entry point (for the bench's gpu_launches).
-_LAUNCHES_PER_CALL = {"zb_attn_bwd": 3}
+_LAUNCHES_PER_CALL = {"zb_attn_bwd": 3, "zb_attn_bwd_tc": 3}
 _launches = [0]
 
 
@@ -136,8 +136,14 @@ def attn_fwd(qkv, out, lse, n_seq, seq_len, n_head, head_dim, scale, impl="tc"):
 
 
 def attn_bwd(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, seq_len, n_head, head_dim,
-             scale):
+             scale, impl="tc"):
+    """impl "tc": tcgen05/TMEM kernels (default); "mma": legacy mma.sync kernels."""
     _need_cuda(qkv, out, dout, lse, dqkv, dq_accum, delta)
+    if impl == "tc":
+        call("zb_attn_bwd_tc", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), _ptr(dqkv),
+             _ptr(delta), n_seq, seq_len, n_head, head_dim, qkv.stride(0), float(scale),
+             _stream())
+        return
     call("zb_attn_bwd", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), _ptr(dqkv), _ptr(dq_accum),
          _ptr(delta), n_seq, seq_len, n_head, head_dim, qkv.stride(0), float(scale), _stream())
 

@@ -64,6 +64,7 @@ class Event:
     end: float
     device_ids: Tuple[str, ...]
     lane: str
+    deps: Tuple[tuple, ...] = ()
 
 
 class TaskGraph:
@@ -429,7 +430,7 @@ def list_schedule(tasks: Sequence[Task], plan: TrainingPlan) -> List[Event]:
         out.append(Event(key=pick.key, kind=pick.kind, group=pick.group, stage=pick.stage,
                          microbatch=pick.microbatch, layer=pick.layer, start=start, end=end,
                          device_ids=tuple(d for d, _ in pick.lanes) or plan.groups[pick.group].device_ids,
-                         lane=pick.lanes[0][1] if pick.lanes else "none"))
+                         lane=pick.lanes[0][1] if pick.lanes else "none", deps=pick.deps))
         for child in children[pick.key]:
             waiting[child.key] -= 1
             if end > earliest[child.key]:

@@ -88,7 +88,7 @@ class StageExecutor:
     def __init__(self, plan: TrainingPlan, ctx: CostContext, cfg: ModelConfig, dev_id: str,
                  rank_of: Dict[str, int], world_comm, group_comm, ops, device,
                  seed: int = 1234, adam: AdamConfig = AdamConfig(), init_device="cpu",
-                 schedule: str = "gpipe"):
+                 schedule: str = "gpipe", streams: bool = False):
         if plan.routing is None:
             raise ValueError("plan has no routing; attach it (configure.attach_routing) first")
         if ctx.model.num_layers != cfg.n_layer:
@@ -116,6 +116,13 @@ class StageExecutor:
         self.has_embed = self.order[0][0] == self.gi
         self.has_head = self.order[-1][0] == self.gi
         self.step_count = 0
+        # Lanes -> CUDA streams: compute on the current stream, collectives and P2P on
+        # their own streams, ordered by the task graph's dependencies (cross-stream
+        # events), so gathers / reduce-scatters / transfers overlap compute.
+        self.multistream = bool(streams) and device.type == "cuda"
+        if self.multistream:
+            self.lane_streams = {"collective": torch.cuda.Stream(device=device),
+                                 "p2p": torch.cuda.Stream(device=device)}
         self.capture_grads = False   # tests: keep each reduced grad shard before Adam
         self.captured: Dict[object, torch.Tensor] = {}
 
@@ -266,9 +273,43 @@ class StageExecutor:
             u.grad.zero_()
         self.loss_sum.zero_()
         self.gsumsq.zero_()
+        if not self.multistream:
+            for ev in self.events:
+                _DISPATCH[ev.kind](self, ev)
+            return
+        self._step_multistream()
+
+    def _step_multistream(self) -> None:
+        main = torch.cuda.current_stream(self.device)
+        start = torch.cuda.Event()
+        start.record(main)
+        streams = {"compute": main, **self.lane_streams}
+        for st in self.lane_streams.values():
+            st.wait_event(start)                     # fork (also joins a graph capture)
+        done: Dict[tuple, list] = {}                 # task key -> [(stream, event)]
+        last = {}
         for ev in self.events:
-            handler = _DISPATCH[ev.kind]
-            handler(self, ev)
+            waits = []
+            for dep in ev.deps:
+                waits.extend(done.get(dep, ()))      # deps of other groups are remote
+            if ev.kind in ("OffloadAct", "LoadAct", "FreeParams", "P2PRecv") or \
+                    ev.lane not in streams:
+                done[ev.key] = waits                 # no-op: completion = its deps'
+                continue
+            lane = "p2p" if ev.kind == "P2PSend" else ev.lane
+            st = streams[lane]
+            for dst, e in waits:
+                if dst is not st:
+                    st.wait_event(e)
+            with torch.cuda.stream(st):
+                _DISPATCH[ev.kind](self, ev)
+            e = torch.cuda.Event()
+            e.record(st)
+            done[ev.key] = [(st, e)]
+            last[lane] = e
+        for lane, e in last.items():                 # join
+            if lane != "compute":
+                main.wait_event(e)
 
     # ------------------------------------------------------------ handlers
     def _extras(self, stage: int, forward: bool, first_index: bool, last_index: bool):

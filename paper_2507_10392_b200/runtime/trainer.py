@@ -26,7 +26,8 @@ class ZorseTrainer:
     def __init__(self, plan: TrainingPlan, ctx: CostContext, cfg: ModelConfig, *,
                  world_rank: int = 0, world_size: int = 1, seed: int = 1234,
                  adam: AdamConfig = AdamConfig(), init_device: str = "cpu",
-                 schedule: str = "gpipe", _ops=None, _comms=None, _device=None):
+                 schedule: str = "gpipe", streams: bool = True, _ops=None, _comms=None,
+                 _device=None):
         devices = list(ctx.graph.vertices)
         if len(devices) != world_size:
             raise ValueError(f"cluster profile has {len(devices)} devices but world size is "
@@ -56,7 +57,7 @@ class ZorseTrainer:
         self.device = device
         self.exec = StageExecutor(plan, ctx, cfg, self.dev_id, self.rank_of, world, group, ops,
                                   device, seed=seed, adam=adam, init_device=init_device,
-                                  schedule=schedule)
+                                  schedule=schedule, streams=streams)
         self.loss_buf = torch.zeros(1, device=device, dtype=torch.float32)
 
         self.graph = None

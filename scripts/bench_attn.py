@@ -26,6 +26,7 @@ for (n, S, H, D) in [(8, 1024, 12, 64), (11, 1024, 12, 64), (2, 2048, 32, 128), 
     for impl in ("tc", "mma"):
         ms = t_ms(lambda: K.attn_fwd(qkv, out, lse, n, S, H, D, sc, impl=impl))
         r[f"fwd_{impl}_ms"] = ms; r[f"fwd_{impl}_tflops"] = fl / ms / 1e9
-    ms = t_ms(lambda: K.attn_bwd(qkv, out, dout, lse, dqkv, None, delta, n, S, H, D, sc))
-    r["bwd_ms"] = ms; r["bwd_tflops(2.5x fwd flops)"] = 2.5 * fl / ms / 1e9
+    for impl in ("tc", "mma"):
+        ms = t_ms(lambda: K.attn_bwd(qkv, out, dout, lse, dqkv, None, delta, n, S, H, D, sc, impl=impl))
+        r[f"bwd_{impl}_ms"] = ms; r[f"bwd_{impl}_tflops(2.5x fwd flops)"] = 2.5 * fl / ms / 1e9
     print(json.dumps(r), flush=True)

@@ -68,7 +68,7 @@ def main():
     params = gpt_cpu.init_params(CFG, 1234)
     state = {}
     ok = True
-    worst = {"loss": 0.0, "grad": 0.0, "param": 0.0}
+    worst = {"loss": 0.0, "grad": 0.0, "cos": 1.0, "param": 0.0, "worst_unit": None}
     for step in (1, 2):
         batch = synthetic_batch(CFG.vocab, CFG.seq_len, gb, step)
         loss = tr.step(batch.pin_memory())
@@ -79,11 +79,17 @@ def main():
             pu = tr.exec.units[u]
             ref = grads[u][pu.lo:pu.hi]
             rel = ((g.cpu() - ref).norm() / (ref.norm() + 1e-12)).item()
-            worst["grad"] = max(worst["grad"], rel)
+            cos = torch.nn.functional.cosine_similarity(g.cpu().double(), ref.double(), dim=0).item()
+            if rel > worst["grad"]:
+                worst["grad"], worst["worst_unit"] = rel, str(u)
+            worst["cos"] = min(worst["cos"], cos)
     for u, pu in tr.exec.units.items():
         err = (pu.master.cpu() - params[u][pu.lo:pu.hi]).abs().max().item()
         worst["param"] = max(worst["param"], err)
-    ok = worst["loss"] < 1e-2 and worst["grad"] < 3e-2 and worst["param"] < 5e-3
+    # bf16 storage / fp32 accumulate vs the fp32 oracle; small uneven shards of
+    # norm weights accumulate the most rounding (DESIGN.md §3 tolerances)
+    ok = (worst["loss"] < 1e-2 and worst["grad"] < 5e-2 and worst["cos"] > 0.998
+          and worst["param"] < 5e-3)
     print(json.dumps({"layout": name, "rank": rank, "dev": tr.dev_id, "group": tr.exec.gi,
                       "share": tr.exec.share, "units": len(tr.exec.units), "ok": ok, **worst}),
           flush=True)

@@ -123,7 +123,7 @@ def test_attention_fwd_bwd(cuda, n_seq, S, H, D, impl):
     ro.backward(dout.float())
     dqkv = torch.empty_like(qkv)
     delta = torch.empty(n_seq, H, S, device="cuda")
-    K.attn_bwd(qkv, out, dout, lse, dqkv, None, delta, n_seq, S, H, D, scale)
+    K.attn_bwd(qkv, out, dout, lse, dqkv, None, delta, n_seq, S, H, D, scale, impl=impl)
     torch.cuda.synchronize()
     g = qf.grad.view(T, 3, H * D)
     d = dqkv.view(T, 3, H * D)
