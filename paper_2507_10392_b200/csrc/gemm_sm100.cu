@@ -51,6 +51,8 @@ struct GemmArgs {
 };
 
 constexpr int BM = 128;
+// 2-CTA (cta_group::2) tiles in the default tile choice; see profiles/r01_gemm_1cta_vs_2cta.txt.
+constexpr bool kPairTilesDefault = false;
 constexpr int BK = 64;
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
@@ -659,10 +661,17 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
   // SM pair, each SM staging 128 rows of A and BN/2 rows of B.
   int BN = 256, pair = 0;
   {
+    static int force = -1;  // ZB_GEMM_CTAS=1|2 pins 1-CTA / 2-CTA tiles (benchmarking)
+    if (force < 0) {
+      const char* f = getenv("ZB_GEMM_CTAS");
+      force = f ? atoi(f) : 0;
+    }
+    const bool allow_pair = kPairTilesDefault ? force != 1 : force == 2;
     const int sms = num_sms();
     double best = 1e30;
     for (int two = 1; two >= 0; --two) {
-      if (two && M < 256) continue;
+      if (two && (M < 256 || !allow_pair)) continue;
+      if (!two && force == 2 && M >= 256) continue;
       for (int bn : {256, 192, 128}) {
         if (two && b_mn_major && bn == 192) continue;  // MN-major half-tiles must be 64-multiples
         const long long t = (long long)((M + (two ? 255 : 127)) / (two ? 256 : 128)) * ((N + bn - 1) / bn);
@@ -679,15 +688,6 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
       }
     }
     if (N <= 128) BN = 128;
-    static int force = -1;
-    if (force < 0) {
-      const char* f = getenv("ZB_GEMM_CTAS");
-      force = f ? atoi(f) : 0;
-    }
-    // 2-CTA tiles are correct but measured ~2x slower than 1-CTA so far (profiles/
-    // r01_gemm_1cta_vs_2cta.txt): opt-in only until the pair pipeline is fixed.
-    if (force != 2) pair = 0;
-    if (force == 2 && M >= 256 && !(b_mn_major && BN == 192)) pair = 1;
   }
   int rc;
   if (a_mn_major)

@@ -123,6 +123,8 @@ class StageExecutor:
         if self.multistream:
             self.lane_streams = {"collective": torch.cuda.Stream(device=device),
                                  "p2p": torch.cuda.Stream(device=device)}
+        self.record_timeline = False  # measured Gantt (see measured_timeline)
+        self._marks = []
         self.capture_grads = False   # tests: keep each reduced grad shard before Adam
         self.captured: Dict[object, torch.Tensor] = {}
 
@@ -281,8 +283,10 @@ class StageExecutor:
 
     def _step_multistream(self) -> None:
         main = torch.cuda.current_stream(self.device)
-        start = torch.cuda.Event()
+        timed = self.record_timeline
+        start = torch.cuda.Event(enable_timing=timed)
         start.record(main)
+        self._marks = [("start", start)] if timed else []
         streams = {"compute": main, **self.lane_streams}
         for st in self.lane_streams.values():
             st.wait_event(start)                     # fork (also joins a graph capture)
@@ -301,10 +305,15 @@ class StageExecutor:
             for dst, e in waits:
                 if dst is not st:
                     st.wait_event(e)
+            if timed:
+                b0 = torch.cuda.Event(enable_timing=True)
+                b0.record(st)
             with torch.cuda.stream(st):
                 _DISPATCH[ev.kind](self, ev)
-            e = torch.cuda.Event()
+            e = torch.cuda.Event(enable_timing=timed)
             e.record(st)
+            if timed:
+                self._marks.append((ev, b0, e))
             done[ev.key] = [(st, e)]
             last[lane] = e
         for lane, e in last.items():                 # join
@@ -427,6 +436,17 @@ class StageExecutor:
 
     def _noop(self, ev: Event) -> None:
         return None
+
+    def measured_timeline(self):
+        """Events of the last recorded step with measured (start, end) seconds
+        relative to the step start; call after torch.cuda.synchronize()."""
+        if not self._marks:
+            raise RuntimeError("set record_timeline = True (multi-stream executor) and run a step")
+        t0 = self._marks[0][1]
+        out = []
+        for ev, b, e in self._marks[1:]:
+            out.append((ev, t0.elapsed_time(b) * 1e-3, t0.elapsed_time(e) * 1e-3))
+        return out
 
     # ------------------------------------------------------------ results
     def gather_master(self, unit) -> Tuple[int, int, torch.Tensor]:
