@@ -51,8 +51,10 @@ struct GemmArgs {
 };
 
 constexpr int BM = 128;
-// 2-CTA (cta_group::2) tiles in the default tile choice; see profiles/r01_gemm_1cta_vs_2cta.txt.
-constexpr bool kPairTilesDefault = false;
+// 2-CTA (cta_group::2) tiles are used by default for long-K GEMMs (K >= 2048) whose B
+// operand is K-major or whose A is also MN-major (TN, wgrad); dgrad-shaped GEMMs (A
+// K-major, B MN-major) measured faster on 1-CTA tiles (profiles/r01_gemm_1cta_vs_2cta.txt).
+constexpr bool kPairTilesDefault = true;
 constexpr int BK = 64;
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
@@ -666,7 +668,8 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
       const char* f = getenv("ZB_GEMM_CTAS");
       force = f ? atoi(f) : 0;
     }
-    const bool allow_pair = kPairTilesDefault ? force != 1 : force == 2;
+    const bool shape_ok = K >= 2048 && !(b_mn_major && !a_mn_major);
+    const bool allow_pair = force == 2 || (kPairTilesDefault && force != 1 && shape_ok);
     const int sms = num_sms();
     double best = 1e30;
     for (int two = 1; two >= 0; --two) {
