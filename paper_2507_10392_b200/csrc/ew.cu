@@ -8,32 +8,42 @@
 namespace zb {
 
 // ------------------------------------------------------------------ LayerNorm
-// One warp per row; the row (<= 20 KB) stays in L1 between the passes.
-__global__ void layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
-                                     const __nv_bfloat16* __restrict__ w,
-                                     const __nv_bfloat16* __restrict__ b,
-                                     __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
-                                     float* __restrict__ rstd_out, int rows, int d, float eps) {
+// One warp per row; each lane holds its MAXV 16-byte vectors of the row in
+// registers, so x is read from HBM once (mean and variance in two register passes).
+template <int MAXV>
+__global__ void __launch_bounds__(256) layernorm_fwd_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+    const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y,
+    float* __restrict__ mean_out, float* __restrict__ rstd_out, int rows, int d, float eps) {
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
   const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * d);
   const int nv = d >> 3;
+  uint4 q[MAXV];
   float s = 0.f;
-  for (int v = lane; v < nv; v += 32) {
-    uint4 q = xr[v];
-    float2 a = unpack_bf16(q.x), c = unpack_bf16(q.y), e = unpack_bf16(q.z), f = unpack_bf16(q.w);
-    s += a.x + a.y + c.x + c.y + e.x + e.y + f.x + f.y;
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    const int v = lane + 32 * j;
+    q[j] = v < nv ? xr[v] : make_uint4(0, 0, 0, 0);
+    const uint32_t* qi = &q[j].x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = unpack_bf16(qi[k]);
+      s += f.x + f.y;
+    }
   }
   const float mean = warp_sum(s) / d;
   float ss = 0.f;
-  for (int v = lane; v < nv; v += 32) {
-    uint4 q = xr[v];
-    float2 p[4] = {unpack_bf16(q.x), unpack_bf16(q.y), unpack_bf16(q.z), unpack_bf16(q.w)};
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    if (lane + 32 * j >= nv) continue;
+    const uint32_t* qi = &q[j].x;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      float a0 = p[k].x - mean, a1 = p[k].y - mean;
+      float2 f = unpack_bf16(qi[k]);
+      const float a0 = f.x - mean, a1 = f.y - mean;
       ss += a0 * a0 + a1 * a1;
     }
   }
@@ -41,11 +51,12 @@ __global__ void layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
   const uint4* wr = reinterpret_cast<const uint4*>(w);
   const uint4* br = reinterpret_cast<const uint4*>(b);
   uint4* yr = reinterpret_cast<uint4*>(y + (size_t)row * d);
-  for (int v = lane; v < nv; v += 32) {
-    uint4 q = xr[v], qw = wr[v], qb = br[v];
-    uint32_t* qi = &q.x;
-    uint32_t* wi = &qw.x;
-    uint32_t* bi = &qb.x;
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    const int v = lane + 32 * j;
+    if (v >= nv) continue;
+    const uint4 qw = wr[v], qb = br[v];
+    const uint32_t *qi = &q[j].x, *wi = &qw.x, *bi = &qb.x;
     uint4 o;
     uint32_t* oi = &o.x;
 #pragma unroll
@@ -289,7 +300,8 @@ __global__ void __launch_bounds__(XENT_THREADS) xent_kernel(const __nv_bfloat16*
 }
 
 // ------------------------------------------------------------------ bias grad
-// db[n] += sum_r dy[r, n].  Block: 32 column-vectors (256 columns) x 8 row lanes.
+// db[n] += sum_r dy[r, n].  Block: 32 column-vectors (256 columns) x 8 row lanes;
+// each thread keeps 4 row loads in flight.
 __global__ void bias_grad_kernel(const __nv_bfloat16* __restrict__ dy, float* __restrict__ db,
                                  int rows, int n, int ld, int rows_per_block) {
   const int cv = blockIdx.x * 32 + (threadIdx.x & 31);  // column vector (8 cols)
@@ -299,7 +311,24 @@ __global__ void bias_grad_kernel(const __nv_bfloat16* __restrict__ dy, float* __
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const bool ok = cv * 8 < n;
   if (ok) {
-    for (int r = r0 + rl; r < r1; r += 8) {
+    int r = r0 + rl;
+    for (; r + 24 < r1; r += 32) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        q[u] = *reinterpret_cast<const uint4*>(dy + (size_t)(r + 8 * u) * ld + cv * 8);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t* qi = &q[u].x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float2 f = unpack_bf16(qi[k]);
+          acc[2 * k] += f.x;
+          acc[2 * k + 1] += f.y;
+        }
+      }
+    }
+    for (; r < r1; r += 8) {
       uint4 q = *reinterpret_cast<const uint4*>(dy + (size_t)r * ld + cv * 8);
       const uint32_t* qi = &q.x;
 #pragma unroll
@@ -365,9 +394,20 @@ extern "C" int zb_layernorm_fwd(const void* x, const void* w, const void* b, voi
   if (d % 8) return set_error(ZB_ERR_INVALID, "layernorm: d must be a multiple of 8");
   if (rows <= 0) return 0;
   const int threads = 256, per = threads / 32;
-  layernorm_fwd_kernel<<<(rows + per - 1) / per, threads, 0, s>>>(
-      (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, (const __nv_bfloat16*)b,
-      (__nv_bfloat16*)y, (float*)mean, (float*)rstd, rows, d, eps);
+  const int vpl = (d / 8 + 31) / 32;
+  auto go = [&](auto kern) {
+    kern<<<(rows + per - 1) / per, threads, 0, s>>>(
+        (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, (const __nv_bfloat16*)b,
+        (__nv_bfloat16*)y, (float*)mean, (float*)rstd, rows, d, eps);
+  };
+  if (vpl <= 1) go(layernorm_fwd_kernel<1>);
+  else if (vpl <= 2) go(layernorm_fwd_kernel<2>);
+  else if (vpl <= 3) go(layernorm_fwd_kernel<3>);
+  else if (vpl <= 4) go(layernorm_fwd_kernel<4>);
+  else if (vpl <= 7) go(layernorm_fwd_kernel<7>);
+  else if (vpl <= 10) go(layernorm_fwd_kernel<10>);
+  else if (vpl <= 20) go(layernorm_fwd_kernel<20>);
+  else return set_error(ZB_ERR_UNSUPPORTED, "layernorm_fwd: d > 5120");
   return launched("layernorm_fwd");
 }
 
@@ -436,7 +476,7 @@ extern "C" int zb_bias_grad(const void* dy, void* db, int rows, int n, int ld, c
   if (n % 8 || ld % 8) return set_error(ZB_ERR_INVALID, "bias_grad: n, ld must be multiples of 8");
   if (rows <= 0) return 0;
   const int cblocks = (n / 8 + 31) / 32;
-  int rblocks = (2 * num_sms() + cblocks - 1) / cblocks;
+  int rblocks = (8 * num_sms() + cblocks - 1) / cblocks;  // ~8 blocks per SM
   int rpb = (rows + rblocks - 1) / rblocks;
   rpb = ((rpb + 7) / 8) * 8;
   rblocks = (rows + rpb - 1) / rpb;
