@@ -37,7 +37,7 @@ struct FwdSmem {
   static constexpr int OFF_V = OFF_K + NST * K_BYTES;
   static constexpr int OFF_P = OFF_V + NST * V_BYTES;
   static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-  static constexpr int TOTAL = OFF_BAR + 256 + 1024;  // barriers + alignment slack
+  static constexpr int TOTAL = OFF_BAR + 256 + 1024;  // barriers + alignment slack (17 x 8 B used)
 };
 
 // K-major SW128 descriptor for a [rows][64*nblk] tile stored as nblk 64-column
@@ -50,7 +50,10 @@ template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tm_rows128,
                const __grid_constant__ CUtensorMap tm_rows64, __nv_bfloat16* __restrict__ out,
-               float* __restrict__ lse, int S, int H, float scale) {
+               float* __restrict__ lse, int S, int H, int n_seq, float scale) {
+  // Persistent: each CTA walks (query tile, head, sequence) work items in
+  // heavy-first order with a stride of gridDim.x; TMEM, barriers and the K/V /
+  // S / P rings persist across items (ring positions are global block counters).
   using L = FwdSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -64,20 +67,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = bar + 9;         // [2]
   uint64_t* p_empty = bar + 11;       // [2]
   uint64_t* o_bar = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* q_empty = bar + 14;       // all S MMAs of an item done -> Q reusable
+  uint64_t* o_empty = bar + 15;       // epilogue read O -> next item may overwrite
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqt = S / BQ;
-  const int qt = nqt - 1 - blockIdx.x;  // heavy (late) query tiles first
-  const int h = blockIdx.y, b = blockIdx.z;
   const int HD = H * D;
-  const int row0 = b * S;               // first qkv row of this sequence
-  const int nblk = qt + 1;              // causal: key blocks 0..qt
+  const int per_q = H * n_seq;
+  const int items = nqt * per_q;
+  auto decode = [&](int t, int& qt, int& h, int& b) {
+    qt = nqt - 1 - t / per_q;  // heavy (late) query tiles first
+    const int rem = t % per_q;
+    h = rem % H;
+    b = rem / H;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_rows128);
     tma_prefetch_desc(&tm_rows64);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    mbar_init(o_empty, 4);
     for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
@@ -102,27 +113,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, L::Q_BYTES);
-#pragma unroll
-      for (int kc = 0; kc < D / 64; ++kc)
-        tma_load_2d(sm + L::OFF_Q + kc * BQ * 128, &tm_rows128, q_full, h * D + kc * 64,
-                    row0 + qt * BQ);
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j % NST;
-        mbar_wait(&kv_empty[st], ((j / NST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], L::K_BYTES + L::V_BYTES);
-        uint8_t* kd = sm + L::OFF_K + st * L::K_BYTES;
-        uint8_t* vd = sm + L::OFF_V + st * L::V_BYTES;
-        const int kr = row0 + j * BKV;
+      int g = 0, lt = 0;
+      for (int t = blockIdx.x; t < items; t += gridDim.x, ++lt) {
+        int qt, h, b;
+        decode(t, qt, h, b);
+        const int row0 = b * S;
+        mbar_wait(q_empty, (lt & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, L::Q_BYTES);
 #pragma unroll
         for (int kc = 0; kc < D / 64; ++kc)
-          tma_load_2d(kd + kc * BKV * 128, &tm_rows128, &kv_full[st], HD + h * D + kc * 64, kr);
+          tma_load_2d(sm + L::OFF_Q + kc * BQ * 128, &tm_rows128, q_full, h * D + kc * 64,
+                      row0 + qt * BQ);
+        for (int j = 0; j <= qt; ++j, ++g) {
+          const int st = g % NST;
+          mbar_wait(&kv_empty[st], ((g / NST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[st], L::K_BYTES + L::V_BYTES);
+          uint8_t* kd = sm + L::OFF_K + st * L::K_BYTES;
+          uint8_t* vd = sm + L::OFF_V + st * L::V_BYTES;
+          const int kr = row0 + j * BKV;
 #pragma unroll
-        for (int kb = 0; kb < 2; ++kb)
+          for (int kc = 0; kc < D / 64; ++kc)
+            tma_load_2d(kd + kc * BKV * 128, &tm_rows128, &kv_full[st], HD + h * D + kc * 64, kr);
 #pragma unroll
-          for (int dc = 0; dc < D / 64; ++dc)
-            tma_load_2d(vd + (kb * (D / 64) + dc) * 8192, &tm_rows64, &kv_full[st],
-                        2 * HD + h * D + dc * 64, kr + kb * 64);
+          for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+            for (int dc = 0; dc < D / 64; ++dc)
+              tma_load_2d(vd + (kb * (D / 64) + dc) * 8192, &tm_rows64, &kv_full[st],
+                          2 * HD + h * D + dc * 64, kr + kb * 64);
+        }
       }
     }
   } else if (warp == 1) {
@@ -131,45 +149,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_s = umma_idesc_bf16(BQ, BKV, 0, 0);
       constexpr uint32_t idesc_o = umma_idesc_bf16(BQ, D, 0, 1);
       const uint32_t q_base = smem_u32(sm + L::OFF_Q);
-      auto issue_s = [&](int j) {
-        const int st = j % NST, sb = j & 1;
-        mbar_wait(&kv_full[st], (j / NST) & 1);
-        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t k_base = smem_u32(sm + L::OFF_K + st * L::K_BYTES);
+      int gbase = 0, lt = 0;
+      for (int t = blockIdx.x; t < items; t += gridDim.x, ++lt) {
+        int qt, h, b;
+        decode(t, qt, h, b);
+        const int nblk = qt + 1;
+        auto issue_s = [&](int j) {
+          const int gi = gbase + j;
+          const int st = gi % NST, sb = gi & 1;
+          mbar_wait(&kv_full[st], (gi / NST) & 1);
+          mbar_wait(&s_empty[sb], ((gi >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t k_base = smem_u32(sm + L::OFF_K + st * L::K_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16_ss(t_s[sb], desc_kmajor(q_base, kk, BQ), desc_kmajor(k_base, kk, BKV),
-                      idesc_s, kk > 0 ? 1u : 0u);
-        mma_commit(&s_full[sb]);
-      };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      issue_s(0);
-      for (int j = 0; j < nblk; ++j) {
-        if (j + 1 < nblk) issue_s(j + 1);
-        const int st = j % NST, sb = j & 1;
-        mbar_wait(&p_full[sb], (j >> 1) & 1);
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_bf16_ss(t_s[sb], desc_kmajor(q_base, kk, BQ), desc_kmajor(k_base, kk, BKV),
+                        idesc_s, kk > 0 ? 1u : 0u);
+          mma_commit(&s_full[sb]);
+          if (j == nblk - 1) mma_commit(q_empty);  // last read of this item's Q
+        };
+        mbar_wait(q_full, lt & 1);
         tc_fence_after();
-        const uint32_t p_base = smem_u32(sm + L::OFF_P + sb * L::P_BYTES);
-        const uint32_t v_base = smem_u32(sm + L::OFF_V + st * L::V_BYTES);
+        issue_s(0);
+        for (int j = 0; j < nblk; ++j) {
+          if (j + 1 < nblk) issue_s(j + 1);
+          const int gi = gbase + j;
+          const int st = gi % NST, sb = gi & 1;
+          mbar_wait(&p_full[sb], (gi >> 1) & 1);
+          if (j == 0) mbar_wait(o_empty, (lt & 1) ^ 1);  // previous item's O was read
+          tc_fence_after();
+          const uint32_t p_base = smem_u32(sm + L::OFF_P + sb * L::P_BYTES);
+          const uint32_t v_base = smem_u32(sm + L::OFF_V + st * L::V_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t a = desc_kmajor(p_base, kk, BQ);
-          const uint64_t bdesc =
-              umma_desc_sw128(v_base + (kk >> 2) * (D / 64) * 8192 + (kk & 3) * 2048, 8192, 1024);
-          mma_bf16_ss(t_o, a, bdesc, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BKV / 16; ++kk) {
+            const uint64_t a = desc_kmajor(p_base, kk, BQ);
+            const uint64_t bdesc =
+                umma_desc_sw128(v_base + (kk >> 2) * (D / 64) * 8192 + (kk & 3) * 2048, 8192, 1024);
+            mma_bf16_ss(t_o, a, bdesc, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&kv_empty[st]);
+          mma_commit(&p_empty[sb]);
+          mma_commit(o_bar);
         }
-        mma_commit(&kv_empty[st]);
-        mma_commit(&p_empty[sb]);
-        mma_commit(o_bar);
+        gbase += nblk;
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax
     const int wq = warp - 4;                 // TMEM lane quarter
     const int r = wq * 32 + lane;            // query row in the tile
-    const int q = qt * BQ + r;               // query position in the sequence
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const float sl2 = scale * LOG2E;
     // Running max in the scaled log2 domain.  It is only moved when a row's new
@@ -177,107 +205,121 @@ __global__ void __launch_bounds__(kThreads, 1)
     // fp32/bf16), so O is rarely rescaled and the softmax warps normally hand P_j
     // to the MMA warp without waiting for P_{j-1} V_{j-1}.
     constexpr float RESCALE_T = 8.f;
-    float m = -INFINITY, l = 0.f;
-    int o_seen = 0;  // o_bar completions consumed (= PV blocks known complete)
-    for (int j = 0; j < nblk; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      float s[BKV];
-#pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_s[sb] + lane_off + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[sb]);
-      if (j == qt) {  // diagonal block: keys after the query are masked
-#pragma unroll
-        for (int c = 0; c < BKV; ++c)
-          if (c > r) s[c] = -INFINITY;
-      }
-      float mx = s[0];
-#pragma unroll
-      for (int c = 1; c < BKV; ++c) mx = fmaxf(mx, s[c]);
-      mx *= sl2;
-      const bool move = mx > m + RESCALE_T;
-      const float m_new = move ? mx : m;
-      const float corr = move ? exp2_fast(m - m_new) : 1.f;  // 0 on the first block
-      m = m_new;
-      float rs = 0.f;
-#pragma unroll
-      for (int c = 0; c < BKV; ++c) {
-        s[c] = exp2_fast(fmaf(s[c], sl2, -m));
-        rs += s[c];
-      }
-      l = l * corr + rs;
-      // P row -> smem (bf16, K-major SW128: two 64-key blocks of [128 rows][128 B])
-      mbar_wait(&p_empty[sb], ((j >> 1) & 1) ^ 1);
-      uint8_t* prow = sm + L::OFF_P + sb * L::P_BYTES + r * 128;
-#pragma unroll
-      for (int ch = 0; ch < BKV / 8; ++ch) {
-        uint4 pk;
-        pk.x = pack_bf16(s[ch * 8 + 0], s[ch * 8 + 1]);
-        pk.y = pack_bf16(s[ch * 8 + 2], s[ch * 8 + 3]);
-        pk.z = pack_bf16(s[ch * 8 + 4], s[ch * 8 + 5]);
-        pk.w = pack_bf16(s[ch * 8 + 6], s[ch * 8 + 7]);
-        const int kb = ch >> 3, cc = ch & 7;
-        *reinterpret_cast<uint4*>(prow + kb * (BQ * 128) + ((cc ^ (r & 7)) << 4)) = pk;
-      }
-      fence_proxy_async_smem();
-      const bool rescale = j > 0 && __any_sync(0xffffffffu, move);
-      if (rescale) {  // O must hold P_{j-1} V_{j-1} before it is rescaled
-        mbar_wait(o_bar, o_seen & 1);
-        ++o_seen;
+    int gbase = 0;
+    int o_seen = 0;  // o_bar completions consumed (= PV blocks known complete, global)
+    for (int t = blockIdx.x; t < items; t += gridDim.x) {
+      int qt, h, b;
+      decode(t, qt, h, b);
+      const int nblk = qt + 1;
+      const int q = qt * BQ + r;
+      const int row0 = b * S;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nblk; ++j) {
+        const int gi = gbase + j;
+        const int sb = gi & 1;
+        mbar_wait(&s_full[sb], (gi >> 1) & 1);
         tc_fence_after();
+        float sv[BKV];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < BKV / 32; ++c) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+          tmem_ld_32x32b_x32(t_s[sb] + lane_off + c * 32, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
-          tmem_st_32x32b_x32(t_o + lane_off + c * 32, v);
+          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]);
         }
-        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        if (j == qt) {  // diagonal block: keys after the query are masked
+#pragma unroll
+          for (int c = 0; c < BKV; ++c)
+            if (c > r) sv[c] = -INFINITY;
+        }
+        float mx = sv[0];
+#pragma unroll
+        for (int c = 1; c < BKV; ++c) mx = fmaxf(mx, sv[c]);
+        mx *= sl2;
+        const bool move = mx > m + RESCALE_T;
+        const float m_new = move ? mx : m;
+        const float corr = move ? exp2_fast(m - m_new) : 1.f;  // 0 on the first block
+        m = m_new;
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < BKV; ++c) {
+          sv[c] = exp2_fast(fmaf(sv[c], sl2, -m));
+          rs += sv[c];
+        }
+        l = l * corr + rs;
+        mbar_wait(&p_empty[sb], ((gi >> 1) & 1) ^ 1);
+        uint8_t* prow = sm + L::OFF_P + sb * L::P_BYTES + r * 128;
+#pragma unroll
+        for (int ch = 0; ch < BKV / 8; ++ch) {
+          uint4 pk;
+          pk.x = pack_bf16(sv[ch * 8 + 0], sv[ch * 8 + 1]);
+          pk.y = pack_bf16(sv[ch * 8 + 2], sv[ch * 8 + 3]);
+          pk.z = pack_bf16(sv[ch * 8 + 4], sv[ch * 8 + 5]);
+          pk.w = pack_bf16(sv[ch * 8 + 6], sv[ch * 8 + 7]);
+          const int kb = ch >> 3, cc = ch & 7;
+          *reinterpret_cast<uint4*>(prow + kb * (BQ * 128) + ((cc ^ (r & 7)) << 4)) = pk;
+        }
+        fence_proxy_async_smem();
+        const bool rescale = j > 0 && __any_sync(0xffffffffu, move);
+        if (rescale) {  // O must hold P_{j-1} V_{j-1} before it is rescaled
+          while (o_seen < gi) {
+            mbar_wait(o_bar, o_seen & 1);
+            ++o_seen;
+          }
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st_32x32b_x32(t_o + lane_off + c * 32, v);
+          }
+          tmem_st_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[sb]);
+        // keep o_bar consumption in step (never more than one completion behind)
+        while (o_seen < gi) {
+          mbar_wait(o_bar, o_seen & 1);
+          ++o_seen;
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[sb]);
-      // keep o_bar consumption in step (never more than one completion behind)
-      if (j > 0 && o_seen < j) {
+      // epilogue: O / l -> bf16 row, lse
+      while (o_seen < gbase + nblk) {
         mbar_wait(o_bar, o_seen & 1);
         ++o_seen;
       }
-    }
-    // epilogue: O / l -> bf16 row, lse
-    while (o_seen < nblk) {
-      mbar_wait(o_bar, o_seen & 1);
-      ++o_seen;
-    }
-    tc_fence_after();
-    const float inv = 1.f / l;
-    __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D;
+      tc_fence_after();
+      const float inv = 1.f / l;
+      __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
-      tmem_ld_wait();
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+        tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 pk;
-        pk.x = pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
-        pk.y = pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
-        pk.z = pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
-        pk.w = pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
-        *reinterpret_cast<uint4*>(orow + c * 32 + i) = pk;
+        for (int i = 0; i < 32; i += 8) {
+          uint4 pk;
+          pk.x = pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
+          pk.y = pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
+          pk.z = pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
+          pk.w = pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = pk;
+        }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_empty);
+      lse[((size_t)b * H + h) * S + q] = (m + __log2f(l)) / LOG2E;
+      gbase += nblk;
     }
-    lse[((size_t)b * H + h) * S + q] = (m + __log2f(l)) / LOG2E;
   }
 
   tc_fence_before();
@@ -300,8 +342,10 @@ static int run_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int 
     if (e != cudaSuccess) return set_cuda_error(e, "attn_sm100: cudaFuncSetAttribute");
     configured = true;
   }
-  fwd_kernel<D><<<dim3(S / BQ, H, n_seq), kThreads, smem, s>>>(m128, m64, (__nv_bfloat16*)out,
-                                                               (float*)lse, S, H, scale);
+  const int items = (S / BQ) * H * n_seq;
+  const int grid = items < num_sms() ? items : num_sms();
+  fwd_kernel<D><<<grid, kThreads, smem, s>>>(m128, m64, (__nv_bfloat16*)out, (float*)lse, S, H,
+                                             n_seq, scale);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_sm100 fwd launch");
 }

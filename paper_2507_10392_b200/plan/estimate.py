@@ -28,6 +28,7 @@ class _PlanView:
         self.order = plan.global_order()
         self.ranges = plan.stage_layer_ranges()
         self.n = len(self.order)
+        self._pm_cache = {}
 
     def layers(self, s: int) -> range:
         return range(*self.ranges[s])
@@ -37,20 +38,33 @@ class _PlanView:
 
     def per_microbatch(self, s: int, part: str) -> float:
         """Slowest member's time for one microbatch through ministage s.
-        part: "fwd", "bwd" (fwd recompute + gradient) or "bwd_only"."""
+        part: "fwd", "bwd" (fwd recompute + gradient) or "bwd_only".
+
+        Members with the same (kind, share) produce the identical float, so each
+        distinct pair is accumulated once (the max is unchanged, bit for bit);
+        the per-layer terms are added in layer order exactly as the reference
+        does (costs.py:220-249) — this is the planner's hot loop."""
         ctx, g = self.ctx, self.group(s)
+        key = (s, part)
+        hit = self._pm_cache.get(key)
+        if hit is not None:
+            return hit
+        classes = [ctx.model.class_of(layer) for layer in self.layers(s)]
         worst = 0.0
+        seen = set()
         for dev in g.devices:
             share = g.shares[dev.id]
-            if share <= 0:
+            if share <= 0 or (dev.kind, share) in seen:
                 continue
+            seen.add((dev.kind, share))
             t = 0.0
-            for layer in self.layers(s):
-                f = ctx.runtime.fit_for(dev.kind, ctx.model.class_of(layer))
+            for cls in classes:
+                f = ctx.runtime.fit_for(dev.kind, cls)
                 fwd = f.fwd_alpha + f.fwd_beta * share
                 bwd = f.bwd_alpha + f.bwd_beta * share
                 t += fwd if part == "fwd" else (fwd + bwd if part == "bwd" else bwd)
             worst = max(worst, t)
+        self._pm_cache[key] = worst
         return worst
 
     def gathers(self, s: int) -> List[float]:

@@ -133,6 +133,20 @@ def planner_case(name, nodes, model_cfg, global_batch, k_max=None, strategies=("
     }
 
 
+def reference_fixture_case(name, profile, model, workload, **kw):
+    """plan_training on one of the reference's own fixture clusters."""
+    _dump(rf.profile_to_json_dict(profile), f"cluster_{name}.json")
+    _dump(rf.model_to_json_dict(model, workload), f"model_{name}.json")
+    prof = load_cluster_profile(os.path.join(HERE, f"cluster_{name}.json"))
+    m, w = load_model_workload(os.path.join(HERE, f"model_{name}.json"))
+    runtime = fit_runtime_model(prof)
+    plan, records = rc.plan_training(prof, m, w, runtime, **kw)
+    return {"name": name, "kind": "plan_training", "cluster": f"cluster_{name}.json",
+            "model": f"model_{name}.json", "k_max": kw.get("k_max"), "strategies": ["zorse"],
+            "n_candidates": len(records), "plan_json": _plan_text(plan), "events": None,
+            "shards": None}
+
+
 def agreement_cases(seed, n):
     """Randomized feasible plans from the reference's own suite, serialized."""
     out = []
@@ -174,6 +188,9 @@ def main():
         planner_case("tiny_search", E.CONFIG_NODES["tiny-2stage"], E.TINY_GPT, 8, k_max=2),
         planner_case("gpt2s_search", E.dp_group_nodes(8), E.GPT2_SMALL, 64, k_max=1),
         planner_case("llama13b_search", E.CONFIG_NODES["llama13b-8"], E.LLAMA_13B, 256),
+        # the reference README's planner benchmark: 128 GPUs, ~1,600 candidates (README:139-140)
+        reference_fixture_case("ref_128gpu", rf.large_two_region_cluster(), rf.transformer_model(),
+                               rf.default_workload()),
     ]
     _dump(cases, "plans.json")
     _dump(agreement_cases(seed=2024, n=12), "agreement.json")

@@ -52,7 +52,8 @@ def test_build_plan_bit_exact(case):
     assert [list(x) for x in plan.stage_layer_ranges()] == case["stage_layer_ranges"]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: c["name"])
+@pytest.mark.parametrize("case", [c for c in CASES if c["events"] is not None],
+                         ids=lambda c: c["name"])
 def test_schedule_bit_exact(case):
     prof, ctx = _ctx(case)
     plan = P.TrainingPlan.from_json_dict(json.loads(case["plan_json"]), prof)
@@ -69,7 +70,8 @@ def test_schedule_bit_exact(case):
         assert counts[str(gi)] == {"allgather": ag, "reduce_scatter": rs}
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: c["name"])
+@pytest.mark.parametrize("case", [c for c in CASES if c["shards"] is not None],
+                         ids=lambda c: c["name"])
 def test_shard_layout_matches_reference_apportionment(case):
     prof, ctx = _ctx(case)
     plan = P.TrainingPlan.from_json_dict(json.loads(case["plan_json"]), prof)
