@@ -194,6 +194,66 @@ def run_reference(args):
     return 0
 
 
+NVLINK_PEER_GBS = 770.0   # measured B200 peer copy per direction (B200_PROFILING.md)
+
+
+def measure_collectives(trainer, dist, iters=20):
+    """AG-v and fused RS-v+AdamW GB/s on the largest parameter unit of this rank's
+    group, through the executor's own communicator (the NVLink peer path), after
+    the timed region.  AG re-gathers identical values; RS+AdamW writes scratch
+    optimizer state, so the trained state is untouched.  Time = max over ranks;
+    bytes = what the slowest rank moves over NVLink."""
+    import types
+    ex = trainer.exec
+    comm = ex.group_comm
+    if comm is None or not getattr(comm, "fused_optimizer", False):
+        return None
+    key = max(ex.units, key=lambda k: ex.units[k].layout.numel)
+    pu = ex.units[key]
+    g = len(pu.counts)
+    P = pu.layout.numel
+    shard = pu.hi - pu.lo
+    scratch = types.SimpleNamespace(
+        grad_off=pu.grad_off, flag_off=pu.flag_off, lo=pu.lo, hi=pu.hi, grad=pu.grad,
+        master=pu.master.clone(), exp_avg=pu.exp_avg.clone(), exp_avg_sq=pu.exp_avg_sq.clone(),
+        full=torch.empty_like(pu.full))
+    sumsq = torch.zeros(1, device=pu.grad.device)
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([s.elapsed_time(e) / iters], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def maxed(x):
+        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    ag_ms = timeit(lambda: comm.allgather_unit(pu))
+    rs_ms = timeit(lambda: comm.reduce_scatter_adamw(scratch, ex.adam, sumsq, ex.step_dev))
+    ag_bytes = maxed((P - shard) * 2)                 # bf16 received from peers
+    rs_bytes = maxed((g - 1) * shard * 4)             # fp32 peer slices read
+    out = {"unit": str(key), "params": P, "group_size": g, "peak_gbs": NVLINK_PEER_GBS,
+           "peak_source": "measured peer copy, B200_PROFILING.md"}
+    for name, ms, b, how in (("allgather_v", ag_ms, ag_bytes, "copy engines over NVLink peer memory"),
+                             ("reduce_scatter_v+adamw", rs_ms, rs_bytes,
+                              "one kernel: NVLink loads + sum + AdamW + bf16 cast")):
+        gbs = b / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "nvlink_bytes": int(b), "gbs": gbs,
+                     "frac": gbs / NVLINK_PEER_GBS, "path": how}
+    return out
+
+
 def run_ours(args):
     from paper_2507_10392_b200 import kernels
     from paper_2507_10392_b200.runtime.data import synthetic_batch
@@ -210,7 +270,8 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg, plan, ctx, gb = build_workload(args.gpus)
-    trainer = ZorseTrainer(plan, ctx, cfg, world_rank=rank, world_size=world)
+    trainer = ZorseTrainer(plan, ctx, cfg, world_rank=rank, world_size=world,
+                           collectives=args.collectives)
     ex = trainer.exec
     batch = synthetic_batch(cfg.vocab, cfg.seq_len, gb, 1, pin=True)
     h2d = trainer.load(batch)
@@ -267,6 +328,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = t.item()
 
+    coll = measure_collectives(trainer, dist) if world > 1 else None
+
     # ---------------- roofline of the dominant kernel (tcgen05 GEMM) ------------
     timed = TimedOps(kernels)
     ex.ops = timed
@@ -314,6 +377,7 @@ def run_ours(args):
                 "parallelism": f"dp{world}", "shares": [plan.groups[0].shares[d]
                                                          for d in plan.groups[0].device_ids],
                 "n_microbatches": plan.n_microbatches, "ministages": len(plan.groups[0].ministage_sizes),
+                "collectives": args.collectives if world > 1 else None,
                 "l2": "per-step working set (params+grads+activations) >> 126 MB L2; no flush",
             },
             "loss": loss,
@@ -331,6 +395,8 @@ def run_ours(args):
                          "algorithmic_flops_per_step": g_flops},
             "clocks": clocks.summary(),
         }
+        if coll is not None:
+            line["collectives"] = coll
         if world == 1:
             line["cpu_baseline"] = cpu_reference_sample(cfg)
         print(json.dumps(line), flush=True)
@@ -347,6 +413,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--eager", action="store_true", help="no CUDA-graph capture of the step")
+    ap.add_argument("--collectives", choices=["peer", "nccl"], default="peer",
+                    help="DP-group AG-v / RS-v: NVLink peer memory (fused RS+AdamW) or NCCL")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -142,6 +142,39 @@ int zb_p2p_group(void* comm, int n, const int* peers, void* const* bufs, const i
                  const int* is_send, int dtype, zb_stream_t stream);
 int zb_allreduce_sum(void* comm, void* buf, int64_t count, int dtype, zb_stream_t stream);
 
+/* ---- NVLink peer-memory collectives of one DP group (csrc/peer.cu) ------------------
+ * Each rank's arena (per parameter unit: bf16 full, fp32 grad, 16-B flag record
+ * {param_ready, grad_ready, done, pad}) is exported once with a CUDA IPC handle;
+ * `bases[p]` is rank p's arena base as mapped in this process (bases[me] local).
+ * Offsets are byte offsets inside the arena, identical on every rank. */
+int zb_ipc_handle_size(void);
+int zb_ipc_get_handle(const void* ptr, void* handle_out, uint64_t* offset_out);
+int zb_ipc_open(const void* handle, void** base_out);
+int zb_ipc_close(void* base);
+/* *flag = *epoch_dev + delta with system-scope release (after a system fence). */
+int zb_peer_signal(void* flag, const void* epoch_dev, int delta, zb_stream_t stream);
+/* AllGather-v before a layer (replaces the AllGather task, simulate.py:292-328 and
+ * :408-446; costs.py:138-149): wait for every peer's param_ready >= *epoch_dev +
+ * epoch_delta, then copy peer p's [displs[p], displs[p]+counts[p]) elements into the
+ * local buffer at buf_off.  mode 0: copy engines; mode 1: SM pull kernel. */
+int zb_peer_allgather_v(void* const* bases, int nranks, int me, uint64_t buf_off,
+                        int elem_bytes, const int64_t* counts, const int64_t* displs,
+                        uint64_t flag_off, const void* epoch_dev, int epoch_delta, int mode,
+                        zb_stream_t stream);
+/* ReduceScatter-v + grad scale + AdamW + bf16 cast in one kernel (replaces the
+ * ReduceScatter task simulate.py:523-534 followed by OptimStep :536-550): publish
+ * grad_ready = *epoch_dev, wait for all peers', sum the fp32 gradient slices
+ * [lo, lo+n) of every peer's grad buffer (grad_off), update master / exp_avg /
+ * exp_avg_sq (torch AdamW), write the bf16 shard to param_bf16 and (if non-NULL) the
+ * reduced gradient to grad_out, accumulate sum(g^2) into sumsq (if non-NULL); the
+ * last CTA publishes param_ready = *epoch_dev. */
+int zb_peer_rs_adamw(void* const* bases, int nranks, int me, uint64_t grad_off, int64_t lo,
+                     int64_t n, uint64_t flag_off, const void* epoch_dev, void* master,
+                     void* exp_avg, void* exp_avg_sq, void* param_bf16, void* grad_out,
+                     void* sumsq, float lr, float beta1, float beta2, float eps,
+                     float weight_decay, float grad_scale, const void* step_dev,
+                     zb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,7 @@ P = ctypes.c_void_p
 I = ctypes.c_int
 I64 = ctypes.c_int64
 F = ctypes.c_float
+U64 = ctypes.c_uint64
 
 # name -> argtypes (all functions return int status, 0 == ok)
 SIGNATURES = {
@@ -49,6 +50,13 @@ SIGNATURES = {
     "zb_reduce_scatter_v": [P, P, P, P, I, I, P],
     "zb_p2p_group": [P, I, P, P, P, P, I, P],
     "zb_allreduce_sum": [P, P, I64, I, P],
+    "zb_ipc_handle_size": [],
+    "zb_ipc_get_handle": [P, P, P],
+    "zb_ipc_open": [P, P],
+    "zb_ipc_close": [P],
+    "zb_peer_signal": [P, P, I, P],
+    "zb_peer_allgather_v": [P, I, I, U64, I, P, P, U64, P, I, I, P],
+    "zb_peer_rs_adamw": [P, I, I, U64, I64, I64, U64, P, P, P, P, P, P, P, F, F, F, F, F, F, P, P],
     "zb_version": [],
     "zb_device_sync": [],
 }

@@ -9,35 +9,10 @@
 // per-shard sum of squared gradients reduced with warp shuffles (for logging;
 // the interleaved per-ministage optimizer cannot clip by a global norm).
 // Update rule follows torch.optim.AdamW (decoupled weight decay, bias-corrected).
-#include "common.cuh"
+#include "adam.cuh"
 #include "zb_internal.h"
 
 namespace zb {
-
-struct AdamParams {
-  float lr, beta1, beta2, eps, wd, grad_scale;
-  float step_size;      // lr / (1 - beta1^t)
-  float inv_bc2_sqrt;   // 1 / sqrt(1 - beta2^t)
-  float decay;          // 1 - lr * wd
-  const int* step_dev;  // if set: t is read on the device (CUDA-graph replay)
-};
-
-ZB_DEVICE void resolve_step(AdamParams& a) {
-  if (a.step_dev) {
-    const int t = *a.step_dev;
-    const double bc1 = 1.0 - pow((double)a.beta1, t), bc2 = 1.0 - pow((double)a.beta2, t);
-    a.step_size = (float)(a.lr / bc1);
-    a.inv_bc2_sqrt = (float)(1.0 / sqrt(bc2));
-  }
-}
-
-ZB_DEVICE void adam_elem(float& p, float& m, float& v, float g, const AdamParams& a) {
-  p *= a.decay;
-  m = m + (g - m) * (1.f - a.beta1);
-  v = v * a.beta2 + (1.f - a.beta2) * g * g;
-  const float denom = sqrtf(v) * a.inv_bc2_sqrt + a.eps;
-  p = p - a.step_size * (m / denom);
-}
 
 __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master,
                                                     float* __restrict__ exp_avg,

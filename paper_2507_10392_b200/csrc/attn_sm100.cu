@@ -37,7 +37,7 @@ struct FwdSmem {
   static constexpr int OFF_V = OFF_K + NST * K_BYTES;
   static constexpr int OFF_P = OFF_V + NST * V_BYTES;
   static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-  static constexpr int TOTAL = OFF_BAR + 256 + 1024;  // barriers + alignment slack (17 x 8 B used)
+  static constexpr int TOTAL = OFF_BAR + 256 + 1024;  // barriers + alignment slack (18 x 8 B used)
 };
 
 // K-major SW128 descriptor for a [rows][64*nblk] tile stored as nblk 64-column
@@ -66,10 +66,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* s_empty = bar + 7;        // [2]
   uint64_t* p_full = bar + 9;         // [2]
   uint64_t* p_empty = bar + 11;       // [2]
-  uint64_t* o_bar = bar + 13;
-  uint64_t* q_empty = bar + 14;       // all S MMAs of an item done -> Q reusable
-  uint64_t* o_empty = bar + 15;       // epilogue read O -> next item may overwrite
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  // O-accumulation completions alternate between two barriers (PV block k commits
+  // o_bar[k & 1]).  With one barrier, PV_k and PV_{k+1} could both complete before
+  // the softmax warps poll for PV_k (the MMA may issue PV_{k+1} as soon as P_{k+1}
+  // is handed over), and a parity wait cannot tell phase k from phase k+2.
+  // Two barriers cannot run two phases ahead: P_{k+2} is handed over only after
+  // PV_k was consumed.
+  uint64_t* o_bar = bar + 13;         // [2]
+  uint64_t* q_empty = bar + 15;       // all S MMAs of an item done -> Q reusable
+  uint64_t* o_empty = bar + 16;       // epilogue read O -> next item may overwrite
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqt = S / BQ;
@@ -99,7 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_full[i], 4);
       mbar_init(&p_empty[i], 1);
     }
-    mbar_init(o_bar, 1);
+    mbar_init(&o_bar[0], 1);
+    mbar_init(&o_bar[1], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           mma_commit(&kv_empty[st]);
           mma_commit(&p_empty[sb]);
-          mma_commit(o_bar);
+          mma_commit(&o_bar[gi & 1]);
         }
         gbase += nblk;
       }
@@ -206,7 +213,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // to the MMA warp without waiting for P_{j-1} V_{j-1}.
     constexpr float RESCALE_T = 8.f;
     int gbase = 0;
-    int o_seen = 0;  // o_bar completions consumed (= PV blocks known complete, global)
+    int o_seen = 0;  // PV blocks known complete (global block counter)
+    auto consume_o = [&](int upto) {
+      while (o_seen < upto) {
+        mbar_wait(&o_bar[o_seen & 1], (o_seen >> 1) & 1);
+        ++o_seen;
+      }
+    };
     for (int t = blockIdx.x; t < items; t += gridDim.x) {
       int qt, h, b;
       decode(t, qt, h, b);
@@ -266,10 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         const bool rescale = j > 0 && __any_sync(0xffffffffu, move);
         if (rescale) {  // O must hold P_{j-1} V_{j-1} before it is rescaled
-          while (o_seen < gi) {
-            mbar_wait(o_bar, o_seen & 1);
-            ++o_seen;
-          }
+          consume_o(gi);
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
@@ -285,17 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[sb]);
-        // keep o_bar consumption in step (never more than one completion behind)
-        while (o_seen < gi) {
-          mbar_wait(o_bar, o_seen & 1);
-          ++o_seen;
-        }
+        // keep o_bar consumption in step (PV_{gi-1} consumed before P_{gi+1} is handed over)
+        consume_o(gi);
       }
       // epilogue: O / l -> bf16 row, lse
-      while (o_seen < gbase + nblk) {
-        mbar_wait(o_bar, o_seen & 1);
-        ++o_seen;
-      }
+      consume_o(gbase + nblk);
       tc_fence_after();
       const float inv = 1.f / l;
       __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D;

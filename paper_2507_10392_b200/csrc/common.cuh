@@ -1,6 +1,7 @@
 // Shared device helpers for the sm_100a kernels of libzorse_b200.
 // Inline PTX for mbarriers, TMA, tcgen05 (TMEM alloc / MMA / commit / ld).
 #pragma once
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -41,9 +42,27 @@ ZB_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-ZB_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
+// Bounded wait: a barrier that never completes (a bug, or a peer that died)
+// reports and traps after ~20 s instead of hanging the GPU.  The timing loop is
+// out of line so the hot path stays a single try_wait.
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if ((++n & 0xFF) == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t - t0 > 20ull * 1000000000ull) {
+        printf("zorse: mbarrier wait timeout block (%d,%d,%d) thread %d parity %u\n",
+               blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, parity);
+        __trap();
+      }
+    }
   }
+}
+ZB_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
 }
 
 // ---------------------------------------------------------------- TMA

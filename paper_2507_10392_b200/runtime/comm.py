@@ -10,6 +10,7 @@ The NCCL unique ids are exchanged with ``torch.distributed`` (plumbing only).
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import List, Sequence, Tuple
 
 import torch
@@ -17,6 +18,12 @@ import torch
 from .._lib import call, lib
 
 DT_BF16, DT_F32 = 0, 1
+
+
+def _count_launch(n: int = 1) -> None:
+    """Peer collectives are this library's kernels: count them with the others."""
+    from .. import kernels
+    kernels._launches[0] += n
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -82,7 +89,8 @@ class NcclComm:
             self.handle = None
 
 
-def build_comms(dist, world_rank: int, world_size: int, groups_ranks: List[List[int]]):
+def build_comms(dist, world_rank: int, world_size: int, groups_ranks: List[List[int]],
+                group_comms: bool = True):
     """Create the world communicator and this rank's group communicator.
 
     ``groups_ranks[gi]`` lists the world ranks of DP group gi in shard order.
@@ -97,6 +105,89 @@ def build_comms(dist, world_rank: int, world_size: int, groups_ranks: List[List[
     world = NcclComm(ids[0], world_size, world_rank)
     group = None
     for gi, ranks in enumerate(groups_ranks):
-        if world_rank in ranks and len(ranks) > 1:
+        if group_comms and world_rank in ranks and len(ranks) > 1:
             group = NcclComm(ids[1 + gi], len(ranks), ranks.index(world_rank))
     return world, group
+
+
+class PeerGroup:
+    """Collectives of one DP group over NVLink peer memory (csrc/peer.cu).
+
+    Every rank's ``Arena`` is exported once with a CUDA IPC handle and mapped by
+    the other ranks of its group.  ``allgather_unit`` is the AllGather-v before a
+    layer (copy engines by default); ``reduce_scatter_adamw`` is ReduceScatter-v +
+    scale + AdamW + bf16 cast in ONE kernel, so the executor skips the separate
+    OptimStep launch for this group (``fused_optimizer``).  Cross-rank ordering
+    uses per-unit flags stamped with the device-resident step counter.
+    """
+
+    fused_optimizer = True
+
+    def __init__(self, arena, ranks: List[int], world_rank: int, handles, mode: int = 0):
+        self.ranks = list(ranks)
+        self.nranks = len(ranks)
+        self.rank = ranks.index(world_rank)
+        self.mode = mode
+        self.arena = arena
+        self._opened = []
+        bases = []
+        for r in self.ranks:
+            if r == world_rank:
+                bases.append(arena.buf.data_ptr())
+                continue
+            handle, off = handles[r]
+            base = ctypes.c_void_p()
+            call("zb_ipc_open", ctypes.create_string_buffer(handle, len(handle)),
+                 ctypes.byref(base))
+            self._opened.append(base.value)
+            bases.append(base.value + off)
+        self.bases = (ctypes.c_void_p * self.nranks)(*bases)
+        self.epoch = None   # device int32 step counter (set by the executor)
+
+    @staticmethod
+    def build(dist, arena, world_rank: int, groups_ranks: List[List[int]], mode: int = 0):
+        """Collective over the whole world (every rank calls it).  Returns this
+        rank's PeerGroup, or None when its group has a single rank."""
+        n = lib().zb_ipc_handle_size()
+        handle = ctypes.create_string_buffer(n)
+        off = ctypes.c_uint64()
+        torch.cuda.synchronize()   # flags of the arena are zero before anyone maps it
+        call("zb_ipc_get_handle", ctypes.c_void_p(arena.buf.data_ptr()), handle, ctypes.byref(off))
+        mine = (handle.raw, off.value)
+        world = dist.get_world_size()
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        for ranks in groups_ranks:
+            if world_rank in ranks and len(ranks) > 1:
+                mode = {"ce": 0, "sm": 1}.get(os.environ.get("ZB_PEER_AG", ""), mode)
+                return PeerGroup(arena, ranks, world_rank, allh, mode)
+        return None
+
+    def _stream(self):
+        return torch.cuda.current_stream().cuda_stream
+
+    def _unit_arrays(self, pu):
+        if pu.peer_cache is None:
+            pu.peer_cache = ((ctypes.c_int64 * self.nranks)(*pu.counts),
+                             (ctypes.c_int64 * self.nranks)(*pu.displs))
+        return pu.peer_cache
+
+    def allgather_unit(self, pu) -> None:
+        counts, displs = self._unit_arrays(pu)
+        _count_launch(1 if self.mode == 0 else 2)   # wait kernel (+ SM pull)
+        call("zb_peer_allgather_v", self.bases, self.nranks, self.rank, pu.full_off, 2, counts,
+             displs, pu.flag_off, self.epoch.data_ptr(), -1, self.mode, self._stream())
+
+    def reduce_scatter_adamw(self, pu, adam, sumsq, step_dev, write_grad: bool = False) -> None:
+        grad_out = pu.grad[pu.lo:pu.hi].data_ptr() if write_grad else None
+        _count_launch(2)                            # publish+wait kernel, fused kernel
+        call("zb_peer_rs_adamw", self.bases, self.nranks, self.rank, pu.grad_off, pu.lo,
+             pu.hi - pu.lo, pu.flag_off, self.epoch.data_ptr(), pu.master.data_ptr(),
+             pu.exp_avg.data_ptr(), pu.exp_avg_sq.data_ptr(), pu.full[pu.lo:pu.hi].data_ptr(),
+             grad_out, sumsq.data_ptr() if sumsq is not None else None, adam.lr, adam.beta1,
+             adam.beta2, adam.eps, adam.weight_decay, 1.0, step_dev.data_ptr(), self._stream())
+
+    def close(self) -> None:
+        for b in self._opened:
+            call("zb_ipc_close", ctypes.c_void_p(b))
+        self._opened = []

@@ -59,27 +59,73 @@ class ParamUnit:
     full  : bf16 [P]  gathered parameters (this rank's shard lives in place at [lo, hi))
     grad  : fp32 [P]  gradient accumulator; after RS-v its [lo, hi) slice is the shard sum
     master, exp_avg, exp_avg_sq : fp32 [hi - lo]  optimizer state of the shard
+
+    ``full`` and ``grad`` are views into the rank's arena (see ``Arena``) at byte
+    offsets ``full_off`` / ``grad_off``; ``flag_off`` is the unit's 16-byte flag
+    record there (used by the NVLink peer collectives).
     """
 
     def __init__(self, name: str, layout: FlatLayout, spec: ShardSpec, pos: int, init_full,
-                 device):
+                 device, arena: "Arena", key):
         self.name, self.layout, self.spec, self.pos = name, layout, spec, pos
         self.lo, self.hi = spec.bounds[pos]
         n = self.hi - self.lo
         self.master = init_full[self.lo:self.hi].to(device=device, dtype=torch.float32).clone()
         self.exp_avg = torch.zeros(n, device=device, dtype=torch.float32)
         self.exp_avg_sq = torch.zeros(n, device=device, dtype=torch.float32)
-        self.full = torch.full((layout.numel,), float("nan"), device=device, dtype=torch.bfloat16)
+        self.full_off, self.grad_off, self.flag_off = arena.offsets[key]
+        self.full = arena.view(self.full_off, layout.numel, torch.bfloat16)
+        self.full.fill_(float("nan"))
         self.full[self.lo:self.hi] = self.master.to(torch.bfloat16)
-        self.grad = torch.zeros(layout.numel, device=device, dtype=torch.float32)
+        self.grad = arena.view(self.grad_off, layout.numel, torch.float32)
         self.p = layout.views(self.full)
         self.g = layout.views(self.grad)
         self.counts = spec.counts
         self.displs = spec.displs
+        self.peer_cache = None   # per-unit ctypes arrays of the peer collectives
 
     @property
     def shard_numel(self) -> int:
         return self.hi - self.lo
+
+
+class Arena:
+    """One allocation per rank holding every parameter unit's bf16 ``full`` buffer,
+    then every fp32 ``grad`` buffer (contiguous, so one memset clears them), then a
+    16-byte flag record per unit.  Every rank of a DP group holds the same units in
+    the same order, so all offsets agree across the group — the NVLink peer
+    collectives address a peer's buffer as (peer arena base + offset)."""
+
+    ALIGN = 256
+
+    def __init__(self, units: Sequence[Tuple[object, int]], device):
+        a = self.ALIGN
+        rnd = lambda x: (x + a - 1) // a * a  # noqa: E731
+        off = 0
+        full = {}
+        for key, numel in units:
+            full[key] = off
+            off = rnd(off + 2 * numel)
+        self.grad_lo = off
+        grad = {}
+        for key, numel in units:
+            grad[key] = off
+            off = rnd(off + 4 * numel)
+        self.grad_hi = off
+        self.flags_off = off
+        off = rnd(off + 16 * len(units))
+        self.nbytes = off
+        self.offsets = {key: (full[key], grad[key], self.flags_off + 16 * i)
+                        for i, (key, _) in enumerate(units)}
+        self.buf = torch.empty(self.nbytes, device=device, dtype=torch.uint8)
+        self.buf[self.flags_off:].zero_()
+
+    def view(self, off: int, numel: int, dtype) -> torch.Tensor:
+        nb = numel * torch.empty((), dtype=dtype).element_size()
+        return self.buf[off:off + nb].view(dtype)
+
+    def zero_grads(self) -> None:
+        self.buf[self.grad_lo:self.grad_hi].view(torch.float32).zero_()
 
 
 class StageExecutor:
@@ -135,19 +181,25 @@ class StageExecutor:
         if lay.numel != ctx.model.params_of(0):
             raise ValueError(f"layer layout has {lay.numel} params, planner spec says "
                              f"{ctx.model.params_of(0)}")
+        specs = []   # (key, layout, init kind, init index) in arena order
         for s in self.my_stages:
             for layer in range(*self.ranges[s]):
-                full = init_flat(lay, "layer", layer, cfg, seed, device=init_device)
-                self.units[layer] = ParamUnit(f"layer{layer}", lay, split_flat(lay.numel, shares),
-                                              self.pos, full, device)
+                specs.append((layer, lay, "layer", layer))
         if self.has_embed:
-            el = embed_layout(cfg)
-            self.units["embed"] = ParamUnit("embed", el, split_flat(el.numel, shares), self.pos,
-                                            init_flat(el, "embed", 0, cfg, seed, init_device), device)
+            specs.append(("embed", embed_layout(cfg), "embed", 0))
         if self.has_head:
-            hl = head_layout(cfg)
-            self.units["head"] = ParamUnit("head", hl, split_flat(hl.numel, shares), self.pos,
-                                           init_flat(hl, "head", 0, cfg, seed, init_device), device)
+            specs.append(("head", head_layout(cfg), "head", 0))
+        self.arena = Arena([(k, l.numel) for k, l, _, _ in specs], device)
+        for key, layout, kind, idx in specs:
+            full = init_flat(layout, kind, idx, cfg, seed, device=init_device)
+            name = f"layer{key}" if kind == "layer" else kind
+            self.units[key] = ParamUnit(name, layout, split_flat(layout.numel, shares), self.pos,
+                                        full, device, self.arena, key)
+        # Group collectives: NCCL AG-v / RS-v + a separate AdamW launch, or a
+        # communicator with ``fused_optimizer`` (NVLink peer memory: RS-v + scale +
+        # AdamW + cast in one kernel at the ReduceScatter event; OptimStep is then
+        # empty for this group).
+        self._zeroed = set()
 
         # ---------------- activations ----------------
         d = cfg.d_model
@@ -271,8 +323,9 @@ class StageExecutor:
         the current stream; does not synchronise."""
         self.step_count += 1
         self.ops.step_increment(self.step_dev)
-        for u in self.units.values():
-            u.grad.zero_()
+        self._zeroed = set()
+        if not self._fused:
+            self.arena.zero_grads()
         self.loss_sum.zero_()
         self.gsumsq.zero_()
         if not self.multistream:
@@ -330,15 +383,29 @@ class StageExecutor:
                 out.append("head")
         return out
 
+    @property
+    def _fused(self) -> bool:
+        return getattr(self.group_comm, "fused_optimizer", False)
+
     def _on_allgather(self, ev: Event) -> None:
         key = ev.key
         s, i = key[1], key[2]
         units = [ev.layer] + self._extras(s, key[0] == "AGf", i == 0, False)
         if self.group_comm is None:
             return
+        fused = self._fused
         for u in units:
             pu = self.units[u]
-            self.group_comm.allgather_v(pu.full, pu.counts, pu.displs)
+            if fused:
+                self.group_comm.allgather_unit(pu)
+                # A peer reads this rank's grad buffer until its fused RS+AdamW of the
+                # previous step ends; the gather above waited for exactly that
+                # (param_ready of every peer), so the buffer is free from here on.
+                if u not in self._zeroed:
+                    self._zeroed.add(u)
+                    pu.grad.zero_()
+            else:
+                self.group_comm.allgather_v(pu.full, pu.counts, pu.displs)
 
     def _on_reduce_scatter(self, ev: Event) -> None:
         s, i = ev.key[1], ev.key[2]
@@ -349,6 +416,15 @@ class StageExecutor:
         if s == self.n_stages - 1 and self.has_head and i == 0:
             units.append("head")
         if self.group_comm is None:
+            return
+        if self._fused:
+            a = self.adam
+            for u in units:
+                pu = self.units[u]
+                self.group_comm.reduce_scatter_adamw(pu, a, self.gsumsq, self.step_dev,
+                                                     write_grad=self.capture_grads)
+                if self.capture_grads:
+                    self.captured[u] = pu.grad[pu.lo:pu.hi].clone()
             return
         for u in units:
             pu = self.units[u]
@@ -361,6 +437,8 @@ class StageExecutor:
             units.append("embed")
         if s == self.n_stages - 1 and self.has_head:
             units.append("head")
+        if self._fused:
+            return   # done at each unit's ReduceScatter (fused RS-v + AdamW)
         a = self.adam
         for u in units:
             pu = self.units[u]

@@ -26,8 +26,10 @@ class ZorseTrainer:
     def __init__(self, plan: TrainingPlan, ctx: CostContext, cfg: ModelConfig, *,
                  world_rank: int = 0, world_size: int = 1, seed: int = 1234,
                  adam: AdamConfig = AdamConfig(), init_device: str = "cpu",
-                 schedule: str = "gpipe", streams: bool = True, _ops=None, _comms=None,
-                 _device=None):
+                 schedule: str = "gpipe", streams: bool = True, collectives: str = "peer",
+                 _ops=None, _comms=None, _device=None):
+        if collectives not in ("peer", "nccl"):
+            raise ValueError(f"collectives must be 'peer' or 'nccl', not {collectives!r}")
         devices = list(ctx.graph.vertices)
         if len(devices) != world_size:
             raise ValueError(f"cluster profile has {len(devices)} devices but world size is "
@@ -45,7 +47,8 @@ class ZorseTrainer:
             if world_size > 1:
                 import torch.distributed as dist
                 from .comm import build_comms
-                world, group = build_comms(dist, world_rank, world_size, groups_ranks)
+                world, group = build_comms(dist, world_rank, world_size, groups_ranks,
+                                           group_comms=(collectives == "nccl"))
             else:
                 world, group = None, None
         else:  # test harness injection (tests/cpu_ops.py)
@@ -58,6 +61,14 @@ class ZorseTrainer:
         self.exec = StageExecutor(plan, ctx, cfg, self.dev_id, self.rank_of, world, group, ops,
                                   device, seed=seed, adam=adam, init_device=init_device,
                                   schedule=schedule, streams=streams)
+        self.collectives = collectives if world_size > 1 else None
+        if _ops is None and world_size > 1 and collectives == "peer":
+            # AG-v / fused RS-v+AdamW over NVLink peer memory (csrc/peer.cu)
+            from .comm import PeerGroup
+            peer = PeerGroup.build(dist, self.exec.arena, world_rank, groups_ranks)
+            if peer is not None:
+                peer.epoch = self.exec.step_dev
+                self.exec.group_comm = peer
         self.loss_buf = torch.zeros(1, device=device, dtype=torch.float32)
 
         self.graph = None

@@ -29,6 +29,7 @@ XLW = E.ModelConfig("mgpu-xl-width", "gpt", n_layer=4, d_model=1600, n_head=25, 
 LAYOUTS = {
     # name: (nodes, groups, n_microbatches, ministage counts, strategy, global batch)
     "dp2": ([("n0", ["b200", "b200h"])], [["n0-0", "n0-1"]], 2, [2], "zorse", 8),
+    "dp2z3": ([("n0", ["b200", "b200h"])], [["n0-0", "n0-1"]], 2, [2], "pp-zero3", 8),
     "pp2": ([("n0", ["b200"]), ("n1", ["b200h"])], [["n0-0"], ["n1-0"]], 2, [2, 2], "zorse", 8),
     "pp1+3": ([("n0", ["b200"]), ("n1", ["b200", "b200h", "b200h"])],
               [["n0-0"], ["n1-0", "n1-1", "n1-2"]], 2, [1, 1], "zorse", 8),
@@ -62,8 +63,10 @@ def main():
     plan = P.build_plan(ctx, prof, P.make_partition(ctx.graph, groups), M, counts,
                         P.Strategy(strategy), P.cluster_fingerprint(prof), "transformer")
     P.attach_routing(plan, rt, "transformer")
+    coll = os.environ.get("ZB_COLLECTIVES", "peer")
+    graph = os.environ.get("ZB_GRAPH", "1") == "1"
     tr = ZorseTrainer(plan, ctx, CFG, world_rank=rank, world_size=world,
-                      schedule=SCHED.get(name, "gpipe"))
+                      schedule=SCHED.get(name, "gpipe"), collectives=coll)
     tr.exec.capture_grads = True
     params = gpt_cpu.init_params(CFG, 1234)
     state = {}
@@ -71,6 +74,8 @@ def main():
     worst = {"loss": 0.0, "grad": 0.0, "cos": 1.0, "param": 0.0, "worst_unit": None}
     for step in (1, 2):
         batch = synthetic_batch(CFG.vocab, CFG.seq_len, gb, step)
+        if step == 2 and graph:
+            tr.capture()      # step 2 replays a CUDA graph of the whole step
         loss = tr.step(batch.pin_memory())
         ref_loss, grads = gpt_cpu.loss_and_grads(CFG, params, batch)
         gpt_cpu.adamw(params, grads, state, step)
@@ -90,7 +95,7 @@ def main():
     # norm weights accumulate the most rounding (DESIGN.md §3 tolerances)
     ok = (worst["loss"] < 1e-2 and worst["grad"] < 5e-2 and worst["cos"] > 0.998
           and worst["param"] < 5e-3)
-    print(json.dumps({"layout": name, "rank": rank, "dev": tr.dev_id, "group": tr.exec.gi,
+    print(json.dumps({"layout": name, "collectives": coll, "graph": graph, "rank": rank, "dev": tr.dev_id, "group": tr.exec.gi,
                       "share": tr.exec.share, "units": len(tr.exec.units), "ok": ok, **worst}),
           flush=True)
     dist.barrier()

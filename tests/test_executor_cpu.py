@@ -108,7 +108,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, spec, q, cfg=None, schedule="gpipe"):
+def _worker(rank, world, port, spec, q, cfg=None, schedule="gpipe", fused=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -118,8 +118,9 @@ def _worker(rank, world, port, spec, q, cfg=None, schedule="gpipe"):
         def comms(groups_ranks):
             world_c = cpu_ops.GlooComm(list(range(world)), rank)
             group = None
+            kind = cpu_ops.GlooFusedComm if fused else cpu_ops.GlooComm
             for ranks in groups_ranks:  # every rank must create every subgroup
-                c = cpu_ops.GlooComm(ranks, rank)
+                c = kind(ranks, rank)
                 if rank in ranks and len(ranks) > 1:
                     group = c
             return world_c, group
@@ -148,11 +149,11 @@ def test_three_ranks_gloo_matches_oracle(spec):
     _run_gloo(spec, 3)
 
 
-def _run_gloo(spec, world, cfg=None, schedule="gpipe"):
+def _run_gloo(spec, world, cfg=None, schedule="gpipe", fused=False):
     ctx_mp = mp.get_context("spawn")
     q = ctx_mp.Queue()
     port = _free_port()
-    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, spec, q, cfg, schedule))
+    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, spec, q, cfg, schedule, fused))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -168,6 +169,19 @@ def _run_gloo(spec, world, cfg=None, schedule="gpipe"):
         r["shards"] = {u: (lo, hi, torch.from_numpy(m), torch.from_numpy(g))
                        for u, (lo, hi, m, g) in r["shards"].items()}
     _check(list(results.values()), 2, cfg)
+
+
+@pytest.mark.parametrize("spec,schedule", [
+    (([("n0", ["b200", "b200h"]), ("n1", ["b200"])], [["n0-0", "n0-1"], ["n1-0"]], 2, [2, 2],
+      "zorse"), "gpipe"),
+    (([("n0", ["b200", "b200", "b200h"])], [["n0-0", "n0-1", "n0-2"]], 2, [1], "pp-zero3"),
+     "1f1b"),
+], ids=["interleaved", "dp3-1f1b"])
+def test_fused_optimizer_path_gloo(spec, schedule):
+    """The executor path of the NVLink peer collectives (RS-v + AdamW fused at the
+    ReduceScatter event, grads cleared after each unit's first gather, OptimStep
+    empty) against the oracle, with a gloo twin of the communicator."""
+    _run_gloo(spec, 3, CFG, schedule, fused=True)
 
 
 def test_1f1b_three_stages_llama_gloo():
