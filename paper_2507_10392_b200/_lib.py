@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libzorse_b200.so")
+LIB_PATH = os.environ.get("ZB_LIB_PATH") or os.path.join(_HERE, "libzorse_b200.so")
 
 P = ctypes.c_void_p
 I = ctypes.c_int

@@ -37,8 +37,11 @@ def _newer(target: str, deps) -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
-def build(verbose: bool = False, jobs: int = 8) -> str:
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(verbose: bool = False, jobs: int = 8, defines=(), out: str = OUT) -> str:
+    """Compile every csrc/ source for sm_100a and link the C-ABI library.
+    ``defines`` / ``out``: experiment builds (separate object dir, other .so name)."""
+    objdir = OBJDIR if not defines else OBJDIR + "_" + "_".join(d.replace("=", "") for d in defines)
+    os.makedirs(objdir, exist_ok=True)
     nccl_inc, nccl_lib = _nccl_paths()
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
     headers.append(os.path.join(HERE, "..", "include", "zorse_b200.h"))
@@ -46,13 +49,13 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     cmds = []
     objs = []
     for src in sources:
-        obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
         if _newer(obj, [src] + headers):
             continue
         cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", CSRC, "-I", os.path.join(HERE, "..", "include"), "-I", nccl_inc,
-               "-c", src, "-o", obj]
+               *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
         cmds.append(cmd)
@@ -64,13 +67,13 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
         if len(procs) >= jobs:
             _drain(procs, verbose)
     _drain(procs, verbose)
-    if cmds or not os.path.exists(OUT):
-        link = ["nvcc", *ARCH, "-shared", "-o", OUT, *objs, "-L", nccl_lib, "-l:libnccl.so.2",
+    if cmds or not os.path.exists(out):
+        link = ["nvcc", *ARCH, "-shared", "-o", out, *objs, "-L", nccl_lib, "-l:libnccl.so.2",
                 "-Xlinker", "-rpath", "-Xlinker", nccl_lib, "-lcudart"]
         if verbose:
             print(" ".join(link), flush=True)
         subprocess.run(link, check=True)
-    return OUT
+    return out
 
 
 def _drain(procs, verbose):

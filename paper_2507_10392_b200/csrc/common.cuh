@@ -42,9 +42,11 @@ ZB_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a barrier that never completes (a bug, or a peer that died)
-// reports and traps after ~20 s instead of hanging the GPU.  The timing loop is
-// out of line so the hot path stays a single try_wait.
+// Debug builds (-DZB_WAIT_TIMEOUT, e.g. build(defines=("ZB_WAIT_TIMEOUT",))):
+// a barrier that never completes reports and traps after ~20 s instead of
+// hanging the GPU.  Off by default: even out of line, the check costs ~10% of
+// the attention kernels' throughput (measured, profiles/r01_attention_bench_*).
+#ifdef ZB_WAIT_TIMEOUT
 static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
   uint64_t t0;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
@@ -61,8 +63,14 @@ static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parit
     }
   }
 }
+#endif
 ZB_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef ZB_WAIT_TIMEOUT
   if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
+#else
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#endif
 }
 
 // ---------------------------------------------------------------- TMA
