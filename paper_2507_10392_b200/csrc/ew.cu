@@ -84,48 +84,64 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
     const __nv_bfloat16* __restrict__ w, const float* __restrict__ mean_in,
     const float* __restrict__ rstd_in, __nv_bfloat16* dx, float* __restrict__ dw,
     float* __restrict__ db, const __nv_bfloat16* dres, int rows, int d) {
-  extern __shared__ float sh[];  // [2*d]
-  float* sdw = sh;
-  float* sdb = sh + d;
-  for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) sh[i] = 0.f;
-  __syncthreads();
+  extern __shared__ float sh[];  // [16][warps][32] block-reduction staging
   const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nv = d >> 3;
+  // Small rows (MAXV <= 4, d <= 1024): w stays in registers and the next row's
+  // dy / x loads are in flight while this row computes.  Wider rows would spill,
+  // so they reload w through L1 and do not prefetch.
+  constexpr bool kPipe = MAXV <= 4;
+  uint4 qw[MAXV];
   const uint4* wr = reinterpret_cast<const uint4*>(w);
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    const int v = lane + 32 * j;
+    qw[j] = v < nv ? wr[v] : make_uint4(0, 0, 0, 0);
+  }
   float adw[MAXV][8], adb[MAXV][8];
 #pragma unroll
   for (int j = 0; j < MAXV; ++j)
 #pragma unroll
     for (int k = 0; k < 8; ++k) adw[j][k] = adb[j][k] = 0.f;
-  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
-    const uint4* dyr = reinterpret_cast<const uint4*>(dy + (size_t)row * d);
-    const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * d);
-    const float mean = mean_in[row], rstd = rstd_in[row];
-    uint4 qd[MAXV], qx[MAXV];
-    float sg = 0.f, sgx = 0.f;
+  const int stride = gridDim.x * warps;
+  int row = blockIdx.x * warps + warp;
+  // software pipeline: the next row's dy / x are in flight while this row computes
+  uint4 qd[MAXV], qx[MAXV];
+  auto load = [&](int r, uint4* a, uint4* b) {
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + (size_t)r * d);
+    const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)r * d);
 #pragma unroll
     for (int j = 0; j < MAXV; ++j) {
       const int v = lane + 32 * j;
-      qd[j] = make_uint4(0, 0, 0, 0);
-      qx[j] = make_uint4(0, 0, 0, 0);
-      if (v < nv) {
-        qd[j] = dyr[v];
-        qx[j] = xr[v];
-        const uint4 qw = wr[v];
-        const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw.x;
+      a[j] = v < nv ? dyr[v] : make_uint4(0, 0, 0, 0);
+      b[j] = v < nv ? xr[v] : make_uint4(0, 0, 0, 0);
+    }
+  };
+  if (row < rows) load(row, qd, qx);
+  for (; row < rows; row += stride) {
+    const int next = row + stride;
+    uint4 nd[kPipe ? MAXV : 1], nx[kPipe ? MAXV : 1];
+    if constexpr (kPipe) {
+      if (next < rows) load(next, nd, nx);
+    }
+    const float mean = mean_in[row], rstd = rstd_in[row];
+    float sg = 0.f, sgx = 0.f;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
-          const float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
-          const float g0 = dv.x * wv.x, g1 = dv.y * wv.y;
-          adw[j][2 * k] += dv.x * h0;
-          adw[j][2 * k + 1] += dv.y * h1;
-          adb[j][2 * k] += dv.x;
-          adb[j][2 * k + 1] += dv.y;
-          sg += g0 + g1;
-          sgx += g0 * h0 + g1 * h1;
-        }
+    for (int j = 0; j < MAXV; ++j) {
+      const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw[j].x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
+        const float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
+        const float g0 = dv.x * wv.x, g1 = dv.y * wv.y;
+        adw[j][2 * k] += dv.x * h0;
+        adw[j][2 * k + 1] += dv.y * h1;
+        adb[j][2 * k] += dv.x;
+        adb[j][2 * k + 1] += dv.y;
+        sg += g0 + g1;
+        sgx += g0 * h0 + g1 * h1;
       }
     }
     const float mg = warp_sum(sg) / d, mgx = warp_sum(sgx) / d;
@@ -135,9 +151,8 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
     for (int j = 0; j < MAXV; ++j) {
       const int v = lane + 32 * j;
       if (v >= nv) continue;
-      const uint4 qw = wr[v];
       const uint4 qr = rr ? rr[v] : make_uint4(0, 0, 0, 0);
-      const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw.x, *ri = &qr.x;
+      const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw[j].x, *ri = &qr.x;
       uint4 o;
       uint32_t* oi = &o.x;
 #pragma unroll
@@ -151,21 +166,37 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
       }
       dxr[v] = o;
     }
-  }
+    if constexpr (kPipe) {
 #pragma unroll
-  for (int j = 0; j < MAXV; ++j) {
-    const int v = lane + 32 * j;
-    if (v >= nv) continue;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      atomicAdd(&sdw[v * 8 + k], adw[j][k]);
-      atomicAdd(&sdb[v * 8 + k], adb[j][k]);
+      for (int j = 0; j < MAXV; ++j) {
+        qd[j] = nd[j];
+        qx[j] = nx[j];
+      }
+    } else if (next < rows) {
+      load(next, qd, qx);
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    atomicAdd(&dw[i], sdw[i]);
-    atomicAdd(&db[i], sdb[i]);
+  // Block reduction of the per-lane partials without shared-memory atomics:
+  // per column group j, stage [16 values][warp][lane], sum over warps, one
+  // global atomic per column and block.
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    if (j) __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      sh[(k * warps + warp) * 32 + lane] = adw[j][k];
+      sh[((8 + k) * warps + warp) * 32 + lane] = adb[j][k];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 16 * 32; idx += blockDim.x) {
+      const int k = idx >> 5, ln = idx & 31;
+      const int v = ln + 32 * j;
+      if (v >= nv) continue;
+      float t = 0.f;
+      for (int wi = 0; wi < warps; ++wi) t += sh[(k * warps + wi) * 32 + ln];
+      float* dst = k < 8 ? dw + v * 8 + k : db + v * 8 + (k - 8);
+      atomicAdd(dst, t);
+    }
   }
 }
 
@@ -418,9 +449,11 @@ extern "C" int zb_layernorm_bwd(const void* dy, const void* x, const void* w, co
   if (d > 5120) return set_error(ZB_ERR_UNSUPPORTED, "layernorm_bwd: d > 5120");
   if (rows <= 0) return 0;
   const int threads = 256, per = threads / 32;
-  int blocks = (rows + per * 8 - 1) / (per * 8);  // >= 8 rows per warp amortises the reduction
-  if (blocks > 2 * num_sms()) blocks = 2 * num_sms();
-  const size_t smem = 2 * (size_t)d * sizeof(float);
+  // One CTA per SM (measured: more CTAs lose to the per-CTA reduction), each warp
+  // walking rows with the next row's loads in flight.
+  int blocks = (rows + per - 1) / per;
+  if (blocks > num_sms()) blocks = num_sms();
+  const size_t smem = 16 * (size_t)per * 32 * sizeof(float);
   const int vpl = (d / 8 + 31) / 32;  // column vectors per lane
   auto go = [&](auto kern) {
     if (smem > 48 * 1024)

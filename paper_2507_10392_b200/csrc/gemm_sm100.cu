@@ -22,7 +22,13 @@
 #include "common.cuh"
 #include "zb_internal.h"
 
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
+#include <tuple>
+#include <mutex>
+#include <map>
 
 namespace zb {
 
@@ -48,6 +54,7 @@ struct GemmArgs {
   int num_m_tiles, num_n_tiles;
   int splits;      // K splits (1 unless EPI_F32 with beta == 1)
   int kb_per_split;
+  int tma_epi;     // 1: TMA-store epilogue (aligned C / R / aux, beta in {0, 1})
 };
 
 constexpr int BM = 128;
@@ -64,9 +71,10 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 192 ? 5 : 6);
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 192 ? 4 : 6);
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;  // two accumulators, pow2 alloc
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BYTES = 8 * 4096;  // per-epilogue-warp TMA staging
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 // Apply the epilogue to 32 consecutive accumulator columns of one row and store.
@@ -194,10 +202,177 @@ ZB_DEVICE void epilogue_chunk(const GemmArgs& args, const uint32_t (&r)[32], int
   }
 }
 
+// ---------------------------------------------------------------- TMA epilogue
+// Each epilogue warp owns a 32-row slab of the tile and drains it in 32-column
+// chunks through a 4 KB shared staging area (two 2 KB slots): the thread of row r
+// writes its 64-byte (bf16) or 128-byte (fp32) row of the chunk into the slot in
+// the TMA swizzle layout (conflict-free), and one lane issues a TMA tile store —
+// or, for fp32 accumulation (beta = 1 / split-K), a TMA reduce-add store — so the
+// global writes leave the SM as full lines instead of 32 row-strided 16-byte
+// pieces per instruction.  Residual / GELU-backward operands are TMA-loaded into
+// the slot (prefetched one chunk ahead) and read back from shared memory.
+constexpr int kEpiSlot = 2048;
+constexpr int kEpiWarpBytes = 2 * kEpiSlot;
+
+struct EpiMaps {
+  const CUtensorMap* C;
+  const CUtensorMap* aux;
+  const CUtensorMap* R;
+};
+
+// byte offset of 16-byte chunk j of row r in a [32 rows][64 B] SWIZZLE_64B box
+ZB_DEVICE uint32_t sw64(int r, int j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
+// ... and in a [32 rows][128 B] SWIZZLE_128B box
+ZB_DEVICE uint32_t sw128(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
+
+ZB_DEVICE void st_row_bf16(uint8_t* slot, int r, const float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 q;
+    q.x = pack_bf16(v[8 * j], v[8 * j + 1]);
+    q.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+    q.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+    q.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+    *reinterpret_cast<uint4*>(slot + sw64(r, j)) = q;
+  }
+}
+
+ZB_DEVICE void ld_row_bf16(const uint8_t* slot, int r, float (&o)[32]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 q = *reinterpret_cast<const uint4*>(slot + sw64(r, j));
+    float2 f0 = unpack_bf16(q.x), f1 = unpack_bf16(q.y), f2 = unpack_bf16(q.z), f3 = unpack_bf16(q.w);
+    o[8 * j] = f0.x; o[8 * j + 1] = f0.y; o[8 * j + 2] = f1.x; o[8 * j + 3] = f1.y;
+    o[8 * j + 4] = f2.x; o[8 * j + 5] = f2.y; o[8 * j + 6] = f3.x; o[8 * j + 7] = f3.y;
+  }
+}
+
+// Drain one accumulator slab.  tacc = TMEM address of column 0 of this warp's lane
+// quarter in the accumulator; chunks [cb, ce) of 32 columns; row0 / n0 = global
+// coordinates of the slab's first row / the tile's first column.  `release` is
+// called once the last TMEM read retired (the accumulator may be reused).
+template <int EPI, typename Release>
+ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* stg,
+                            uint64_t* ebar, uint32_t& eph, uint32_t& ecnt, uint32_t tacc,
+                            uint64_t* tfull,
+                            uint32_t tfull_parity, int row0, int n0, int cb, int ce, int lane,
+                            Release release) {
+  constexpr bool LOADS = (EPI == EPI_BIAS_RESID || EPI == EPI_RESID || EPI == EPI_GELU_BWD);
+  const CUtensorMap* tm_in = EPI == EPI_GELU_BWD ? maps.aux : maps.R;
+  // Prefetch the first chunk's residual / aux operand before the accumulator is ready.
+  if (LOADS) {
+    if (lane == 0) {
+      bulk_wait_read<0>();
+      mbar_arrive_expect_tx(&ebar[0], kEpiSlot);
+      tma_load_2d(stg, tm_in, &ebar[0], n0 + cb * 32, row0);
+    }
+  }
+  mbar_wait(tfull, tfull_parity);
+  tc_fence_after();
+#pragma unroll 1
+  for (int c = cb; c < ce; ++c) {
+    const int k = c - cb;
+    const int col0 = n0 + c * 32;
+    uint8_t* slot = stg + (k & 1) * kEpiSlot;  // LOADS path: per-tile slot order
+    if (LOADS && c + 1 < ce && lane == 0) {  // prefetch the next chunk into the other slot
+      bulk_wait_read<0>();
+      const int ns = (k + 1) & 1;
+      mbar_arrive_expect_tx(&ebar[ns], kEpiSlot);
+      tma_load_2d(stg + ns * kEpiSlot, tm_in, &ebar[ns], col0 + 32, row0);
+    }
+    __syncwarp();
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tacc + c * 32, r);
+    tmem_ld_wait();
+    if (c + 1 == ce) {
+      tc_fence_before();
+      __syncwarp();
+      release();
+    }
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID) {
+      if (col0 + 32 <= args.N) {
+        const uint4* bp = reinterpret_cast<const uint4*>(args.bias + col0);
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          const uint4 q = bp[j / 8];
+          float2 f0 = unpack_bf16(q.x), f1 = unpack_bf16(q.y), f2 = unpack_bf16(q.z),
+                 f3 = unpack_bf16(q.w);
+          v[j] += f0.x; v[j + 1] += f0.y; v[j + 2] += f1.x; v[j + 3] += f1.y;
+          v[j + 4] += f2.x; v[j + 5] += f2.y; v[j + 6] += f3.x; v[j + 7] += f3.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < args.N) v[j] += __bfloat162float(args.bias[col0 + j]);
+      }
+    }
+    if (LOADS) {
+      const int bs = k & 1;
+      mbar_wait(&ebar[bs], (eph >> bs) & 1);
+      eph ^= 1u << bs;
+      float in[32];
+      ld_row_bf16(slot, lane, in);
+      if (EPI == EPI_GELU_BWD) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= gelu_tanh_grad(in[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += in[j];
+      }
+      st_row_bf16(slot, lane, v);   // in place: each thread rewrites only its own row
+    } else if (EPI == EPI_F32) {
+      if (lane == 0) bulk_wait_read<0>();  // one 4 KB slot
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<float4*>(stg + sw128(lane, j)) =
+            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    } else if (EPI == EPI_BIAS_GELU) {
+      if (lane == 0) bulk_wait_read<0>();  // aux -> slot 0, C -> slot 1
+      __syncwarp();
+      st_row_bf16(stg, lane, v);
+      // GELU of the bf16-rounded pre-activation, so forward and backward agree.
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
+      st_row_bf16(stg + kEpiSlot, lane, v);
+    } else {
+      // slots alternate over a running chunk count (across tiles), so the slot
+      // written now was last stored two chunks ago
+      slot = stg + (ecnt & 1) * kEpiSlot;
+      ++ecnt;
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      st_row_bf16(slot, lane, v);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (EPI == EPI_F32) {
+        if (args.splits > 1 || args.beta != 0.f)
+          tma_reduce_add_2d(maps.C, stg, col0, row0);
+        else
+          tma_store_2d(maps.C, stg, col0, row0);
+      } else if (EPI == EPI_BIAS_GELU) {
+        tma_store_2d(maps.aux, stg, col0, row0);
+        tma_store_2d(maps.C, stg + kEpiSlot, col0, row0);
+      } else {
+        tma_store_2d(maps.C, slot, col0, row0);
+      }
+      bulk_commit();
+    }
+  }
+}
+
 template <int BN, int A_MN, int B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
+                      const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmC,
+                      const __grid_constant__ CUtensorMap tmAux,
+                      const __grid_constant__ CUtensorMap tmR, GemmArgs args) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -207,11 +382,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + pad;
   uint8_t* smA = smem;
   uint8_t* smB = smem + S * Cfg::A_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
+  uint8_t* smE = smem + S * Cfg::STAGE_BYTES;  // epilogue staging, 4 KB per warp
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smE + Cfg::EPI_BYTES);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* epi_bar = tempty_bar + 2;  // [8 warps][2 slots]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_bar + 2 * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -230,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], kEpiWarps);  // one arrive per epilogue warp
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&epi_bar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -321,6 +499,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = (warp - 4) & 3;     // TMEM lane quarter this warp may access
     const int half = (warp - 4) >> 2;  // which half of the tile's columns it drains
     int local = 0;
+    if (args.tma_epi) {
+      const EpiMaps maps{&tmC, &tmAux, &tmR};
+      uint8_t* stg = smE + (warp - 4) * kEpiWarpBytes;
+      uint64_t* ebar = epi_bar + 2 * (warp - 4);
+      uint32_t eph = 0, ecnt = 0;
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
+        const int tile = unit % num_tiles;
+        const int acc = local & 1;
+        const int m0 = (tile % args.num_m_tiles) * BM;
+        const int n0 = (tile / args.num_m_tiles) * BN;
+        epilogue_tma<EPI>(args, maps, stg, ebar, eph, ecnt,
+                          tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN, &tfull_bar[acc],
+                          (local >> 1) & 1, m0 + ew * 32, n0, half * (BN / 64),
+                          (half + 1) * (BN / 64), lane,
+                          [&] { if (lane == 0) mbar_arrive(&tempty_bar[acc]); });
+      }
+      if (lane == 0) bulk_wait_all();
+    } else
     for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
       const int tile = unit % num_tiles;
       const int acc = local & 1;
@@ -364,15 +560,19 @@ struct Gemm2Cfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 6 : (BN == 192 ? 7 : 8);
+  static constexpr int STAGES = (BN == 256) ? 6 : (BN == 192 ? 6 : 8);
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_BYTES = 8 * 4096;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
 };
 
 template <int BN, int A_MN, int B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2cta_kernel(const __grid_constant__ CUtensorMap tmA,
-                    const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
+                    const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmC,
+                    const __grid_constant__ CUtensorMap tmAux,
+                    const __grid_constant__ CUtensorMap tmR, GemmArgs args) {
   using Cfg = Gemm2Cfg<BN>;
   constexpr int S = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -380,11 +580,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((base + 1023u) & ~1023u) - base);
   uint8_t* smA = smem;
   uint8_t* smB = smem + S * Cfg::A_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
+  uint8_t* smE = smem + S * Cfg::STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smE + Cfg::EPI_BYTES);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* epi_bar = tempty_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_bar + 2 * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -406,6 +608,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], 2 * kEpiWarps);  // both CTAs' epilogue warps (leader's copy)
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&epi_bar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_2cta(tmem_slot, Cfg::TMEM_COLS);
@@ -495,6 +698,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int ew = (warp - 4) & 3;
     const int half = (warp - 4) >> 2;
     int local = 0;
+    if (args.tma_epi) {
+      const EpiMaps maps{&tmC, &tmAux, &tmR};
+      uint8_t* stg = smE + (warp - 4) * kEpiWarpBytes;
+      uint64_t* ebar = epi_bar + 2 * (warp - 4);
+      uint32_t eph = 0, ecnt = 0;
+      for (int unit = cluster; unit < num_units; unit += nclusters, ++local) {
+        const int tile = unit % num_tiles;
+        const int acc = local & 1;
+        const int m0 = (tile % args.num_m_tiles) * 256 + (int)rank * 128;
+        const int n0 = (tile / args.num_m_tiles) * BN;
+        epilogue_tma<EPI>(args, maps, stg, ebar, eph, ecnt,
+                          tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN, &tfull_bar[acc],
+                          (local >> 1) & 1, m0 + ew * 32, n0, half * (BN / 64),
+                          (half + 1) * (BN / 64), lane, [&] {
+                            if (lane == 0) {
+                              if (leader)
+                                mbar_arrive(&tempty_bar[acc]);
+                              else
+                                mbar_arrive_remote(&tempty_bar[acc], 0);
+                            }
+                          });
+      }
+      if (lane == 0) bulk_wait_all();
+    } else
     for (int unit = cluster; unit < num_units; unit += nclusters, ++local) {
       const int tile = unit % num_tiles;
       const int acc = local & 1;
@@ -547,9 +774,28 @@ static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
+struct EpiTm {
+  CUtensorMap c, aux, r;
+};
+
+// Epilogue tile map: {32 columns, 32 rows} box; bf16 rows of 64 B use the 64-byte
+// swizzle, fp32 rows of 128 B the 128-byte swizzle (see sw64 / sw128).
+static int make_tmap_epi(CUtensorMap* m, const void* ptr, bool f32, uint64_t cols, uint64_t rows,
+                         uint64_t ld) {
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * (f32 ? 4 : 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return tensor_map_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
 template <int BN, int A_MN, int B_MN, int EPI>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs args,
-                       cudaStream_t stream) {
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm& et,
+                       GemmArgs args, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_sm100_kernel<BN, A_MN, B_MN, EPI>;
   static bool configured = false;
@@ -563,26 +809,52 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs ar
   args.num_n_tiles = (args.N + BN - 1) / BN;
   const int tiles = args.num_m_tiles * args.num_n_tiles;
   const int num_kb = (args.K + BK - 1) / BK;
-  int splits = 1;
-  if (EPI == EPI_F32 && args.beta == 1.f && tiles < num_sms()) {
-    // split K so that at least ~2 waves of (tile, split) units exist, >= 8 k-blocks each
-    splits = (2 * num_sms() + tiles - 1) / tiles;
-    int cap = num_kb / 8;
-    if (splits > cap) splits = cap > 1 ? cap : 1;
-  }
+  const int splits = (EPI == EPI_F32 && args.beta == 1.f) ? (args.splits > 0 ? args.splits : 1) : 1;
   args.kb_per_split = (num_kb + splits - 1) / splits;
   args.splits = (num_kb + args.kb_per_split - 1) / args.kb_per_split;
   const int units = tiles * args.splits;
   int grid = units < num_sms() ? units : num_sms();
-  kern<<<grid, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, args);
+  kern<<<grid, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, et.c, et.aux, et.r, args);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   return 0;
 }
 
+// Co-resident 2-CTA clusters for a kernel with `smem` bytes of dynamic shared memory.
+static int max_active_pairs(const void* kern, int smem) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(2 * (num_sms() / 2));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = num_sms() / 2;
+  }
+  return n < num_sms() / 2 ? n : num_sms() / 2;
+}
+
+// Slots for the tile cost model (all 2-CTA configurations use ~225 KB of smem).
+static int pair_slots() {
+  static int n = 0;
+  if (!n) {
+    auto k = gemm2cta_kernel<256, 0, 0, EPI_BF16>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg<256>::SMEM_BYTES);
+    n = max_active_pairs((const void*)k, Gemm2Cfg<256>::SMEM_BYTES);
+  }
+  return n;
+}
+
 template <int BN, int A_MN, int B_MN, int EPI>
-static int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs args,
-                        cudaStream_t stream) {
+static int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm& et,
+                        GemmArgs args, cudaStream_t stream) {
   using Cfg = Gemm2Cfg<BN>;
   auto kern = gemm2cta_kernel<BN, A_MN, B_MN, EPI>;
   static bool configured = false;
@@ -596,55 +868,282 @@ static int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a
   args.num_n_tiles = (args.N + BN - 1) / BN;
   const int tiles = args.num_m_tiles * args.num_n_tiles;
   const int num_kb = (args.K + BK - 1) / BK;
-  const int pairs = num_sms() / 2;
-  int splits = 1;
-  if (EPI == EPI_F32 && args.beta == 1.f && tiles < pairs) {
-    splits = (2 * pairs + tiles - 1) / tiles;
-    int cap = num_kb / 8;
-    if (splits > cap) splits = cap > 1 ? cap : 1;
-  }
+  // A persistent grid must be fully co-resident: not every SM pair can host a
+  // cluster (GPC shapes), so ask the occupancy API instead of assuming sms / 2.
+  static int max_clusters = 0;
+  if (!max_clusters) max_clusters = max_active_pairs((const void*)kern, Cfg::SMEM_BYTES);
+  const int pairs = max_clusters;
+  const int splits = (EPI == EPI_F32 && args.beta == 1.f) ? (args.splits > 0 ? args.splits : 1) : 1;
   args.kb_per_split = (num_kb + splits - 1) / splits;
   args.splits = (num_kb + args.kb_per_split - 1) / args.kb_per_split;
   const int units = tiles * args.splits;
   const int clusters = units < pairs ? units : pairs;
-  kern<<<2 * clusters, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, args);
+  kern<<<2 * clusters, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, et.c, et.aux, et.r, args);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "gemm2cta launch");
   return 0;
 }
 
 template <int BN, int A_MN, int B_MN>
-static int dispatch_epi2(int epi, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs args,
-                         cudaStream_t s) {
+static int dispatch_epi2(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm& et,
+                         GemmArgs args, cudaStream_t s) {
   switch (epi) {
-    case EPI_BF16: return launch_gemm2<BN, A_MN, B_MN, EPI_BF16>(ta, tb, args, s);
-    case EPI_BIAS: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS>(ta, tb, args, s);
-    case EPI_BIAS_GELU: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_GELU>(ta, tb, args, s);
-    case EPI_BIAS_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_RESID>(ta, tb, args, s);
-    case EPI_GELU_BWD: return launch_gemm2<BN, A_MN, B_MN, EPI_GELU_BWD>(ta, tb, args, s);
-    case EPI_F32: return launch_gemm2<BN, A_MN, B_MN, EPI_F32>(ta, tb, args, s);
-    case EPI_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_RESID>(ta, tb, args, s);
+    case EPI_BF16: return launch_gemm2<BN, A_MN, B_MN, EPI_BF16>(ta, tb, et, args, s);
+    case EPI_BIAS: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS>(ta, tb, et, args, s);
+    case EPI_BIAS_GELU: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_GELU>(ta, tb, et, args, s);
+    case EPI_BIAS_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_RESID>(ta, tb, et, args, s);
+    case EPI_GELU_BWD: return launch_gemm2<BN, A_MN, B_MN, EPI_GELU_BWD>(ta, tb, et, args, s);
+    case EPI_F32: return launch_gemm2<BN, A_MN, B_MN, EPI_F32>(ta, tb, et, args, s);
+    case EPI_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_RESID>(ta, tb, et, args, s);
   }
   return set_error(ZB_ERR_INVALID, "gemm: unknown epilogue %d", epi);
 }
 
 template <int BN, int A_MN, int B_MN>
-static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs args,
-                        cudaStream_t s) {
+static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm& et,
+                         GemmArgs args, cudaStream_t s) {
   switch (epi) {
-    case EPI_BF16: return launch_gemm<BN, A_MN, B_MN, EPI_BF16>(ta, tb, args, s);
-    case EPI_BIAS: return launch_gemm<BN, A_MN, B_MN, EPI_BIAS>(ta, tb, args, s);
-    case EPI_BIAS_GELU: return launch_gemm<BN, A_MN, B_MN, EPI_BIAS_GELU>(ta, tb, args, s);
-    case EPI_BIAS_RESID: return launch_gemm<BN, A_MN, B_MN, EPI_BIAS_RESID>(ta, tb, args, s);
-    case EPI_GELU_BWD: return launch_gemm<BN, A_MN, B_MN, EPI_GELU_BWD>(ta, tb, args, s);
-    case EPI_F32: return launch_gemm<BN, A_MN, B_MN, EPI_F32>(ta, tb, args, s);
-    case EPI_RESID: return launch_gemm<BN, A_MN, B_MN, EPI_RESID>(ta, tb, args, s);
+    case EPI_BF16: return launch_gemm<BN, A_MN, B_MN, EPI_BF16>(ta, tb, et, args, s);
+    case EPI_BIAS: return launch_gemm<BN, A_MN, B_MN, EPI_BIAS>(ta, tb, et, args, s);
+    case EPI_BIAS_GELU: return launch_gemm<BN, A_MN, B_MN, EPI_BIAS_GELU>(ta, tb, et, args, s);
+    case EPI_BIAS_RESID: return launch_gemm<BN, A_MN, B_MN, EPI_BIAS_RESID>(ta, tb, et, args, s);
+    case EPI_GELU_BWD: return launch_gemm<BN, A_MN, B_MN, EPI_GELU_BWD>(ta, tb, et, args, s);
+    case EPI_F32: return launch_gemm<BN, A_MN, B_MN, EPI_F32>(ta, tb, et, args, s);
+    case EPI_RESID: return launch_gemm<BN, A_MN, B_MN, EPI_RESID>(ta, tb, et, args, s);
   }
   return set_error(ZB_ERR_INVALID, "gemm: unknown epilogue %d", epi);
 }
 
-}  // namespace zb
+// ---------------------------------------------------------------- tile selection
+struct GemmChoice {
+  int pair, bn, splits;
+};
 
+// Wave-quantisation cost model (SM cycles), calibrated on B200 (scripts/gemm_sweep.py,
+// profiles/r01_gemm_sweep.jsonl): per k-block a 128 x BN tile costs 512 / 400 / 360
+// cycles for BN = 256 / 192 / 128 (smaller tiles are operand-bandwidth bound), a
+// 256 x BN CTA-pair tile 480 / 380 per SM; each (tile, K-split) unit adds fill /
+// drain; fp32 accumulation (beta = 1) may split K and pays the TMA reduce-add of
+// every split's partial tile at ~1500 B/cycle of L2 reduction bandwidth.
+static GemmChoice model_choice(int M, int N, int K, int a_mn, int b_mn, int epilogue, float beta,
+                               int force) {
+  GemmChoice best_c{0, 256, 1};
+  const bool pair_ok = force == 2 || (kPairTilesDefault && force != 1 && M >= 256 &&
+                                      !(b_mn && !a_mn));
+  const int sms = num_sms();
+  const int nkb = (K + BK - 1) / BK;
+  const bool can_split = epilogue == EPI_F32 && beta == 1.f;
+  const int max_s = can_split ? (nkb / 4 < 16 ? (nkb / 4 > 1 ? nkb / 4 : 1) : 16) : 1;
+  double best = 1e30;
+  for (int two = 0; two <= 1; ++two) {
+    if (two && (!pair_ok || M < 256)) continue;
+    if (!two && force == 2 && M >= 256) continue;
+    for (int bn : {256, 192, 128}) {
+      if (two && bn == 128) continue;
+      if (two && b_mn && bn == 192) continue;  // MN-major half-tiles must be 64-multiples
+      const long long t = (long long)((M + (two ? 255 : 127)) / (two ? 256 : 128)) * ((N + bn - 1) / bn);
+      const long long slots = two ? pair_slots() : sms;
+      const double per = two ? (bn == 256 ? 480.0 : 380.0)
+                             : (bn == 256 ? 512.0 : (bn == 192 ? 400.0 : 360.0));
+      const double fixed = two ? 2000.0 : 800.0;
+      for (int sp = 1; sp <= max_s; ++sp) {
+        const long long units = t * sp;
+        const long long waves = (units + slots - 1) / slots;
+        const int kbs = (nkb + sp - 1) / sp;
+        double cost = waves * (kbs * per + fixed);
+        if (can_split) cost += (double)sp * M * N * 4.0 / 1500.0;
+        if (cost < best - 1e-9) {
+          best = cost;
+          best_c = {two, bn, sp};
+        }
+      }
+    }
+  }
+  if (N <= 128 && !best_c.pair) best_c.bn = 128;
+  return best_c;
+}
+
+struct GemmKey {
+  int M, N, K, a_mn, b_mn, epi, beta1, ldc;
+  bool operator<(const GemmKey& o) const {
+    return std::tie(M, N, K, a_mn, b_mn, epi, beta1, ldc) <
+           std::tie(o.M, o.N, o.K, o.a_mn, o.b_mn, o.epi, o.beta1, o.ldc);
+  }
+};
+static std::mutex g_tune_mu;
+static std::map<GemmKey, GemmChoice> g_tuned;
+
+struct GemmCall {
+  const void *A, *B, *bias, *R;
+  int M, N, K, lda, ldb, ldc, ldr, ldaux, a_mn, b_mn, epilogue;
+  float beta;
+};
+
+static int launch_choice(const GemmCall& g, const GemmChoice& ch, void* C, void* aux,
+                         cudaStream_t stream) {
+  const int BN = ch.bn, pair = ch.pair;
+  CUtensorMap ta, tb;
+  int rc;
+  if (g.a_mn)
+    rc = make_tmap(&ta, g.A, (uint64_t)g.M, (uint64_t)g.K, (uint64_t)g.lda, BK);
+  else
+    rc = make_tmap(&ta, g.A, (uint64_t)g.K, (uint64_t)g.M, (uint64_t)g.lda, BM);
+  if (rc) return rc;
+  if (g.b_mn)
+    rc = make_tmap(&tb, g.B, (uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.ldb, BK);
+  else
+    rc = make_tmap(&tb, g.B, (uint64_t)g.K, (uint64_t)g.N, (uint64_t)g.ldb,
+                   (uint32_t)(pair ? BN / 2 : BN));
+  if (rc) return rc;
+  GemmArgs args{};
+  args.C = C;
+  args.bias = reinterpret_cast<const __nv_bfloat16*>(g.bias);
+  args.R = reinterpret_cast<const __nv_bfloat16*>(g.R);
+  args.aux = reinterpret_cast<__nv_bfloat16*>(aux);
+  args.M = g.M; args.N = g.N; args.K = g.K;
+  args.ldc = g.ldc; args.ldr = g.ldr; args.ldaux = g.ldaux;
+  args.beta = g.beta;
+  args.splits = ch.splits;
+  const int epilogue = g.epilogue;
+  {
+    const int celem = (epilogue == EPI_F32) ? 4 : 8;  // elements per 16 bytes
+    bool v = (g.ldc % celem) == 0 && ((uintptr_t)C & 15) == 0;
+    if (g.R) v = v && (g.ldr % 8) == 0 && ((uintptr_t)g.R & 15) == 0;
+    if (aux) v = v && (g.ldaux % 8) == 0 && ((uintptr_t)aux & 15) == 0;
+    if (g.bias) v = v && ((uintptr_t)g.bias & 15) == 0;
+    args.vec = v ? 1 : 0;
+  }
+  // TMA-store epilogue: C / aux / R tile maps with a {32 cols, 32 rows} box (64-byte
+  // swizzle for bf16 rows, 128-byte for fp32).  Needs 16-byte aligned bases and
+  // pitches, and fp32 accumulation only as beta in {0, 1} (TMA reduce-add).
+  EpiTm et;
+  std::memset(&et, 0, sizeof(et));
+  {
+    const bool f32 = epilogue == EPI_F32;
+    const int esz = f32 ? 4 : 2;
+    bool ok = ((uintptr_t)C & 15) == 0 && ((size_t)g.ldc * esz) % 16 == 0;
+    if (f32) ok = ok && (g.beta == 0.f || g.beta == 1.f);
+    if (aux) ok = ok && ((uintptr_t)aux & 15) == 0 && (g.ldaux % 8) == 0;
+    if (g.R) ok = ok && ((uintptr_t)g.R & 15) == 0 && (g.ldr % 8) == 0;
+    if (epilogue == EPI_BIAS_GELU || epilogue == EPI_GELU_BWD) ok = ok && aux;
+    if (epilogue == EPI_BIAS_RESID || epilogue == EPI_RESID) ok = ok && g.R;
+    if (ok && getenv("ZB_GEMM_NO_TMA_EPI")) ok = false;
+    if (ok) {
+      int rc2 = make_tmap_epi(&et.c, C, f32, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldc);
+      if (!rc2 && aux)
+        rc2 = make_tmap_epi(&et.aux, aux, false, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldaux);
+      if (!rc2 && g.R)
+        rc2 = make_tmap_epi(&et.r, g.R, false, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldr);
+      if (rc2) return rc2;
+    }
+    args.tma_epi = ok ? 1 : 0;
+  }
+  const int key = g.a_mn * 2 + g.b_mn;
+  if (pair) {
+    if (BN == 256) {
+      switch (key) {
+        case 0: return dispatch_epi2<256, 0, 0>(epilogue, ta, tb, et, args, stream);
+        case 1: return dispatch_epi2<256, 0, 1>(epilogue, ta, tb, et, args, stream);
+        case 3: return dispatch_epi2<256, 1, 1>(epilogue, ta, tb, et, args, stream);
+      }
+    } else if (BN == 192) {
+      switch (key) {
+        case 0: return dispatch_epi2<192, 0, 0>(epilogue, ta, tb, et, args, stream);
+      }
+    } else {
+      switch (key) {
+        case 0: return dispatch_epi2<128, 0, 0>(epilogue, ta, tb, et, args, stream);
+        case 1: return dispatch_epi2<128, 0, 1>(epilogue, ta, tb, et, args, stream);
+        case 3: return dispatch_epi2<128, 1, 1>(epilogue, ta, tb, et, args, stream);
+      }
+    }
+    return set_error(ZB_ERR_INVALID, "gemm: unsupported 2-CTA layout");
+  }
+  if (BN == 256) {
+    switch (key) {
+      case 0: return dispatch_epi<256, 0, 0>(epilogue, ta, tb, et, args, stream);
+      case 1: return dispatch_epi<256, 0, 1>(epilogue, ta, tb, et, args, stream);
+      case 3: return dispatch_epi<256, 1, 1>(epilogue, ta, tb, et, args, stream);
+    }
+  } else if (BN == 192) {
+    switch (key) {
+      case 0: return dispatch_epi<192, 0, 0>(epilogue, ta, tb, et, args, stream);
+      case 1: return dispatch_epi<192, 0, 1>(epilogue, ta, tb, et, args, stream);
+      case 3: return dispatch_epi<192, 1, 1>(epilogue, ta, tb, et, args, stream);
+    }
+  } else {
+    switch (key) {
+      case 0: return dispatch_epi<128, 0, 0>(epilogue, ta, tb, et, args, stream);
+      case 1: return dispatch_epi<128, 0, 1>(epilogue, ta, tb, et, args, stream);
+      case 3: return dispatch_epi<128, 1, 1>(epilogue, ta, tb, et, args, stream);
+    }
+  }
+  return set_error(ZB_ERR_INVALID, "gemm: unsupported layout (A MN-major with B K-major)");
+}
+
+// Measured choice: time the model's pick and its neighbours once per shape on
+// scratch outputs (inputs are only read), keep the fastest.  Runs only outside
+// CUDA-graph capture (the first eager step warms every shape); ZB_GEMM_TUNE=0
+// keeps the model's choice.
+static GemmChoice tune_choice(const GemmCall& g, const GemmChoice& model, void* aux_ro,
+                              cudaStream_t stream) {
+  std::vector<GemmChoice> cands{model};
+  const bool can_split = g.epilogue == EPI_F32 && g.beta == 1.f;
+  const int nkb = (g.K + BK - 1) / BK;
+  for (int bn : {256, 192, 128})
+    for (int sp : {1, 2, 4, 8}) {
+      if (sp > 1 && (!can_split || nkb / sp < 4)) continue;
+      cands.push_back({0, bn, sp});
+      if (g.M >= 256 && bn != 128 && !(g.b_mn && !g.a_mn) && !(g.b_mn && bn == 192))
+        cands.push_back({1, bn, sp});
+    }
+  const size_t esz = g.epilogue == EPI_F32 ? 4 : 2;
+  void *c = nullptr, *x = nullptr;
+  // stream-ordered scratch (no device-wide synchronisation while other streams,
+  // e.g. peer collectives, are in flight)
+  if (cudaMallocAsync(&c, (size_t)g.ldc * g.M * esz, stream) != cudaSuccess) {
+    cudaGetLastError();
+    return model;
+  }
+  if (g.epilogue == EPI_BIAS_GELU &&
+      cudaMallocAsync(&x, (size_t)g.ldaux * g.M * 2, stream) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFreeAsync(c, stream);
+    return model;
+  }
+  void* aux = g.epilogue == EPI_BIAS_GELU ? x : nullptr;
+  if (g.epilogue == EPI_GELU_BWD) aux = aux_ro;  // read-only operand
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  GemmChoice best = model;
+  float best_ms = 1e30f;
+  for (const GemmChoice& ch : cands) {
+    bool ok = true;
+    for (int w = 0; w < 2 && ok; ++w) ok = launch_choice(g, ch, c, aux, stream) == 0;
+    if (!ok) continue;
+    cudaEventRecord(e0, stream);
+    for (int it = 0; it < 5 && ok; ++it) ok = launch_choice(g, ch, c, aux, stream) == 0;
+    cudaEventRecord(e1, stream);
+    if (!ok || cudaEventSynchronize(e1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best_ms * 0.98f) {  // keep the model's pick unless clearly beaten
+      best_ms = ms;
+      best = ch;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(c, stream);
+  if (x) cudaFreeAsync(x, stream);
+  return best;
+}
+
+}  // namespace zb
 using namespace zb;
 
 extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* bias,
@@ -656,108 +1155,40 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
     return set_error(ZB_ERR_INVALID, "gemm: lda/ldb must be multiples of 8 elements");
   if (((uintptr_t)A & 15) || ((uintptr_t)B & 15))
     return set_error(ZB_ERR_INVALID, "gemm: A/B must be 16-byte aligned");
-  CUtensorMap ta, tb;
-  // Tile choice by a wave-quantisation cost model: cost = waves x per-tile time per
-  // k-block on one SM = max(MMA 2*BN cycles, smem operand bytes at ~87% of 128 B/cycle).
-  // 1-CTA tiles are 128 x BN on one SM; 2-CTA (cta_group::2) tiles are 256 x BN on an
-  // SM pair, each SM staging 128 rows of A and BN/2 rows of B.
-  int BN = 256, pair = 0;
-  {
-    static int force = -1;  // ZB_GEMM_CTAS=1|2 pins 1-CTA / 2-CTA tiles (benchmarking)
-    if (force < 0) {
-      const char* f = getenv("ZB_GEMM_CTAS");
-      force = f ? atoi(f) : 0;
-    }
-    const bool shape_ok = K >= 2048 && !(b_mn_major && !a_mn_major);
-    const bool allow_pair = force == 2 || (kPairTilesDefault && force != 1 && shape_ok);
-    const int sms = num_sms();
-    double best = 1e30;
-    for (int two = 1; two >= 0; --two) {
-      if (two && (M < 256 || !allow_pair)) continue;
-      if (!two && force == 2 && M >= 256) continue;
-      for (int bn : {256, 192, 128}) {
-        if (two && b_mn_major && bn == 192) continue;  // MN-major half-tiles must be 64-multiples
-        const long long t = (long long)((M + (two ? 255 : 127)) / (two ? 256 : 128)) * ((N + bn - 1) / bn);
-        const long long slots = two ? sms / 2 : sms;
-        const long long waves = (t + slots - 1) / slots;
-        const double smem_cyc = 1.15 * (128 + (two ? bn / 2 : bn));
-        const double per = 2.0 * bn > smem_cyc ? 2.0 * bn : smem_cyc;
-        const double cost = waves * per;
-        if (cost < best - 1e-9) {
-          best = cost;
-          BN = bn;
-          pair = two;
-        }
-      }
-    }
-    if (N <= 128) BN = 128;
-  }
-  int rc;
-  if (a_mn_major)
-    rc = make_tmap(&ta, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, BK);
-  else
-    rc = make_tmap(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BM);
-  if (rc) return rc;
-  if (b_mn_major)
-    rc = make_tmap(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BK);
-  else
-    rc = make_tmap(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, (uint32_t)(pair ? BN / 2 : BN));
-  if (rc) return rc;
-  GemmArgs args{};
-  args.C = C;
-  args.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
-  args.R = reinterpret_cast<const __nv_bfloat16*>(R);
-  args.aux = reinterpret_cast<__nv_bfloat16*>(aux);
-  args.M = M; args.N = N; args.K = K;
-  args.ldc = ldc; args.ldr = ldr; args.ldaux = ldaux;
-  args.beta = beta;
-  {
-    const int celem = (epilogue == EPI_F32) ? 4 : 8;  // elements per 16 bytes
-    bool v = (ldc % celem) == 0 && ((uintptr_t)C & 15) == 0;
-    if (R) v = v && (ldr % 8) == 0 && ((uintptr_t)R & 15) == 0;
-    if (aux) v = v && (ldaux % 8) == 0 && ((uintptr_t)aux & 15) == 0;
-    if (bias) v = v && ((uintptr_t)bias & 15) == 0;
-    args.vec = v ? 1 : 0;
-  }
-  const int key = a_mn_major * 2 + b_mn_major;
-  if (pair) {
-    if (BN == 256) {
-      switch (key) {
-        case 0: return dispatch_epi2<256, 0, 0>(epilogue, ta, tb, args, stream);
-        case 1: return dispatch_epi2<256, 0, 1>(epilogue, ta, tb, args, stream);
-        case 3: return dispatch_epi2<256, 1, 1>(epilogue, ta, tb, args, stream);
-      }
-    } else if (BN == 192) {
-      switch (key) {
-        case 0: return dispatch_epi2<192, 0, 0>(epilogue, ta, tb, args, stream);
-      }
+  const char* fenv = getenv("ZB_GEMM_CTAS");  // 1|2 pins 1-CTA / 2-CTA tiles (benchmarking)
+  const int force = fenv ? atoi(fenv) : 0;
+  const char* e1 = getenv("ZB_GEMM_BN");      // benchmarking overrides
+  const char* e2 = getenv("ZB_GEMM_SPLITS");
+  const char* e3 = getenv("ZB_GEMM_DEBUG");
+  const char* e4 = getenv("ZB_GEMM_TUNE");
+  const int fbn = e1 ? atoi(e1) : 0, fsp = e2 ? atoi(e2) : 0, dbg = e3 ? atoi(e3) : 0;
+  const bool tune = !(e4 && atoi(e4) == 0) && !force && !fbn && !fsp;
+  GemmCall g{A, B, bias, R, M, N, K, lda, ldb, ldc, ldr, ldaux, a_mn_major, b_mn_major,
+             epilogue, beta};
+  GemmChoice ch = model_choice(M, N, K, a_mn_major, b_mn_major, epilogue, beta, force);
+  if (fbn == 128 || fbn == 256 || (fbn == 192 && !(ch.pair && b_mn_major))) ch.bn = fbn;
+  if (fsp > 0 && epilogue == EPI_F32 && beta == 1.f) ch.splits = fsp;
+  const char* how = "model";
+  if (tune) {
+    const GemmKey key{M, N, K, a_mn_major, b_mn_major, epilogue, beta == 1.f ? 1 : 0, ldc};
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    auto it = g_tuned.find(key);
+    if (it != g_tuned.end()) {
+      ch = it->second;
+      how = "tuned";
     } else {
-      switch (key) {
-        case 0: return dispatch_epi2<128, 0, 0>(epilogue, ta, tb, args, stream);
-        case 1: return dispatch_epi2<128, 0, 1>(epilogue, ta, tb, args, stream);
-        case 3: return dispatch_epi2<128, 1, 1>(epilogue, ta, tb, args, stream);
+      cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(stream, &st);
+      if (st == cudaStreamCaptureStatusNone) {
+        ch = tune_choice(g, ch, aux, stream);
+        g_tuned[key] = ch;
+        how = "tuned";
       }
     }
-    return set_error(ZB_ERR_INVALID, "gemm: unsupported 2-CTA layout");
   }
-  if (BN == 256) {
-    switch (key) {
-      case 0: return dispatch_epi<256, 0, 0>(epilogue, ta, tb, args, stream);
-      case 1: return dispatch_epi<256, 0, 1>(epilogue, ta, tb, args, stream);
-      case 3: return dispatch_epi<256, 1, 1>(epilogue, ta, tb, args, stream);
-    }
-  } else if (BN == 192) {
-    switch (key) {
-      case 0: return dispatch_epi<192, 0, 0>(epilogue, ta, tb, args, stream);
-      case 1: return dispatch_epi<192, 0, 1>(epilogue, ta, tb, args, stream);
-      case 3: return dispatch_epi<192, 1, 1>(epilogue, ta, tb, args, stream);
-    }
-  } else {
-    switch (key) {
-      case 0: return dispatch_epi<128, 0, 0>(epilogue, ta, tb, args, stream);
-      case 1: return dispatch_epi<128, 0, 1>(epilogue, ta, tb, args, stream);
-      case 3: return dispatch_epi<128, 1, 1>(epilogue, ta, tb, args, stream);
-    }
-  }
-  return set_error(ZB_ERR_INVALID, "gemm: unsupported layout (A MN-major with B K-major)");
+  if (dbg)
+    fprintf(stderr, "zb_gemm M=%d N=%d K=%d a_mn=%d b_mn=%d epi=%d -> %s BN=%d splits=%d (%s)\n",
+            M, N, K, a_mn_major, b_mn_major, epilogue, ch.pair ? "2cta" : "1cta", ch.bn,
+            ch.splits, how);
+  return launch_choice(g, ch, C, aux, stream);
 }

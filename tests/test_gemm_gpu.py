@@ -71,9 +71,20 @@ def test_gemm_wgrad_layout_f32_accumulate(cuda, M, N, Kd):
     _close(c, ref, tol=1e-3)
 
 
-def test_gemm_epilogues(cuda):
+@pytest.fixture(params=["tma", "direct"])
+def epi_path(request, monkeypatch):
+    """Run with the TMA-store epilogue (default) and with the direct-store fallback."""
+    if request.param == "direct":
+        monkeypatch.setenv("ZB_GEMM_NO_TMA_EPI", "1")
+    else:
+        monkeypatch.delenv("ZB_GEMM_NO_TMA_EPI", raising=False)
+    return request.param
+
+
+@pytest.mark.parametrize("M,N,Kd", [(512, 1536, 384), (200, 136, 72), (130, 328, 96),
+                                    (512, 768, 2048), (1000, 2304, 2560)])
+def test_gemm_epilogues(cuda, epi_path, M, N, Kd):
     torch.manual_seed(3)
-    M, N, Kd = 512, 1536, 384
     a = _rand(M, Kd)
     b = _rand(N, Kd, scale=0.05)
     bias = _rand(N)
@@ -91,3 +102,21 @@ def test_gemm_epilogues(cuda):
     K.gemm(a, b, out, epilogue=K.EPI_GELU_BWD, aux=aux)
     _close(out, acc * _gelu_grad(aux.float()))
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("M,N,Kd", [(256, 384, 512), (200, 136, 2048), (768, 768, 8192)])
+def test_gemm_f32_store_and_accumulate(cuda, epi_path, M, N, Kd):
+    """fp32 epilogue: beta = 0 (plain store) and beta = 1 (accumulate / split-K)."""
+    torch.manual_seed(4)
+    dy = _rand(Kd, M)
+    x = _rand(Kd, N)
+    prod = dy.float().t() @ x.float()
+    c = torch.full((M, N), 7.0, device="cuda")
+    K.gemm(dy, x, c, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=0.0)
+    torch.cuda.synchronize()
+    _close(c, prod, tol=1e-3)
+    c2 = torch.randn(M, N, device="cuda")
+    ref = c2 + prod
+    K.gemm(dy, x, c2, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=1.0)
+    torch.cuda.synchronize()
+    _close(c2, ref, tol=1e-3)
