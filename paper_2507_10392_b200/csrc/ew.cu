@@ -509,7 +509,11 @@ extern "C" int zb_bias_grad(const void* dy, void* db, int rows, int n, int ld, c
   if (n % 8 || ld % 8) return set_error(ZB_ERR_INVALID, "bias_grad: n, ld must be multiples of 8");
   if (rows <= 0) return 0;
   const int cblocks = (n / 8 + 31) / 32;
-  int rblocks = (8 * num_sms() + cblocks - 1) / cblocks;  // ~8 blocks per SM
+  // ~2 CTAs per SM and >= 64 rows per CTA: each warp then streams >= 8 rows with
+  // 4 loads in flight, so the per-CTA reduction is amortised (short CTAs were
+  // latency-bound at ~1/6 of HBM bandwidth).
+  int rblocks = (2 * num_sms() + cblocks - 1) / cblocks;
+  if (rblocks > rows / 64) rblocks = rows / 64 > 0 ? rows / 64 : 1;
   int rpb = (rows + rblocks - 1) / rblocks;
   rpb = ((rpb + 7) / 8) * 8;
   rblocks = (rows + rpb - 1) / rpb;

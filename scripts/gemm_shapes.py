@@ -13,14 +13,26 @@ import torch
 from paper_2507_10392_b200 import kernels as K
 
 
-def t_ms(fn, iters=30):
+def t_ms(fn, iters=30, graph=True):
+    """Device time per call: `iters` calls captured in one CUDA graph and replayed
+    (no host launch gaps between short kernels), after eager warm-up."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(iters):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for _ in range(iters):
-        fn()
+    if graph:
+        g.replay()
+    else:
+        for _ in range(iters):
+            fn()
     e.record()
     torch.cuda.synchronize()
     return s.elapsed_time(e) / iters
