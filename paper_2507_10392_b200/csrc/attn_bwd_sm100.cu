@@ -49,7 +49,7 @@ ZB_DEVICE void st_row32(uint8_t* tile, int r, int c0, const float* v) {
 // ------------------------------------------------------------------ dQ
 template <int D>
 struct DqSmem {
-  static constexpr int NST = 2;                  // K/V stages (224 KB at D = 128)
+  static constexpr int NST = (D == 64) ? 3 : 2;  // K/V stages (192 KB at D = 64, 224 KB at 128)
   static constexpr int DSB = (D == 64) ? 2 : 1;
   static constexpr int TILE = T * D * 2;
   static constexpr int OFF_Q = 0, OFF_DO = TILE;
@@ -72,14 +72,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t* qo_full = bar;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_empty = bar + 6;
-  uint64_t* ds_full = bar + 7;   // [2]
-  uint64_t* ds_empty = bar + 9;  // [2]
-  uint64_t* dq_done = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* kv_full = bar + 1;          // [NST]
+  uint64_t* kv_empty = bar + 1 + NST;   // [NST]
+  uint64_t* s_full = bar + 1 + 2 * NST;
+  uint64_t* s_empty = s_full + 1;
+  uint64_t* ds_full = s_full + 2;       // [2]
+  uint64_t* ds_empty = s_full + 4;      // [2]
+  uint64_t* dq_done = s_full + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = S / T - 1 - blockIdx.x;
   const int h = blockIdx.y, b = blockIdx.z, HD = H * D, row0 = b * S, nblk = qt + 1;
@@ -88,9 +88,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
     mbar_init(qo_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&ds_full[i], 4);
       mbar_init(&ds_empty[i], 1);
     }
@@ -187,7 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float ds[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          float p = exp2_fast(fmaf(__uint_as_float(sv[i]), sl2, -L2));
+          const float xe = fmaf(__uint_as_float(sv[i]), sl2, -L2);
+          float p = (i & 3) == 3 ? exp2_poly(xe) : exp2_fast(xe);  // 1/4 on the FMA pipe
           if (j == qt && c * 32 + i > r) p = 0.f;
           ds[i] = p * (__uint_as_float(dv[i]) - Dl);
         }
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ dK, dV
 template <int D>
 struct DkvSmem {
-  static constexpr int NST = (D == 64) ? 2 : 1;
+  static constexpr int NST = (D == 64) ? 3 : 1;  // Q/dO stages (196 KB at D = 64)
   static constexpr int TILE = T * D * 2;
   static constexpr int OFF_K = 0, OFF_V = TILE;
   static constexpr int OFF_Q = 2 * TILE;              // [NST] Q_i
@@ -252,14 +255,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t* kv_full = bar;
-  uint64_t* qo_full = bar + 1;   // [2]
-  uint64_t* qo_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_empty = bar + 6;
-  uint64_t* p_full = bar + 7;
-  uint64_t* p_empty = bar + 8;
-  uint64_t* done = bar + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+  uint64_t* qo_full = bar + 1;          // [NST]
+  uint64_t* qo_empty = bar + 1 + NST;   // [NST]
+  uint64_t* s_full = bar + 1 + 2 * NST;
+  uint64_t* s_empty = s_full + 1;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* p_empty = s_full + 3;
+  uint64_t* done = s_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
   float* vec = reinterpret_cast<float*>(sm + L::OFF_VEC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x;  // early key tiles see the most query tiles: launch first
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&qo_full[i], 1);
       mbar_init(&qo_empty[i], 1);
     }
@@ -379,7 +382,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           const int qq = c * 32 + t;
-          float x = exp2_fast(fmaf(__uint_as_float(sv[t]), sl2, -vl[qq]));
+          const float xe = fmaf(__uint_as_float(sv[t]), sl2, -vl[qq]);
+          float x = (t & 3) == 3 ? exp2_poly(xe) : exp2_fast(xe);  // 1/4 on the FMA pipe
           if (qt == kt && qq < r) x = 0.f;
           p[t] = x;
           ds[t] = x * (__uint_as_float(dv[t]) - vd[qq]);

@@ -17,17 +17,22 @@
 #include "common.cuh"
 #include "zb_internal.h"
 
+#include <cstdlib>
+#include <type_traits>
+
 namespace zb {
 namespace fa {
 
 constexpr int BQ = 128;   // queries per CTA (= TMEM lanes = softmax threads)
 constexpr int BKV = 128;  // keys per block
-constexpr int NST = 2;    // K/V pipeline stages
 constexpr int kThreads = 256;
 constexpr float LOG2E = 1.4426950408889634f;
 
 template <int D>
 struct FwdSmem {
+  // K/V ring depth: at D = 64 a block's MMAs take ~512 cycles, so 4 stages are
+  // needed to keep the L2 -> smem latency off the critical path (208 KB).
+  static constexpr int NST = (D == 64) ? 4 : 2;
   static constexpr int Q_BYTES = BQ * D * 2;
   static constexpr int K_BYTES = BKV * D * 2;
   static constexpr int V_BYTES = BKV * D * 2;
@@ -37,7 +42,7 @@ struct FwdSmem {
   static constexpr int OFF_V = OFF_K + NST * K_BYTES;
   static constexpr int OFF_P = OFF_V + NST * V_BYTES;
   static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-  static constexpr int TOTAL = OFF_BAR + 256 + 1024;  // barriers + alignment slack (18 x 8 B used)
+  static constexpr int TOTAL = OFF_BAR + 256 + 1024;  // barriers + alignment slack (<= 26 x 8 B)
 };
 
 // K-major SW128 descriptor for a [rows][64*nblk] tile stored as nblk 64-column
@@ -55,27 +60,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   // heavy-first order with a stride of gridDim.x; TMEM, barriers and the K/V /
   // S / P rings persist across items (ring positions are global block counters).
   using L = FwdSmem<D>;
+  constexpr int NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;        // [NST]
-  uint64_t* kv_empty = bar + 3;       // [NST]
-  uint64_t* s_full = bar + 5;         // [2]
-  uint64_t* s_empty = bar + 7;        // [2]
-  uint64_t* p_full = bar + 9;         // [2]
-  uint64_t* p_empty = bar + 11;       // [2]
+  uint64_t* kv_full = bar + 1;              // [NST]
+  uint64_t* kv_empty = bar + 1 + NST;       // [NST]
+  uint64_t* s_full = bar + 1 + 2 * NST;     // [2]
+  uint64_t* s_empty = s_full + 2;           // [2]
+  uint64_t* p_full = s_full + 4;            // [2]
+  uint64_t* p_empty = s_full + 6;           // [2]
   // O-accumulation completions alternate between two barriers (PV block k commits
   // o_bar[k & 1]).  With one barrier, PV_k and PV_{k+1} could both complete before
   // the softmax warps poll for PV_k (the MMA may issue PV_{k+1} as soon as P_{k+1}
   // is handed over), and a parity wait cannot tell phase k from phase k+2.
   // Two barriers cannot run two phases ahead: P_{k+2} is handed over only after
   // PV_k was consumed.
-  uint64_t* o_bar = bar + 13;         // [2]
-  uint64_t* q_empty = bar + 15;       // all S MMAs of an item done -> Q reusable
-  uint64_t* o_empty = bar + 16;       // epilogue read O -> next item may overwrite
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+  uint64_t* o_bar = s_full + 8;             // [2]
+  uint64_t* q_empty = s_full + 10;          // all S MMAs of an item done -> Q reusable
+  uint64_t* o_empty = s_full + 11;          // epilogue read O -> next item may overwrite
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqt = S / BQ;
@@ -232,15 +238,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sb = gi & 1;
         mbar_wait(&s_full[sb], (gi >> 1) & 1);
         tc_fence_after();
+        // the whole S row in flight at once: one TMEM round trip instead of four
         float sv[BKV];
+        uint32_t v[BKV / 32][32];
 #pragma unroll
-        for (int c = 0; c < BKV / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_s[sb] + lane_off + c * 32, v);
-          tmem_ld_wait();
+        for (int c = 0; c < BKV / 32; ++c) tmem_ld_32x32b_x32(t_s[sb] + lane_off + c * 32, v[c]);
+        tmem_ld_wait_regs(v[0]);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]);
-        }
+        for (int c = 1; c < BKV / 32; ++c) reg_tie(v[c]);
+#pragma unroll
+        for (int c = 0; c < BKV / 32; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[c][i]);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
@@ -249,20 +258,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < BKV; ++c)
             if (c > r) sv[c] = -INFINITY;
         }
-        float mx = sv[0];
+        // 8 independent max / sum chains (a single 128-long dependent chain costs
+        // ~4 cycles per element of latency on one warp per scheduler)
+        float mx8[8];
 #pragma unroll
-        for (int c = 1; c < BKV; ++c) mx = fmaxf(mx, sv[c]);
+        for (int i = 0; i < 8; ++i) mx8[i] = sv[i];
+#pragma unroll
+        for (int c = 8; c < BKV; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], sv[c]);
+        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         mx *= sl2;
         const bool move = mx > m + RESCALE_T;
         const float m_new = move ? mx : m;
         const float corr = move ? exp2_fast(m - m_new) : 1.f;  // 0 on the first block
         m = m_new;
-        float rs = 0.f;
+        float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < BKV; ++c) {
-          sv[c] = exp2_fast(fmaf(sv[c], sl2, -m));
-          rs += sv[c];
+          const float xe = fmaf(sv[c], sl2, -m);
+          sv[c] = (c & 3) == 3 ? exp2_poly(xe) : exp2_fast(xe);  // 1/4 on the FMA pipe
+          rs8[c & 7] += sv[c];
         }
+        const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
         l = l * corr + rs;
         mbar_wait(&p_empty[sb], ((gi >> 1) & 1) ^ 1);
         uint8_t* prow = sm + L::OFF_P + sb * L::P_BYTES + r * 128;
@@ -332,6 +349,342 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------- D = 64: two CTAs per SM
+// The single-CTA kernel above keeps each SM's tensor core idle while its one softmax
+// warpgroup works (one warp per scheduler, nothing to hide its latencies).  Here P
+// is written to TMEM (tcgen05.st) and the PV MMA reads it from there (A operand in
+// TMEM), so a CTA needs only Q + a 2-stage K/V ring in smem (80 KB), 256 TMEM
+// columns (S | P | O) and <= 128 registers per thread: two CTAs share every SM and
+// one CTA's MMAs run while the other's softmax warps work.  The softmax makes two
+// passes over the S row in TMEM (max, then exp / sum / pack) instead of holding
+// 128 values in registers.
+namespace fa_ts {
+constexpr int BQ = 128, BKV = 128, D = 64, NST = 2, kThreads = 256;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr int Q_BYTES = BQ * D * 2, K_BYTES = BKV * D * 2, V_BYTES = BKV * D * 2;
+constexpr int OFF_Q = 0, OFF_K = 2 * Q_BYTES, OFF_V = OFF_K + NST * K_BYTES;  // Q double-buffered
+constexpr int OFF_BAR = OFF_V + NST * V_BYTES;
+constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;
+constexpr uint32_t COL_S = 0, COL_P = 128, COL_O = 192, TMEM_COLS = 256;
+
+__global__ void __launch_bounds__(kThreads, 2)
+    fwd_ts_kernel(const __grid_constant__ CUtensorMap tm_rows128,
+                  const __grid_constant__ CUtensorMap tm_rows64, __nv_bfloat16* __restrict__ out,
+                  float* __restrict__ lse, int S, int H, int n_seq, float scale) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
+  uint64_t* q_full = bar + 0;     // [2] (the next item's Q loads during this item)
+  uint64_t* q_empty = bar + 2;    // [2]
+  uint64_t* kv_full = bar + 4;    // [NST]
+  uint64_t* kv_empty = bar + 6;   // [NST]
+  uint64_t* s_full = bar + 8;
+  uint64_t* s_empty = bar + 9;    // softmax finished reading S
+  uint64_t* p_full = bar + 10;    // P in TMEM (and any O rescale) done
+  uint64_t* o_bar = bar + 11;     // [2] PV block k commits o_bar[k & 1] (see fwd_kernel)
+  uint64_t* o_empty = bar + 13;   // epilogue read O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqt = S / BQ;
+  const int HD = H * D;
+  const int per_q = H * n_seq;
+  const int items = nqt * per_q;
+  // Work items sorted heavy-first (late query tiles have the most key blocks), dealt
+  // to the persistent CTAs in boustrophedon order (round k: CTA c takes rank
+  // k*P + c for even k, k*P + P-1-c for odd k) so per-CTA totals even out.
+  const int P = gridDim.x;
+  auto item_of = [&](int k) { return k * P + ((k & 1) ? (P - 1 - (int)blockIdx.x) : (int)blockIdx.x); };
+  auto decode = [&](int t, int& qt, int& h, int& b) {
+    qt = nqt - 1 - t / per_q;  // heavy (late) query tiles first
+    const int rem = t % per_q;
+    h = rem % H;
+    b = rem / H;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_rows128);
+    tma_prefetch_desc(&tm_rows64);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, 4);
+    mbar_init(p_full, 4);
+    mbar_init(&o_bar[0], 1);
+    mbar_init(&o_bar[1], 1);
+    mbar_init(o_empty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem + COL_S, t_p = tmem + COL_P, t_o = tmem + COL_O;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int g = 0, lt = 0;
+      for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
+        int qt, h, b;
+        decode(t, qt, h, b);
+        const int row0 = b * S;
+        const int qb = lt & 1;
+        mbar_wait(&q_empty[qb], ((lt >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], Q_BYTES);
+        tma_load_2d(sm + OFF_Q + qb * Q_BYTES, &tm_rows128, &q_full[qb], h * D, row0 + qt * BQ);
+        for (int j = 0; j <= qt; ++j, ++g) {
+          const int st = g % NST;
+          mbar_wait(&kv_empty[st], ((g / NST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[st], K_BYTES + V_BYTES);
+          uint8_t* kd = sm + OFF_K + st * K_BYTES;
+          uint8_t* vd = sm + OFF_V + st * V_BYTES;
+          const int kr = row0 + j * BKV;
+          tma_load_2d(kd, &tm_rows128, &kv_full[st], HD + h * D, kr);
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb)
+            tma_load_2d(vd + kb * 8192, &tm_rows64, &kv_full[st], 2 * HD + h * D, kr + kb * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(BQ, BKV, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(BQ, D, 0, 1);
+      int gbase = 0, lt = 0;
+      for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
+        int qt, h, b;
+        decode(t, qt, h, b);
+        const int nblk = qt + 1;
+        const int qb = lt & 1;
+        const uint32_t q_base = smem_u32(sm + OFF_Q + qb * Q_BYTES);
+        mbar_wait(&q_full[qb], (lt >> 1) & 1);
+        for (int j = 0; j < nblk; ++j) {
+          const int gi = gbase + j, st = gi % NST;
+          mbar_wait(&kv_full[st], (gi / NST) & 1);
+          mbar_wait(s_empty, (gi & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t k_base = smem_u32(sm + OFF_K + st * K_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_bf16_ss(t_s, desc_kmajor(q_base, kk, BQ), desc_kmajor(k_base, kk, BKV), idesc_s,
+                        kk > 0 ? 1u : 0u);
+          mma_commit(s_full);
+          if (j == nblk - 1) mma_commit(&q_empty[qb]);
+          mbar_wait(p_full, gi & 1);
+          if (j == 0) mbar_wait(o_empty, (lt & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t v_base = smem_u32(sm + OFF_V + st * V_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk) {
+            const uint64_t bdesc =
+                umma_desc_sw128(v_base + (kk >> 2) * 8192 + (kk & 3) * 2048, 8192, 1024);
+            mma_bf16_ts(t_o, t_p + kk * 8, bdesc, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&kv_empty[st]);
+          mma_commit(&o_bar[gi & 1]);
+        }
+        gbase += nblk;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int wq = warp - 4;
+    const int r = wq * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const float sl2 = scale * LOG2E;
+    constexpr float RESCALE_T = 8.f;  // lazy O rescale (see fwd_kernel)
+    int gbase = 0, o_seen = 0;
+#ifdef ZB_EXP_TRACE
+    long long acc_t[5] = {0, 0, 0, 0, 0}, t_start = clock64();
+    int acc_n = 0;
+#endif
+    auto consume_o = [&](int upto) {
+      while (o_seen < upto) {
+        mbar_wait(&o_bar[o_seen & 1], (o_seen >> 1) & 1);
+        ++o_seen;
+      }
+    };
+    for (int k = 0, t = item_of(0); t < items; t = item_of(++k)) {
+      int qt, h, b;
+      decode(t, qt, h, b);
+      const int nblk = qt + 1;
+      const int q = qt * BQ + r;
+      const int row0 = b * S;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nblk; ++j) {
+        const int gi = gbase + j;
+        const bool diag = j == qt;
+#ifdef ZB_EXP_TRACE
+        long long tr0 = clock64();
+#endif
+        mbar_wait(s_full, gi & 1);
+        tc_fence_after();
+#ifdef ZB_EXP_TRACE
+        long long tr1 = clock64();
+#endif
+        // pass 1: row max (masking only on the diagonal block; 3-input max)
+        auto row_max = [&](auto diag_c) {
+          constexpr bool DG = decltype(diag_c)::value;
+          float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int c = 0; c < BKV / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_s + lane_off + c * 32, v);
+            tmem_ld_wait_regs(v);
+            float x[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              x[i] = __uint_as_float(v[i]);
+              if (DG && c * 32 + i > r) x[i] = -INFINITY;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              mx4[0] = fmax3(mx4[0], x[i], x[i + 1]);
+              mx4[1] = fmax3(mx4[1], x[i + 2], x[i + 3]);
+              mx4[2] = fmax3(mx4[2], x[i + 4], x[i + 5]);
+              mx4[3] = fmax3(mx4[3], x[i + 6], x[i + 7]);
+            }
+          }
+          return fmaxf(fmax3(mx4[0], mx4[1], mx4[2]), mx4[3]) * sl2;
+        };
+        const float mx = diag ? row_max(std::true_type{}) : row_max(std::false_type{});
+        const bool move = mx > m + RESCALE_T;
+        const float m_new = move ? mx : m;
+        const float corr = move ? exp2_fast(m - m_new) : 1.f;
+        m = m_new;
+#ifdef ZB_EXP_TRACE
+        long long tr2 = clock64();
+#endif
+        // P (single TMEM buffer) and O are free once PV of the previous block is done
+        consume_o(gi);
+        tc_fence_after();
+#ifdef ZB_EXP_TRACE
+        long long tr3 = clock64();
+#endif
+        if (j > 0 && __any_sync(0xffffffffu, move)) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+            tmem_ld_wait_regs(v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st_32x32b_x32(t_o + lane_off + c * 32, v);
+          }
+        }
+        // pass 2: exponentials, row sum, bf16 P row into TMEM
+        auto exp_pack = [&](auto diag_c) {
+          constexpr bool DG = decltype(diag_c)::value;
+          float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int c = 0; c < BKV / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_s + lane_off + c * 32, v);
+            tmem_ld_wait_regs(v);
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              // the SM's ex2 (MUFU) rate is the softmax floor: ~1/4 of the
+              // exponentials go to the FMA pipe (exp2_poly)
+              float p0 = exp2_fast(fmaf(__uint_as_float(v[i]), sl2, -m));
+              const float x1 = fmaf(__uint_as_float(v[i + 1]), sl2, -m);
+              float p1 = ((i >> 1) & 1) ? exp2_poly(x1) : exp2_fast(x1);
+              if (DG && c * 32 + i > r) p0 = 0.f;
+              if (DG && c * 32 + i + 1 > r) p1 = 0.f;
+              rs4[(i >> 1) & 3] += p0 + p1;
+              pk[i >> 1] = pack_bf16(p0, p1);
+            }
+            tmem_st_32x32b_x16(t_p + lane_off + c * 16, pk);
+          }
+          return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+        };
+        const float rs = diag ? exp_pack(std::true_type{}) : exp_pack(std::false_type{});
+        l = l * corr + rs;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(s_empty);
+          mbar_arrive(p_full);
+        }
+#ifdef ZB_EXP_TRACE
+        long long tr4 = clock64();
+        acc_t[0] += tr1 - tr0; acc_t[1] += tr2 - tr1; acc_t[2] += tr3 - tr2; acc_t[3] += tr4 - tr3;
+        ++acc_n;
+#endif
+      }
+      // epilogue: O / l -> bf16 row, lse
+      consume_o(gbase + nblk);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+        tmem_ld_wait_regs(v);
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 pk;
+          pk.x = pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
+          pk.y = pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
+          pk.z = pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
+          pk.w = pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = pk;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_empty);
+      lse[((size_t)b * H + h) * S + q] = (m + __log2f(l)) / LOG2E;
+      gbase += nblk;
+    }
+#ifdef ZB_EXP_TRACE  // per-CTA phase cycle totals (debug builds: build(defines=("ZB_EXP_TRACE",)))
+    if (r == 0 && (blockIdx.x == 0 || blockIdx.x == 100 || blockIdx.x == 250 || blockIdx.x == 295))
+      printf("cta %d: blocks %d total %lld wait_s %lld pass1 %lld wait_o %lld pass2 %lld\n",
+             blockIdx.x, acc_n, clock64() - t_start, acc_t[0], acc_t[1], acc_t[2], acc_t[3]);
+#endif
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+static int run(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int ld, float scale,
+               cudaStream_t s) {
+  CUtensorMap m128, m64;
+  const uint64_t T = (uint64_t)n_seq * S;
+  if (int rc = make_tmap_bf16_2d(&m128, qkv, (uint64_t)3 * H * D, T, ld, 64, 128)) return rc;
+  if (int rc = make_tmap_bf16_2d(&m64, qkv, (uint64_t)3 * H * D, T, ld, 64, 64)) return rc;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fwd_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn fwd_ts: cudaFuncSetAttribute");
+    configured = true;
+  }
+  const int items = (S / BQ) * H * n_seq;
+  const int slots = 2 * num_sms();
+  const int grid = items < slots ? items : slots;
+  fwd_ts_kernel<<<grid, kThreads, SMEM_BYTES, s>>>(m128, m64, (__nv_bfloat16*)out, (float*)lse, S,
+                                                   H, n_seq, scale);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "attn fwd_ts launch");
+}
+}  // namespace fa_ts
+
 template <int D>
 static int run_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int ld,
                    float scale, cudaStream_t s) {
@@ -364,7 +717,11 @@ extern "C" int zb_attn_fwd_tc(const void* qkv, void* out, void* lse, int n_seq, 
   if (S % 128) return set_error(ZB_ERR_INVALID, "attn_fwd_tc: seq_len must be a multiple of 128");
   if (ld % 8 || ((uintptr_t)qkv & 15)) return set_error(ZB_ERR_INVALID, "attn_fwd_tc: bad ld/alignment");
   if (n_seq <= 0) return 0;
-  if (D == 64) return fa::run_fwd<64>(qkv, out, lse, n_seq, S, H, ld, scale, s);
+  if (D == 64) {
+    static const bool one = getenv("ZB_ATTN_FWD_1CTA") != nullptr;  // A/B: single-CTA kernel
+    if (!one) return fa::fa_ts::run(qkv, out, lse, n_seq, S, H, ld, scale, s);
+    return fa::run_fwd<64>(qkv, out, lse, n_seq, S, H, ld, scale, s);
+  }
   if (D == 128) return fa::run_fwd<128>(qkv, out, lse, n_seq, S, H, ld, scale, s);
   return set_error(ZB_ERR_UNSUPPORTED, "attn_fwd_tc: head_dim %d unsupported (64, 128)", D);
 }
