@@ -72,7 +72,8 @@ int zb_attn_bwd(const void* qkv, const void* out, const void* dout, const void* 
  * LayerNorm over rows of length d (d % 8 == 0).  mean/rstd: fp32 [rows]. */
 int zb_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void* mean, void* rstd,
                      void* reserved, int rows, int d, float eps, zb_stream_t stream);
-/* dx = dres + LN'(dy) (dres may be NULL; dx may alias dres); dw, db (fp32) += grads. */
+/* dx = dres + LN'(dy) (dres may be NULL; dx may alias dres but not dy or x); dw, db (fp32) += grads.
+ * Two launches: dx per row, then the dw / db column reduction. */
 int zb_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mean,
                      const void* rstd, void* dx, void* dw, void* db, const void* dres, int rows,
                      int d, zb_stream_t stream);
