@@ -15,8 +15,11 @@ to its DP group, and turns every modelled task into real work:
   ReduceScatter  -> uneven in-place ReduceScatter-v (sum) of the fp32 grads
   OptimStep      -> fused AdamW on this rank's shard of the ministage's layers
                     (interleaved optimizer: right after that ministage's RS)
-  OffloadAct / LoadAct / FreeParams -> no-ops: activations and gathered
-                    parameters stay resident in 180 GB of HBM
+  OffloadAct / LoadAct -> with offload_acts (INTERLEAVED strategy): interior
+                    layer-boundary checkpoints copied to pinned host memory after
+                    Fwd and back before Recompute, on a host-copy stream, with a
+                    2-microbatch device ring; otherwise no-ops (HBM-resident)
+  FreeParams       -> no-op: gathered parameters stay resident in the arena
 
 Every rank of every group issues its communication in one global order, so
 the NCCL calls can never form the cyclic wait the paper had to work around
@@ -134,7 +137,7 @@ class StageExecutor:
     def __init__(self, plan: TrainingPlan, ctx: CostContext, cfg: ModelConfig, dev_id: str,
                  rank_of: Dict[str, int], world_comm, group_comm, ops, device,
                  seed: int = 1234, adam: AdamConfig = AdamConfig(), init_device="cpu",
-                 schedule: str = "gpipe", streams: bool = False):
+                 schedule: str = "gpipe", streams: bool = False, offload_acts: bool = False):
         if plan.routing is None:
             raise ValueError("plan has no routing; attach it (configure.attach_routing) first")
         if ctx.model.num_layers != cfg.n_layer:
@@ -168,7 +171,8 @@ class StageExecutor:
         self.multistream = bool(streams) and device.type == "cuda"
         if self.multistream:
             self.lane_streams = {"collective": torch.cuda.Stream(device=device),
-                                 "p2p": torch.cuda.Stream(device=device)}
+                                 "p2p": torch.cuda.Stream(device=device),
+                                 "host": torch.cuda.Stream(device=device)}
         self.record_timeline = False  # measured Gantt (see measured_timeline)
         self._marks = []
         self.capture_grads = False   # tests: keep each reduced grad shard before Adam
@@ -207,12 +211,31 @@ class StageExecutor:
         bf = dict(device=device, dtype=torch.bfloat16)
         self.act: Dict[Tuple[int, int], torch.Tensor] = {}
         self.gbuf: Dict[Tuple[int, int], torch.Tensor] = {}
+        # Host offload of activation checkpoints (the reference's OffloadAct / LoadAct
+        # tasks, simulate.py:369-376 / 451-467; memory model costs.py:596-600): with
+        # the INTERLEAVED strategy the interior layer-boundary checkpoints of a
+        # ministage (inputs of its 2nd..last layer) live on the device only in a
+        # 2-microbatch ring — microbatch m uses slot m % 2 — and are copied to pinned
+        # host memory after Fwd and back before Recompute on their own stream.
+        # Stage-boundary checkpoints (P2P endpoints) stay resident.
+        self.offload = bool(offload_acts) and plan.strategy.offloads
+        self.host_act: Dict[Tuple[int, int], torch.Tensor] = {}
+        self.interior: Dict[int, List[int]] = {}
+        pin = device.type == "cuda"
         for s in self.my_stages:
             lo, hi = self.ranges[s]
+            self.interior[s] = list(range(lo + 1, hi)) if self.offload else []
             for m in range(self.M):
                 for layer in range(lo, hi + 1):
-                    if (layer, m) not in self.act:
+                    if (layer, m) in self.act:
+                        continue
+                    if layer in self.interior[s] and m >= 2:
+                        self.act[(layer, m)] = self.act[(layer, m % 2)]   # ring slot
+                    else:
                         self.act[(layer, m)] = torch.empty(n, d, **bf)
+                    if layer in self.interior[s]:
+                        self.host_act[(layer, m)] = torch.empty(n, d, dtype=torch.bfloat16,
+                                                                pin_memory=pin)
                 for key in ((lo, m), (hi, m)):
                     if key not in self.gbuf:
                         self.gbuf[key] = torch.empty(n, d, **bf)
@@ -349,8 +372,9 @@ class StageExecutor:
             waits = []
             for dep in ev.deps:
                 waits.extend(done.get(dep, ()))      # deps of other groups are remote
-            if ev.kind in ("OffloadAct", "LoadAct", "FreeParams", "P2PRecv") or \
-                    ev.lane not in streams:
+            noop = ("FreeParams", "P2PRecv") if self.offload else \
+                ("OffloadAct", "LoadAct", "FreeParams", "P2PRecv")
+            if ev.kind in noop or ev.lane not in streams:
                 done[ev.key] = waits                 # no-op: completion = its deps'
                 continue
             lane = "p2p" if ev.kind == "P2PSend" else ev.lane
@@ -512,6 +536,24 @@ class StageExecutor:
     def _on_recv(self, ev: Event) -> None:
         return None  # data was received at the matching P2PSend event
 
+    def _on_offload(self, ev: Event) -> None:
+        """OffloadAct: interior checkpoints of (stage, microbatch) -> pinned host."""
+        if not self.offload or self.n_tok == 0:
+            return
+        s, m = ev.key[1], ev.key[2]
+        n = self.n_tok
+        for layer in self.interior.get(s, ()):
+            self.host_act[(layer, m)][:n].copy_(self.act[(layer, m)][:n], non_blocking=True)
+
+    def _on_load(self, ev: Event) -> None:
+        """LoadAct: pinned host -> the microbatch's device ring slot, before Recompute."""
+        if not self.offload or self.n_tok == 0:
+            return
+        s, m = ev.key[1], ev.key[2]
+        n = self.n_tok
+        for layer in self.interior.get(s, ()):
+            self.act[(layer, m)][:n].copy_(self.host_act[(layer, m)][:n], non_blocking=True)
+
     def _noop(self, ev: Event) -> None:
         return None
 
@@ -541,7 +583,7 @@ _DISPATCH = {
     "Bwd": StageExecutor._on_bwd,
     "P2PSend": StageExecutor._on_send,
     "P2PRecv": StageExecutor._on_recv,
-    "OffloadAct": StageExecutor._noop,
-    "LoadAct": StageExecutor._noop,
+    "OffloadAct": StageExecutor._on_offload,
+    "LoadAct": StageExecutor._on_load,
     "FreeParams": StageExecutor._noop,
 }

@@ -27,7 +27,7 @@ class ZorseTrainer:
                  world_rank: int = 0, world_size: int = 1, seed: int = 1234,
                  adam: AdamConfig = AdamConfig(), init_device: str = "cpu",
                  schedule: str = "gpipe", streams: bool = True, collectives: str = "peer",
-                 _ops=None, _comms=None, _device=None):
+                 offload_acts: bool = False, _ops=None, _comms=None, _device=None):
         if collectives not in ("peer", "nccl"):
             raise ValueError(f"collectives must be 'peer' or 'nccl', not {collectives!r}")
         devices = list(ctx.graph.vertices)
@@ -60,7 +60,7 @@ class ZorseTrainer:
         self.device = device
         self.exec = StageExecutor(plan, ctx, cfg, self.dev_id, self.rank_of, world, group, ops,
                                   device, seed=seed, adam=adam, init_device=init_device,
-                                  schedule=schedule, streams=streams)
+                                  schedule=schedule, streams=streams, offload_acts=offload_acts)
         self.collectives = collectives if world_size > 1 else None
         if _ops is None and world_size > 1 and collectives == "peer":
             # AG-v / fused RS-v+AdamW over NVLink peer memory (csrc/peer.cu)

@@ -57,7 +57,8 @@ def main():
     t0 = time.time()
     coll = os.environ.get("ZB_COLLECTIVES", "peer")
     tr = ZorseTrainer(plan, ctx, cfg, world_rank=rank, world_size=world, schedule=r["schedule"],
-                      init_device="cuda", collectives=coll)
+                      init_device="cuda", collectives=coll,
+                      offload_acts=os.environ.get("ZB_OFFLOAD", "0") == "1")
     init_s = time.time() - t0
     batch = synthetic_batch(cfg.vocab, cfg.seq_len, r["gb"], 1, pin=True)
     losses = [tr.step(batch)]  # warm-up
@@ -78,7 +79,7 @@ def main():
     dist.all_reduce(gmem, op=dist.ReduceOp.MAX)
     if rank == 0:
         tok = r["gb"] * cfg.seq_len
-        print(json.dumps({"collectives": coll,
+        print(json.dumps({"collectives": coll, "offload_acts": tr.exec.offload,
             "run": name, "model": cfg.name, "n_gpus": world, "schedule": r["schedule"],
             "strategy": r["strategy"], "groups": [[g.device_ids, g.layers_assigned, g.shares]
                                                   for g in plan.groups],

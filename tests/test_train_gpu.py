@@ -30,16 +30,20 @@ def _rel(a, b):
     return ((a - b).norm() / (b.norm() + 1e-12)).item()
 
 
-@pytest.mark.parametrize("cfg,gb,n_mb,counts,strategy", [
-    (E.TINY_GPT, 8, 2, [1], "zorse"),                  # BASELINE config 1 model
-    (E.TINY_GPT, 8, 2, [4], "pp-zero3"),
-    (E.ModelConfig("mid", "gpt", 2, 768, 12, 4096, 1024), 2, 1, [2], "zorse"),  # GPT-2 widths
-    (E.ModelConfig("llama-tiny", "llama", 2, 512, 4, 4096, 256, d_ff=1376), 4, 2, [2], "zorse"),
-    (E.ModelConfig("llama-hd128", "llama", 2, 1024, 8, 4096, 512, d_ff=2752), 2, 1, [1], "pp-zero3"),
+@pytest.mark.parametrize("cfg,gb,n_mb,counts,strategy,offload", [
+    (E.TINY_GPT, 8, 2, [1], "zorse", False),                  # BASELINE config 1 model
+    (E.TINY_GPT, 8, 2, [4], "pp-zero3", False),
+    (E.ModelConfig("mid", "gpt", 2, 768, 12, 4096, 1024), 2, 1, [2], "zorse", False),  # GPT-2 widths
+    (E.ModelConfig("llama-tiny", "llama", 2, 512, 4, 4096, 256, d_ff=1376), 4, 2, [2], "zorse", False),
+    (E.ModelConfig("llama-hd128", "llama", 2, 1024, 8, 4096, 512, d_ff=2752), 2, 1, [1], "pp-zero3",
+     False),
+    # activation offload to pinned host memory (OffloadAct / LoadAct on the host stream)
+    (E.TINY_GPT, 8, 4, [1], "zorse", True),
 ])
-def test_training_steps_match_oracle(cuda, cfg, gb, n_mb, counts, strategy):
+def test_training_steps_match_oracle(cuda, cfg, gb, n_mb, counts, strategy, offload):
     plan, ctx = _setup(cfg, gb, n_mb, counts, strategy)
-    tr = ZorseTrainer(plan, ctx, cfg)
+    tr = ZorseTrainer(plan, ctx, cfg, offload_acts=offload)
+    assert tr.exec.offload == offload
     tr.exec.capture_grads = True
     batches = [synthetic_batch(cfg.vocab, cfg.seq_len, gb, s) for s in (1, 2)]
     params = gpt_cpu.init_params(cfg, 1234)
