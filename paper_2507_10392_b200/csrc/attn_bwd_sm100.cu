@@ -16,6 +16,8 @@
 #include "common.cuh"
 #include "zb_internal.h"
 
+#include <type_traits>
+
 #include <cstdlib>
 
 namespace zb {
@@ -180,21 +182,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(s_full, j & 1);
       tc_fence_after();
       uint8_t* ds_tile = sm + L::OFF_DS + db * T * T * 2;
-#pragma unroll 1
-      for (int c = 0; c < T / 32; ++c) {
+      // dS = P (dP - delta); the causal mask only exists on the diagonal block
+      auto chunk = [&](int c, auto diag_c) {
+        constexpr bool DG = decltype(diag_c)::value;
         uint32_t sv[32], dv[32];
         tmem_ld_32x32b_x32(t_s + lo + c * 32, sv);
         tmem_ld_32x32b_x32(t_dp + lo + c * 32, dv);
-        tmem_ld_wait();
+        tmem_ld_wait_regs(sv);
+        reg_tie(dv);
         float ds[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float xe = fmaf(__uint_as_float(sv[i]), sl2, -L2);
-          float p = (i & 3) == 3 ? exp2_poly(xe) : exp2_fast(xe);  // 1/4 on the FMA pipe
-          if (j == qt && c * 32 + i > r) p = 0.f;
+          float p = exp2_fast(fmaf(__uint_as_float(sv[i]), sl2, -L2));
+          if (DG && c * 32 + i > r) p = 0.f;
           ds[i] = p * (__uint_as_float(dv[i]) - Dl);
         }
         st_row32(ds_tile, r, c * 32, ds);
+      };
+      if (j == qt) {
+#pragma unroll 1
+        for (int c = 0; c < T / 32; ++c) chunk(c, std::true_type{});
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < T / 32; ++c) chunk(c, std::false_type{});
       }
       tc_fence_before();
       __syncwarp();
@@ -372,24 +382,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       uint8_t* pt = sm + L::OFF_PT;
       uint8_t* dst = sm + L::OFF_DST;
-#pragma unroll 1
-      for (int c = 0; c < T / 32; ++c) {
+      // P^T and dS^T rows of this key; the mask only exists on the diagonal tile;
+      // the per-query lse / delta come from smem as broadcast 16-byte loads
+      auto chunk = [&](int c, auto diag_c) {
+        constexpr bool DG = decltype(diag_c)::value;
         uint32_t sv[32], dv[32];
         tmem_ld_32x32b_x32(t_st + lo + c * 32, sv);
         tmem_ld_32x32b_x32(t_dpt + lo + c * 32, dv);
-        tmem_ld_wait();
+        tmem_ld_wait_regs(sv);
+        reg_tie(dv);
         float p[32], ds[32];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int qq = c * 32 + t;
-          const float xe = fmaf(__uint_as_float(sv[t]), sl2, -vl[qq]);
-          float x = (t & 3) == 3 ? exp2_poly(xe) : exp2_fast(xe);  // 1/4 on the FMA pipe
-          if (qt == kt && qq < r) x = 0.f;
-          p[t] = x;
-          ds[t] = x * (__uint_as_float(dv[t]) - vd[qq]);
+        for (int t4 = 0; t4 < 32; t4 += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(vl + c * 32 + t4);
+          const float4 d4 = *reinterpret_cast<const float4*>(vd + c * 32 + t4);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = t4 + u;
+            float x = exp2_fast(fmaf(__uint_as_float(sv[t]), sl2, -lv[u]));
+            if (DG && c * 32 + t < r) x = 0.f;
+            p[t] = x;
+            ds[t] = x * (__uint_as_float(dv[t]) - dl[u]);
+          }
         }
         st_row32(pt, r, c * 32, p);
         st_row32(dst, r, c * 32, ds);
+      };
+      if (qt == kt) {
+#pragma unroll 1
+        for (int c = 0; c < T / 32; ++c) chunk(c, std::true_type{});
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < T / 32; ++c) chunk(c, std::false_type{});
       }
       tc_fence_before();
       __syncwarp();
