@@ -12,7 +12,9 @@
 // The same smem tile serves as a K-major operand (rows = tokens) and as an
 // MN-major operand (K = tokens) — a [128 rows][64 cols] SW128 tile is both
 // canonical layouts — so nothing is transposed or loaded twice.
-// Warp roles: 0 TMA, 1 MMA (one thread), 2 TMEM alloc, 4..7 math (thread = row).
+// Warp roles: 0 TMA, 1 MMA (one thread), 2 TMEM alloc, 4..11 math: warp w handles the
+// rows of TMEM lane quarter (w-4)%4 and column half (w-4)/4 (no cross-column state
+// in the backward, so the per-row work splits freely).
 #include "common.cuh"
 #include "zb_internal.h"
 
@@ -24,7 +26,8 @@ namespace zb {
 namespace fab {
 
 constexpr int T = 128;  // tile rows (queries or keys)
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;   // warps 4..11: 8 math warps
+constexpr int kMath = 8;        // two per TMEM lane quarter, each on half of the columns
 constexpr float LOG2E = 1.4426950408889634f;
 
 ZB_DEVICE uint64_t desc_k(uint32_t base, int kk) {  // K-major [128 rows][64*n] tile
@@ -95,11 +98,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&kv_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&ds_full[i], 4);
+      mbar_init(&ds_full[i], kMath);
       mbar_init(&ds_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_empty, 4);
+    mbar_init(s_empty, kMath);
     mbar_init(dq_done, 1);
     fence_barrier_init();
   }
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit(dq_done);
     }
   } else if (warp >= 4) {
-    const int wq = warp - 4, r = wq * 32 + lane, q = qt * T + r;
+    const int wq = (warp - 4) & 3, half = (warp - 4) >> 2, r = wq * 32 + lane, q = qt * T + r;
     const uint32_t lo = (uint32_t)(wq * 32) << 16;
     const float sl2 = scale * LOG2E;
     const size_t vrow = ((size_t)b * H + h) * S + q;
@@ -199,12 +202,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         st_row32(ds_tile, r, c * 32, ds);
       };
+      constexpr int CH = T / 64;  // 32-column chunks per half
       if (j == qt) {
 #pragma unroll 1
-        for (int c = 0; c < T / 32; ++c) chunk(c, std::true_type{});
+        for (int c = half * CH; c < (half + 1) * CH; ++c) chunk(c, std::true_type{});
       } else {
 #pragma unroll 1
-        for (int c = 0; c < T / 32; ++c) chunk(c, std::false_type{});
+        for (int c = half * CH; c < (half + 1) * CH; ++c) chunk(c, std::false_type{});
       }
       tc_fence_before();
       __syncwarp();
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     __nv_bfloat16* out = dqkv + ((size_t)row0 + q) * ld + h * D;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
       uint32_t v[32];
       tmem_ld_32x32b_x32(t_dq + lo + c * 32, v);
       tmem_ld_wait();
@@ -289,8 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&qo_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_empty, 4);
-    mbar_init(p_full, 4);
+    mbar_init(s_empty, kMath);
+    mbar_init(p_full, kMath);
     mbar_init(p_empty, 1);
     mbar_init(done, 1);
     fence_barrier_init();
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit(done);
     }
   } else if (warp >= 4) {
-    const int wq = warp - 4, r = wq * 32 + lane;
+    const int wq = (warp - 4) & 3, half = (warp - 4) >> 2, r = wq * 32 + lane;
     const uint32_t lo = (uint32_t)(wq * 32) << 16;
     const float sl2 = scale * LOG2E;
     for (int i = 0; i < ntile; ++i) {
@@ -374,9 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* vl = vec + (i & 1) * 2 * T;
       float* vd = vl + T;
       const size_t vrow = ((size_t)b * H + h) * S + qt * T + r;
-      vl[r] = lse[vrow] * LOG2E;
-      vd[r] = delta[vrow];
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // the four math warps
+      if (half == 0) {
+        vl[r] = lse[vrow] * LOG2E;
+        vd[r] = delta[vrow];
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // the eight math warps
       mbar_wait(s_full, i & 1);
       mbar_wait(p_empty, (i & 1) ^ 1);
       tc_fence_after();
@@ -409,12 +415,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         st_row32(pt, r, c * 32, p);
         st_row32(dst, r, c * 32, ds);
       };
+      constexpr int CH = T / 64;  // 32-column chunks per half
       if (qt == kt) {
 #pragma unroll 1
-        for (int c = 0; c < T / 32; ++c) chunk(c, std::true_type{});
+        for (int c = half * CH; c < (half + 1) * CH; ++c) chunk(c, std::true_type{});
       } else {
 #pragma unroll 1
-        for (int c = 0; c < T / 32; ++c) chunk(c, std::false_type{});
+        for (int c = half * CH; c < (half + 1) * CH; ++c) chunk(c, std::false_type{});
       }
       tc_fence_before();
       __syncwarp();
@@ -429,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __nv_bfloat16* dk_row = dqkv + ((size_t)row0 + k) * ld + HD + h * D;
     __nv_bfloat16* dv_row = dk_row + HD;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
       uint32_t v[32], w[32];
       tmem_ld_32x32b_x32(t_dk + lo + c * 32, v);
       tmem_ld_32x32b_x32(t_dv + lo + c * 32, w);
