@@ -69,7 +69,7 @@ def build(verbose: bool = False, jobs: int = 8, defines=(), out: str = OUT) -> s
     _drain(procs, verbose)
     if cmds or not os.path.exists(out):
         link = ["nvcc", *ARCH, "-shared", "-o", out, *objs, "-L", nccl_lib, "-l:libnccl.so.2",
-                "-Xlinker", "-rpath", "-Xlinker", nccl_lib, "-lcudart"]
+                "-Xlinker", "-rpath", "-Xlinker", nccl_lib, "-lcudart", "-ldl"]
         if verbose:
             print(" ".join(link), flush=True)
         subprocess.run(link, check=True)

@@ -25,6 +25,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
+#include <dlfcn.h>
 #include <vector>
 #include <tuple>
 #include <mutex>
@@ -973,6 +975,44 @@ struct GemmKey {
 static std::mutex g_tune_mu;
 static std::map<GemmKey, GemmChoice> g_tuned;
 
+// Persistent tuning cache (one line per shape: M N K a_mn b_mn epi beta1 ldc pair bn
+// splits).  Path: $ZB_GEMM_TUNE_CACHE, else gemm_tune_cache.txt beside this library.
+// Loaded once; new measurements are appended, so a tuned run (or the committed file)
+// makes later runs start without tuning launches.
+static std::string tune_cache_path() {
+  if (const char* e = getenv("ZB_GEMM_TUNE_CACHE")) return e;
+  Dl_info info;
+  if (dladdr((void*)&tune_cache_path, &info) && info.dli_fname) {
+    std::string so = info.dli_fname;
+    const size_t k = so.find_last_of('/');
+    return (k == std::string::npos ? std::string(".") : so.substr(0, k)) + "/gemm_tune_cache.txt";
+  }
+  return "gemm_tune_cache.txt";
+}
+
+static void tune_cache_load() {
+  static bool loaded = false;
+  if (loaded) return;
+  loaded = true;
+  FILE* f = fopen(tune_cache_path().c_str(), "r");
+  if (!f) return;
+  GemmKey k;
+  GemmChoice c;
+  while (fscanf(f, "%d %d %d %d %d %d %d %d %d %d %d", &k.M, &k.N, &k.K, &k.a_mn, &k.b_mn, &k.epi,
+                &k.beta1, &k.ldc, &c.pair, &c.bn, &c.splits) == 11)
+    if ((c.bn == 128 || c.bn == 192 || c.bn == 256) && c.splits >= 1 && (c.pair == 0 || c.pair == 1))
+      g_tuned[k] = c;
+  fclose(f);
+}
+
+static void tune_cache_append(const GemmKey& k, const GemmChoice& c) {
+  FILE* f = fopen(tune_cache_path().c_str(), "a");
+  if (!f) return;
+  fprintf(f, "%d %d %d %d %d %d %d %d %d %d %d\n", k.M, k.N, k.K, k.a_mn, k.b_mn, k.epi, k.beta1,
+          k.ldc, c.pair, c.bn, c.splits);
+  fclose(f);
+}
+
 struct GemmCall {
   const void *A, *B, *bias, *R;
   int M, N, K, lda, ldb, ldc, ldr, ldaux, a_mn, b_mn, epilogue;
@@ -1172,6 +1212,7 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
   if (tune) {
     const GemmKey key{M, N, K, a_mn_major, b_mn_major, epilogue, beta == 1.f ? 1 : 0, ldc};
     std::lock_guard<std::mutex> lk(g_tune_mu);
+    tune_cache_load();
     auto it = g_tuned.find(key);
     if (it != g_tuned.end()) {
       ch = it->second;
@@ -1182,6 +1223,7 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
       if (st == cudaStreamCaptureStatusNone) {
         ch = tune_choice(g, ch, aux, stream);
         g_tuned[key] = ch;
+        tune_cache_append(key, ch);
         how = "tuned";
       }
     }
