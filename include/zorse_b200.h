@@ -57,11 +57,13 @@ int zb_attn_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H, 
  * by TMA, one softmax thread per query row.  S % 128 == 0. */
 int zb_attn_fwd_tc(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int D, int ld,
                    float scale, zb_stream_t stream);
-/* Backward on 5th-gen tensor cores (two passes, no atomics); contract as zb_attn_bwd,
- * dout pitch H*D, 16-byte aligned.  S % 128 == 0. */
+/* Backward on 5th-gen tensor cores; contract as zb_attn_bwd, dout pitch H*D, 16-byte
+ * aligned, S % 128 == 0.  With dq_accum (fp32 [n_seq*S][H*D] workspace) and D == 64:
+ * one fused pass (dQ partials reduce-added into dq_accum, then scaled into dqkv);
+ * otherwise two passes (dK/dV, then dQ) without atomics. */
 int zb_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const void* lse, void* dqkv,
-                   void* delta, int n_seq, int S, int H, int D, int ld, float scale,
-                   zb_stream_t stream);
+                   void* dq_accum, void* delta, int n_seq, int S, int H, int D, int ld,
+                   float scale, zb_stream_t stream);
 /* Writes dQ, dK, dV into the matching columns of dqkv (pitch ld).
  * delta: fp32 scratch [n_seq, H, S].  dq_accum: reserved (may be NULL). */
 int zb_attn_bwd(const void* qkv, const void* out, const void* dout, const void* lse, void* dqkv,

@@ -30,7 +30,7 @@ SIGNATURES = {
     "zb_attn_fwd": [P, P, P, I, I, I, I, I, F, P],
     "zb_attn_fwd_tc": [P, P, P, I, I, I, I, I, F, P],
     "zb_attn_bwd": [P, P, P, P, P, P, P, I, I, I, I, I, F, P],
-    "zb_attn_bwd_tc": [P, P, P, P, P, P, I, I, I, I, I, F, P],
+    "zb_attn_bwd_tc": [P, P, P, P, P, P, P, I, I, I, I, I, F, P],
     "zb_adamw_shard": [P, P, P, P, P, P, I64, F, F, F, F, F, F, I, P],
     "zb_adamw_shard_dstep": [P, P, P, P, P, P, I64, F, F, F, F, F, F, P, P],
     "zb_step_increment": [P, P],

@@ -243,9 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------ dK, dV
-template <int D>
+template <int D, bool FQ = false>
 struct DkvSmem {
-  static constexpr int NST = (D == 64) ? 3 : 1;  // Q/dO stages (196 KB at D = 64)
+  // Q/dO stages (196 KB at D = 64); the fused-dQ variant needs 32 KB of staging
+  static constexpr int NST = FQ ? 2 : ((D == 64) ? 3 : 1);
   static constexpr int TILE = T * D * 2;
   static constexpr int OFF_K = 0, OFF_V = TILE;
   static constexpr int OFF_Q = 2 * TILE;              // [NST] Q_i
@@ -253,16 +254,24 @@ struct DkvSmem {
   static constexpr int OFF_PT = OFF_DO + NST * TILE;  // P^T  [128 keys][128 queries]
   static constexpr int OFF_DST = OFF_PT + T * T * 2;  // dS^T
   static constexpr int OFF_VEC = OFF_DST + T * T * 2; // [2][2][128] fp32 lse*log2e, delta
-  static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * T * 4;
+  static constexpr int OFF_STG = OFF_VEC + 2 * 2 * T * 4;  // FQ: [8 warps] 32x32 fp32
+  static constexpr int OFF_BAR = OFF_STG + (FQ ? kMath * 4096 : 0);
   static constexpr int TOTAL = OFF_BAR + 256 + 1024;
 };
 
-template <int D>
+// FQ (fused dQ, D = 64): the dQ pass is folded into this kernel — per query tile the
+// MMA warp also computes the partial dQ_i = dS_i K_kt (A = dS^T tile read as MN-major,
+// B = the K tile read as MN-major) into one of two TMEM buffers, and the math warps
+// drain it to a fp32 accumulator in global memory with TMA reduce-add stores.  P and
+// dS are then computed once instead of twice (the separate dq_kernel recomputes S,
+// dP and the exponentials).  The fp32 accumulation order varies between runs.
+template <int D, bool FQ = false>
 __global__ void __launch_bounds__(kThreads, 1)
     dkdv_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                const float* __restrict__ lse, const float* __restrict__ delta,
-                __nv_bfloat16* __restrict__ dqkv, int S, int H, int ld, float scale) {
-  using L = DkvSmem<D>;
+                const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse,
+                const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H,
+                int ld, float scale) {
+  using L = DkvSmem<D, FQ>;
   constexpr int NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -276,7 +285,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = s_full + 2;
   uint64_t* p_empty = s_full + 3;
   uint64_t* done = s_full + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
+  uint64_t* dqp_full = s_full + 5;    // [2] FQ: partial dQ in TMEM
+  uint64_t* dqp_empty = s_full + 7;   // [2] FQ: drained by the math warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 9);
   float* vec = reinterpret_cast<float*>(sm + L::OFF_VEC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x;  // early key tiles see the most query tiles: launch first
@@ -297,6 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(p_full, kMath);
     mbar_init(p_empty, 1);
     mbar_init(done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&dqp_full[i], 1);
+      mbar_init(&dqp_empty[i], kMath);
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -305,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
+  const uint32_t t_dqp = tmem + 256 + 2 * D;  // FQ: [2][D] columns
 
   if (warp == 0) {
     if (lane == 0) {
@@ -363,6 +379,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_bf16_ss(t_dv, desc_k(pt_base, kk), desc_mn(do_base, kk), idesc_o, (i > 0 || kk > 0));
           mma_bf16_ss(t_dk, desc_k(dst_base, kk), desc_mn(q_base, kk), idesc_o, (i > 0 || kk > 0));
         }
+        if constexpr (FQ) {  // partial dQ_i = dS_i K (dS^T and K both read as MN-major)
+          constexpr uint32_t idesc_q = umma_idesc_bf16(T, D, 1, 1);
+          const int bb = i & 1;
+          mbar_wait(&dqp_empty[bb], ((i >> 1) & 1) ^ 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < T / 16; ++kk)
+            mma_bf16_ss(t_dqp + bb * D, desc_mn(dst_base, kk), desc_mn(k_base, kk), idesc_q,
+                        kk > 0 ? 1u : 0u);
+          mma_commit(&dqp_full[bb]);
+        }
         mma_commit(&qo_empty[st]);
         mma_commit(p_empty);
         if (NST == 1 && i + 1 < ntile) issue_s(i + 1);
@@ -373,6 +400,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wq = (warp - 4) & 3, half = (warp - 4) >> 2, r = wq * 32 + lane;
     const uint32_t lo = (uint32_t)(wq * 32) << 16;
     const float sl2 = scale * LOG2E;
+    // FQ: partial dQ of query tile kt+j (this warp: 32 rows x 32 columns) -> fp32
+    // accumulator via a TMA reduce-add store from this warp's 4 KB staging area.
+    auto drain_dq = [&](int j) {
+      uint8_t* stg = sm + L::OFF_STG + (warp - 4) * 4096;
+      const int bb = j & 1;
+      mbar_wait(&dqp_full[bb], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(t_dqp + bb * D + lo + half * 32, v);
+      tmem_ld_wait_regs(v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&dqp_empty[bb]);
+        bulk_wait_read<0>();  // the previous reduce finished reading the staging area
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+            make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
+                        __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_reduce_add_2d(&tm_dq, stg, h * D + half * 32, row0 + (kt + j) * T + wq * 32);
+        bulk_commit();
+      }
+    };
     for (int i = 0; i < ntile; ++i) {
       const int qt = kt + i;
       float* vl = vec + (i & 1) * 2 * T;
@@ -429,6 +485,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if constexpr (FQ) {
+        if (i > 0) drain_dq(i - 1);
+      }
+    }
+    if constexpr (FQ) {
+      drain_dq(ntile - 1);
+      if (lane == 0) bulk_wait_all();
     }
     mbar_wait(done, 0);
     tc_fence_after();
@@ -463,12 +526,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
+// dq (bf16, pitch ld, scaled) = dq_accum (fp32, pitch H*D)
+__global__ void dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dqkv,
+                                  int rows, int HD, int ld, float scale) {
+  const int per_row = HD / 8;
+  const int64_t n = (int64_t)rows * per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i / per_row), c8 = (int)(i % per_row) * 8;
+    const float4 a = *reinterpret_cast<const float4*>(acc + (size_t)row * HD + c8);
+    const float4 b = *reinterpret_cast<const float4*>(acc + (size_t)row * HD + c8 + 4);
+    uint4 o;
+    o.x = pack_bf16(a.x * scale, a.y * scale);
+    o.y = pack_bf16(a.z * scale, a.w * scale);
+    o.z = pack_bf16(b.x * scale, b.y * scale);
+    o.w = pack_bf16(b.z * scale, b.w * scale);
+    *reinterpret_cast<uint4*>(dqkv + (size_t)row * ld + c8) = o;
+  }
+}
+
 template <int D>
 static int run(const void* qkv, const void* out, const void* dout, const void* lse, void* dqkv,
-               void* delta, int n_seq, int S, int H, int ld, float scale, cudaStream_t s) {
+               void* dq_accum, void* delta, int n_seq, int S, int H, int ld, float scale,
+               cudaStream_t s) {
   const int Tn = n_seq * S;
   if (int rc = launch_attn_delta(out, dout, delta, Tn, S, H, D, s)) return rc;
-  CUtensorMap mq, mo;
+  CUtensorMap mq, mo, mdq;
   if (int rc = make_tmap_bf16_2d(&mq, qkv, (uint64_t)3 * H * D, Tn, ld, 64, T)) return rc;
   if (int rc = make_tmap_bf16_2d(&mo, dout, (uint64_t)H * D, Tn, (uint64_t)H * D, 64, T)) return rc;
   static bool configured = false;
@@ -476,8 +559,11 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     cudaError_t e = cudaFuncSetAttribute(dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          DqSmem<D>::TOTAL);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               DkvSmem<D>::TOTAL);
+      e = cudaFuncSetAttribute(dkdv_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               DkvSmem<D, false>::TOTAL);
+    if (e == cudaSuccess && D == 64)
+      e = cudaFuncSetAttribute(dkdv_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               DkvSmem<D, true>::TOTAL);
     if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: cudaFuncSetAttribute");
     configured = true;
   }
@@ -487,10 +573,34 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     const char* e = getenv("ZB_ATTN_BWD_ONLY");
     only = !e ? 0 : (e[0] == 'q' || (e[0] == 'd' && e[1] == 'q')) ? 1 : 2;
   }
+  static const bool two_pass = getenv("ZB_ATTN_BWD_TWO_PASS") != nullptr;  // A/B
+  if (D == 64 && dq_accum && !two_pass && !only) {
+    const int HD = H * D;
+    cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)Tn};
+    cuuint64_t strides[1] = {(cuuint64_t)HD * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    if (int rc = tensor_map_encode(&mdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_accum, dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE))
+      return rc;
+    cudaError_t e = cudaMemsetAsync(dq_accum, 0, (size_t)Tn * HD * 4, s);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: dq_accum memset");
+    dkdv_kernel<D, true><<<grid, kThreads, DkvSmem<D, true>::TOTAL, s>>>(
+        mq, mo, mdq, (const float*)lse, (const float*)delta, (__nv_bfloat16*)dqkv, S, H, ld, scale);
+    const int64_t n8 = (int64_t)Tn * (HD / 8);
+    int cg = (int)((n8 + 255) / 256);
+    if (cg > num_sms() * 8) cg = num_sms() * 8;
+    dq_convert_kernel<<<cg, 256, 0, s>>>((const float*)dq_accum, (__nv_bfloat16*)dqkv, Tn, HD, ld,
+                                         scale);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_bwd_tc fused launch");
+  }
   if (only != 1)
-    dkdv_kernel<D><<<grid, kThreads, DkvSmem<D>::TOTAL, s>>>(mq, mo, (const float*)lse,
-                                                            (const float*)delta,
-                                                            (__nv_bfloat16*)dqkv, S, H, ld, scale);
+    dkdv_kernel<D, false><<<grid, kThreads, DkvSmem<D, false>::TOTAL, s>>>(
+        mq, mo, mq /*unused*/, (const float*)lse, (const float*)delta, (__nv_bfloat16*)dqkv, S, H,
+        ld, scale);
   if (only != 2)
     dq_kernel<D><<<grid, kThreads, DqSmem<D>::TOTAL, s>>>(mq, mo, (const float*)lse,
                                                         (const float*)delta, (__nv_bfloat16*)dqkv,
@@ -505,13 +615,17 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
 using namespace zb;
 
 extern "C" int zb_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const void* lse,
-                              void* dqkv, void* delta, int n_seq, int S, int H, int D, int ld,
-                              float scale, cudaStream_t s) {
+                              void* dqkv, void* dq_accum, void* delta, int n_seq, int S, int H,
+                              int D, int ld, float scale, cudaStream_t s) {
   if (S % 128) return set_error(ZB_ERR_INVALID, "attn_bwd_tc: seq_len must be a multiple of 128");
   if (ld % 8 || ((uintptr_t)qkv & 15) || ((uintptr_t)dout & 15))
     return set_error(ZB_ERR_INVALID, "attn_bwd_tc: bad ld/alignment");
   if (n_seq <= 0) return 0;
-  if (D == 64) return fab::run<64>(qkv, out, dout, lse, dqkv, delta, n_seq, S, H, ld, scale, s);
-  if (D == 128) return fab::run<128>(qkv, out, dout, lse, dqkv, delta, n_seq, S, H, ld, scale, s);
+  if (dq_accum && ((uintptr_t)dq_accum & 15))
+    return set_error(ZB_ERR_INVALID, "attn_bwd_tc: dq_accum must be 16-byte aligned");
+  if (D == 64)
+    return fab::run<64>(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, S, H, ld, scale, s);
+  if (D == 128)
+    return fab::run<128>(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, S, H, ld, scale, s);
   return set_error(ZB_ERR_UNSUPPORTED, "attn_bwd_tc: head_dim %d unsupported (64, 128)", D);
 }

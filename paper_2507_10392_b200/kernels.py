@@ -141,8 +141,8 @@ def attn_bwd(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, seq_len, n_head,
     _need_cuda(qkv, out, dout, lse, dqkv, dq_accum, delta)
     if impl == "tc":
         call("zb_attn_bwd_tc", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), _ptr(dqkv),
-             _ptr(delta), n_seq, seq_len, n_head, head_dim, qkv.stride(0), float(scale),
-             _stream())
+             _ptr(dq_accum), _ptr(delta), n_seq, seq_len, n_head, head_dim, qkv.stride(0),
+             float(scale), _stream())
         return
     call("zb_attn_bwd", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), _ptr(dqkv), _ptr(dq_accum),
          _ptr(delta), n_seq, seq_len, n_head, head_dim, qkv.stride(0), float(scale), _stream())

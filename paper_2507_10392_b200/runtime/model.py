@@ -24,7 +24,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass
-from typing import Dict, List, Tuple
+from typing import Dict, List, Optional, Tuple
 
 import torch
 
@@ -173,6 +173,7 @@ class BwdScratch:
     da: torch.Tensor      # [n, d]
     dqkv: torch.Tensor    # [n, 3d]
     delta: torch.Tensor   # [seqs, H, S]
+    dq_accum: Optional[torch.Tensor] = None  # [n, d] fp32: fused attention backward (D = 64)
 
 
 def alloc_bwd_scratch(cfg: ModelConfig, n_tok: int, device) -> BwdScratch:
@@ -181,7 +182,9 @@ def alloc_bwd_scratch(cfg: ModelConfig, n_tok: int, device) -> BwdScratch:
     bf = dict(device=device, dtype=torch.bfloat16)
     return BwdScratch(dh=torch.empty(n, d, **bf), dx_mid=torch.empty(n, d, **bf),
                       da=torch.empty(n, d, **bf), dqkv=torch.empty(n, 3 * d, **bf),
-                      delta=torch.empty(max(n_tok // S, 1), H, S, device=device))
+                      delta=torch.empty(max(n_tok // S, 1), H, S, device=device),
+                      dq_accum=(torch.empty(n, d, device=device, dtype=torch.float32)
+                                if cfg.head_dim == 64 else None))
 
 
 class GptOps:
@@ -234,7 +237,8 @@ class GptOps:
         o.gemm(s.dx_mid[:n], a.attn[:n], gr["proj_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         o.bias_grad(s.dx_mid[:n], gr["proj_b"])
         o.gemm(s.dx_mid[:n], p["proj_w"], s.da[:n], b_t=True)
-        o.attn_bwd(a.qkv[:n], a.attn[:n], s.da[:n], a.lse[:n_seq], s.dqkv[:n], None,
+        o.attn_bwd(a.qkv[:n], a.attn[:n], s.da[:n], a.lse[:n_seq], s.dqkv[:n],
+                   s.dq_accum[:n] if s.dq_accum is not None else None,
                    s.delta[:n_seq], n_seq, cfg.seq_len, cfg.n_head, cfg.head_dim, self.scale)
         o.gemm(s.dqkv[:n], a.h1[:n], gr["qkv_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         o.bias_grad(s.dqkv[:n], gr["qkv_b"])
@@ -301,7 +305,8 @@ class LlamaOps:
                       gr["mlp_norm"], dx_accum=dy)
         o.gemm(s.dx_mid[:n], a.attn[:n], gr["o_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         o.gemm(s.dx_mid[:n], p["o_w"], s.da[:n], b_t=True)
-        o.attn_bwd(a.qkv[:n], a.attn[:n], s.da[:n], a.lse[:n_seq], s.dqkv[:n], None,
+        o.attn_bwd(a.qkv[:n], a.attn[:n], s.da[:n], a.lse[:n_seq], s.dqkv[:n],
+                   s.dq_accum[:n] if s.dq_accum is not None else None,
                    s.delta[:n_seq], n_seq, cfg.seq_len, cfg.n_head, cfg.head_dim, self.scale)
         o.rope(s.dqkv[:n], cfg.seq_len, cfg.n_head, cfg.head_dim, self.ROPE_THETA, inverse=True)
         o.gemm(s.dqkv[:n], a.h1[:n], gr["qkv_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)

@@ -20,6 +20,7 @@ for (n, S, H, D) in [(8, 1024, 12, 64), (11, 1024, 12, 64), (2, 2048, 32, 128), 
     lse = torch.empty(n, H, S, device="cuda")
     dout = torch.randn(T, H * D, device="cuda").bfloat16()
     dqkv = torch.empty_like(qkv); delta = torch.empty(n, H, S, device="cuda")
+    dq_acc = torch.empty(T, H * D, device="cuda")
     sc = 1 / math.sqrt(D)
     fl = 4.0 * n * H * S * S * D / 2
     r = {"shape": [n, S, H, D]}
@@ -27,6 +28,6 @@ for (n, S, H, D) in [(8, 1024, 12, 64), (11, 1024, 12, 64), (2, 2048, 32, 128), 
         ms = t_ms(lambda: K.attn_fwd(qkv, out, lse, n, S, H, D, sc, impl=impl))
         r[f"fwd_{impl}_ms"] = ms; r[f"fwd_{impl}_tflops"] = fl / ms / 1e9
     for impl in ("tc", "mma"):
-        ms = t_ms(lambda: K.attn_bwd(qkv, out, dout, lse, dqkv, None, delta, n, S, H, D, sc, impl=impl))
+        ms = t_ms(lambda: K.attn_bwd(qkv, out, dout, lse, dqkv, dq_acc if impl == "tc" else None, delta, n, S, H, D, sc, impl=impl))
         r[f"bwd_{impl}_ms"] = ms; r[f"bwd_{impl}_tflops(2.5x fwd flops)"] = 2.5 * fl / ms / 1e9
     print(json.dumps(r), flush=True)

@@ -103,10 +103,12 @@ def _attn_ref(qkv, n_seq, S, H, D):
     return o.transpose(1, 2).reshape(n_seq * S, H * D), lse
 
 
-@pytest.mark.parametrize("impl", ["tc", "mma"])
+@pytest.mark.parametrize("impl", ["tc", "tc-fused-dq", "mma"])
 @pytest.mark.parametrize("n_seq,S,H,D", [(2, 128, 4, 64), (1, 1024, 3, 64), (2, 256, 2, 128),
-                                         (1, 2048, 2, 128)])
+                                         (1, 2048, 2, 128), (3, 512, 12, 64)])
 def test_attention_fwd_bwd(cuda, n_seq, S, H, D, impl):
+    fused = impl == "tc-fused-dq"
+    impl = "tc" if fused else impl
     torch.manual_seed(4)
     T = n_seq * S
     qkv = torch.randn(T, 3 * H * D, device="cuda").bfloat16()
@@ -123,7 +125,9 @@ def test_attention_fwd_bwd(cuda, n_seq, S, H, D, impl):
     ro.backward(dout.float())
     dqkv = torch.empty_like(qkv)
     delta = torch.empty(n_seq, H, S, device="cuda")
-    K.attn_bwd(qkv, out, dout, lse, dqkv, None, delta, n_seq, S, H, D, scale, impl=impl)
+    # tc + dq_accum: single fused pass at D = 64 (dQ by fp32 reduce-add)
+    dq_acc = torch.empty(T, H * D, device="cuda") if fused else None
+    K.attn_bwd(qkv, out, dout, lse, dqkv, dq_acc, delta, n_seq, S, H, D, scale, impl=impl)
     torch.cuda.synchronize()
     g = qf.grad.view(T, 3, H * D)
     d = dqkv.view(T, 3, H * D)
