@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
   const uint32_t t_dqp = tmem + 256 + 2 * D;  // FQ: [2][D] columns
+  griddep_wait();  // PDL: prologue overlapped the previous kernel's tail
 
   if (warp == 0) {
     if (lane == 0) {
@@ -550,6 +551,12 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
                void* dq_accum, void* delta, int n_seq, int S, int H, int ld, float scale,
                cudaStream_t s) {
   const int Tn = n_seq * S;
+  static const bool two_pass = getenv("ZB_ATTN_BWD_TWO_PASS") != nullptr;  // A/B
+  const bool fused = D == 64 && dq_accum && !two_pass;
+  if (fused) {  // before the delta kernel, so the PDL launch below follows a kernel
+    cudaError_t e = cudaMemsetAsync(dq_accum, 0, (size_t)Tn * H * D * 4, s);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: dq_accum memset");
+  }
   if (int rc = launch_attn_delta(out, dout, delta, Tn, S, H, D, s)) return rc;
   CUtensorMap mq, mo, mdq;
   if (int rc = make_tmap_bf16_2d(&mq, qkv, (uint64_t)3 * H * D, Tn, ld, 64, T)) return rc;
@@ -573,8 +580,7 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     const char* e = getenv("ZB_ATTN_BWD_ONLY");
     only = !e ? 0 : (e[0] == 'q' || (e[0] == 'd' && e[1] == 'q')) ? 1 : 2;
   }
-  static const bool two_pass = getenv("ZB_ATTN_BWD_TWO_PASS") != nullptr;  // A/B
-  if (D == 64 && dq_accum && !two_pass && !only) {
+  if (fused && !only) {
     const int HD = H * D;
     cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)Tn};
     cuuint64_t strides[1] = {(cuuint64_t)HD * 4};
@@ -585,10 +591,19 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE))
       return rc;
-    cudaError_t e = cudaMemsetAsync(dq_accum, 0, (size_t)Tn * HD * 4, s);
-    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: dq_accum memset");
-    dkdv_kernel<D, true><<<grid, kThreads, DkvSmem<D, true>::TOTAL, s>>>(
-        mq, mo, mdq, (const float*)lse, (const float*)delta, (__nv_bfloat16*)dqkv, S, H, ld, scale);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = DkvSmem<D, true>::TOTAL;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = getenv("ZB_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, dkdv_kernel<D, true>, mq, mo, mdq, (const float*)lse,
+                                       (const float*)delta, (__nv_bfloat16*)dqkv, S, H, ld, scale);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc fused launch");
     const int64_t n8 = (int64_t)Tn * (HD / 8);
     int cg = (int)((n8 + 255) / 256);
     if (cg > num_sms() * 8) cg = num_sms() * 8;

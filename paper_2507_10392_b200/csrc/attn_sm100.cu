@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_s = tmem + COL_S, t_p = tmem + COL_P, t_o = tmem + COL_O;
+  griddep_wait();  // PDL: prologue overlapped the previous kernel's tail
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -678,9 +679,19 @@ static int run(const void* qkv, void* out, void* lse, int n_seq, int S, int H, i
   const int items = (S / BQ) * H * n_seq;
   const int slots = 2 * num_sms();
   const int grid = items < slots ? items : slots;
-  fwd_ts_kernel<<<grid, kThreads, SMEM_BYTES, s>>>(m128, m64, (__nv_bfloat16*)out, (float*)lse, S,
-                                                   H, n_seq, scale);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = getenv("ZB_NO_PDL") ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fwd_ts_kernel, m128, m64, (__nv_bfloat16*)out,
+                                     (float*)lse, S, H, n_seq, scale);
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_cuda_error(e, "attn fwd_ts launch");
 }
 }  // namespace fa_ts

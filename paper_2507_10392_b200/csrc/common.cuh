@@ -185,6 +185,12 @@ ZB_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::
 
 // Make this thread's generic-proxy shared-memory writes visible to the async
 // proxy (tcgen05.mma operand reads through smem descriptors, TMA).
+// Programmatic dependent launch: a kernel launched with the programmatic stream
+// serialisation attribute may start (prologue: barriers, TMEM, descriptor
+// prefetch) while its predecessor's last CTAs drain; it must wait here before
+// touching memory the predecessor produces or consumes.
+ZB_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 ZB_DEVICE void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

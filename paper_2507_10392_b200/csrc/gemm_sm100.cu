@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // prologue above overlapped the previous kernel's tail (PDL launch)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -618,6 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // prologue above overlapped the previous kernel's tail (PDL launch)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -795,6 +797,24 @@ static int make_tmap_epi(CUtensorMap* m, const void* ptr, bool f32, uint64_t col
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
+// Launch with programmatic stream serialisation (PDL): the GEMM's prologue overlaps
+// the previous kernel's tail; the kernel waits (griddep_wait) before any global access.
+template <typename Kern, typename... Args>
+static cudaError_t launch_pdl(Kern kern, dim3 grid, int smem, cudaStream_t stream, Args... args) {
+  static const bool off = getenv("ZB_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int BN, int A_MN, int B_MN, int EPI>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm& et,
                        GemmArgs args, cudaStream_t stream) {
@@ -816,8 +836,9 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm
   args.splits = (num_kb + args.kb_per_split - 1) / args.kb_per_split;
   const int units = tiles * args.splits;
   int grid = units < num_sms() ? units : num_sms();
-  kern<<<grid, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, et.c, et.aux, et.r, args);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(kern, dim3(grid), Cfg::SMEM_BYTES, stream, ta, tb, et.c, et.aux, et.r,
+                             args);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   return 0;
 }
@@ -880,8 +901,9 @@ static int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const EpiT
   args.splits = (num_kb + args.kb_per_split - 1) / args.kb_per_split;
   const int units = tiles * args.splits;
   const int clusters = units < pairs ? units : pairs;
-  kern<<<2 * clusters, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, et.c, et.aux, et.r, args);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(kern, dim3(2 * clusters), Cfg::SMEM_BYTES, stream, ta, tb, et.c,
+                             et.aux, et.r, args);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "gemm2cta launch");
   return 0;
 }
