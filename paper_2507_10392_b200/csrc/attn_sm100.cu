@@ -359,11 +359,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // passes over the S row in TMEM (max, then exp / sum / pack) instead of holding
 // 128 values in registers.
 namespace fa_ts {
-constexpr int BQ = 128, BKV = 128, D = 64, NST = 2, kThreads = 256;
+constexpr int BQ = 128, BKV = 128, D = 64, NST = 2, kThreads = 384;
+constexpr int kSoft = 8;  // softmax warps: two per TMEM lane quarter, one per column half
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr int Q_BYTES = BQ * D * 2, K_BYTES = BKV * D * 2, V_BYTES = BKV * D * 2;
 constexpr int OFF_Q = 0, OFF_K = 2 * Q_BYTES, OFF_V = OFF_K + NST * K_BYTES;  // Q double-buffered
-constexpr int OFF_BAR = OFF_V + NST * V_BYTES;
+constexpr int OFF_X = OFF_V + NST * V_BYTES;  // [2 halves][128 rows] fp32 row-max / row-sum exchange
+constexpr int OFF_BAR = OFF_X + 2 * BQ * 4;
 constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;
 constexpr uint32_t COL_S = 0, COL_P = 128, COL_O = 192, TMEM_COLS = 256;
 
@@ -415,11 +417,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(&kv_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_empty, 4);
-    mbar_init(p_full, 4);
+    mbar_init(s_empty, kSoft);
+    mbar_init(p_full, kSoft);
     mbar_init(&o_bar[0], 1);
     mbar_init(&o_bar[1], 1);
-    mbar_init(o_empty, 4);
+    mbar_init(o_empty, kSoft);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -499,10 +501,15 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue
-    const int wq = warp - 4;
+    // Warp w owns rows of TMEM lane quarter (w-4)%4 and the column half (w-4)/4 of
+    // every S / P / O tile; the two warps of a quarter exchange their partial row
+    // maxima (and, at the end, row sums) through smem with a 64-thread named barrier.
+    const int wq = (warp - 4) & 3, hf = (warp - 4) >> 2;
     const int r = wq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const float sl2 = scale * LOG2E;
+    float* xch = reinterpret_cast<float*>(sm + OFF_X);  // [2][BQ]
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory"); };
     constexpr float RESCALE_T = 8.f;  // lazy O rescale (see fwd_kernel)
     int gbase = 0, o_seen = 0;
 #ifdef ZB_EXP_TRACE
@@ -533,12 +540,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 #ifdef ZB_EXP_TRACE
         long long tr1 = clock64();
 #endif
-        // pass 1: row max (masking only on the diagonal block; 3-input max)
-        auto row_max = [&](auto diag_c) {
+        // pass 1: max over this warp's 64 columns (masking only on the diagonal block)
+        auto half_max = [&](auto diag_c) {
           constexpr bool DG = decltype(diag_c)::value;
           float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int c = 0; c < BKV / 32; ++c) {
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = hf * 2 + cc;
             uint32_t v[32];
             tmem_ld_32x32b_x32(t_s + lane_off + c * 32, v);
             tmem_ld_wait_regs(v);
@@ -556,9 +564,13 @@ __global__ void __launch_bounds__(kThreads, 2)
               mx4[3] = fmax3(mx4[3], x[i + 6], x[i + 7]);
             }
           }
-          return fmaxf(fmax3(mx4[0], mx4[1], mx4[2]), mx4[3]) * sl2;
+          return fmaxf(fmax3(mx4[0], mx4[1], mx4[2]), mx4[3]);
         };
-        const float mx = diag ? row_max(std::true_type{}) : row_max(std::false_type{});
+        const float mh = diag ? half_max(std::true_type{}) : half_max(std::false_type{});
+        xch[hf * BQ + r] = mh;
+        pair_sync();
+        const float mx = fmaxf(mh, xch[(hf ^ 1) * BQ + r]) * sl2;
+        pair_sync();  // both halves read before the next block overwrites
         const bool move = mx > m + RESCALE_T;
         const float m_new = move ? mx : m;
         const float corr = move ? exp2_fast(m - m_new) : 1.f;
@@ -572,23 +584,21 @@ __global__ void __launch_bounds__(kThreads, 2)
 #ifdef ZB_EXP_TRACE
         long long tr3 = clock64();
 #endif
-        if (j > 0 && __any_sync(0xffffffffu, move)) {
+        if (j > 0 && __any_sync(0xffffffffu, move)) {  // this half's 32 O columns
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_o + lane_off + hf * 32, v);
+          tmem_ld_wait_regs(v);
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
-            tmem_ld_wait_regs(v);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
-            tmem_st_32x32b_x32(t_o + lane_off + c * 32, v);
-          }
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+          tmem_st_32x32b_x32(t_o + lane_off + hf * 32, v);
         }
-        // pass 2: exponentials, row sum, bf16 P row into TMEM
+        // pass 2: exponentials, partial row sum, bf16 P into TMEM
         auto exp_pack = [&](auto diag_c) {
           constexpr bool DG = decltype(diag_c)::value;
           float rs4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int c = 0; c < BKV / 32; ++c) {
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = hf * 2 + cc;
             uint32_t v[32];
             tmem_ld_32x32b_x32(t_s + lane_off + c * 32, v);
             tmem_ld_wait_regs(v);
@@ -610,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
         };
         const float rs = diag ? exp_pack(std::true_type{}) : exp_pack(std::false_type{});
-        l = l * corr + rs;
+        l = l * corr + rs;  // this half's share of the row sum
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -624,15 +634,18 @@ __global__ void __launch_bounds__(kThreads, 2)
         ++acc_n;
 #endif
       }
-      // epilogue: O / l -> bf16 row, lse
+      // epilogue: O / l -> bf16 row (this half's 32 columns), lse
+      xch[hf * BQ + r] = l;
+      pair_sync();
+      const float lt = l + xch[(hf ^ 1) * BQ + r];
+      pair_sync();
       consume_o(gbase + nblk);
       tc_fence_after();
-      const float inv = 1.f / l;
-      __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D;
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      const float inv = 1.f / lt;
+      __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D + hf * 32;
+      {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+        tmem_ld_32x32b_x32(t_o + lane_off + hf * 32, v);
         tmem_ld_wait_regs(v);
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
@@ -641,17 +654,17 @@ __global__ void __launch_bounds__(kThreads, 2)
           pk.y = pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
           pk.z = pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
           pk.w = pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
-          *reinterpret_cast<uint4*>(orow + c * 32 + i) = pk;
+          *reinterpret_cast<uint4*>(orow + i) = pk;
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty);
-      lse[((size_t)b * H + h) * S + q] = (m + __log2f(l)) / LOG2E;
+      if (hf == 0) lse[((size_t)b * H + h) * S + q] = (m + __log2f(lt)) / LOG2E;
       gbase += nblk;
     }
 #ifdef ZB_EXP_TRACE  // per-CTA phase cycle totals (debug builds: build(defines=("ZB_EXP_TRACE",)))
-    if (r == 0 && (blockIdx.x == 0 || blockIdx.x == 100 || blockIdx.x == 250 || blockIdx.x == 295))
+    if (r == 0 && hf == 0 && (blockIdx.x == 0 || blockIdx.x == 100 || blockIdx.x == 250 || blockIdx.x == 295))
       printf("cta %d: blocks %d total %lld wait_s %lld pass1 %lld wait_o %lld pass2 %lld\n",
              blockIdx.x, acc_n, clock64() - t_start, acc_t[0], acc_t[1], acc_t[2], acc_t[3]);
 #endif
