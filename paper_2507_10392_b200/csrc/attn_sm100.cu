@@ -709,6 +709,374 @@ static int run(const void* qkv, void* out, void* lse, int n_seq, int S, int H, i
 }
 }  // namespace fa_ts
 
+// ---------------------------------------------------------------- two query tiles per CTA
+// One persistent CTA per SM processes PAIRS of query tiles (A = 2p, B = 2p+1) of one
+// (head, sequence): the tensor core alternates between the tiles —
+//   S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...
+// so while softmax warpgroup A works on S_A(j+1), the tensor core computes PV_B(j) and
+// S_B(j+1), and vice versa.  P_X is written into the first columns of S_X (bf16
+// pairs) and consumed from TMEM by the PV MMA; S_X(j+1) is issued after PV_X(j), and
+// tcgen05 MMAs of one thread execute in order, so S_X(j+1) completing also means
+// PV_X(j) consumed P_X(j) and O_X holds P_X(j) V_j (the rescale point).
+// TMEM: S_A | S_B | O_A | O_B = 256 + 2D columns.  K/V blocks are shared by the two tiles.
+namespace fa_pp {
+constexpr int BQ = 128, BKV = 128;
+// HV = softmax warps per TMEM lane quarter and tile (column halves of S / O)
+template <int HV> constexpr int threads_for() { return 128 + 2 * 4 * HV * 32; }
+constexpr float LOG2E = 1.4426950408889634f;
+template <int D>
+struct Smem {
+  static constexpr int NST = (D == 64) ? 4 : 2;
+  static constexpr int Q_BYTES = BQ * D * 2, KV_BYTES = BKV * D * 2;
+  static constexpr int OFF_QA = 0, OFF_QB = Q_BYTES;
+  static constexpr int OFF_K = 2 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + NST * KV_BYTES;
+  static constexpr int OFF_X = OFF_V + NST * KV_BYTES;  // [2 tiles][2 halves][128] exchange
+  static constexpr int OFF_BAR = OFF_X + 2 * 2 * BQ * 4;
+  static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+};
+
+template <int D, int HV>
+__global__ void __launch_bounds__(threads_for<HV>(), 1)
+    fwd_pp_kernel(const __grid_constant__ CUtensorMap tm_rows128,
+                  const __grid_constant__ CUtensorMap tm_rows64, __nv_bfloat16* __restrict__ out,
+                  float* __restrict__ lse, int S, int H, int n_seq, float scale) {
+  using L = Smem<D>;
+  constexpr int NST = L::NST;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* q_empty = bar + 1;
+  uint64_t* kv_full = bar + 2;            // [NST]
+  uint64_t* kv_empty = bar + 2 + NST;     // [NST]
+  uint64_t* s_full = bar + 2 + 2 * NST;   // [2] per tile
+  uint64_t* p_full = s_full + 2;          // [2] per tile (count 4)
+  uint64_t* o_done = s_full + 4;          // [2] per tile: last PV of the item
+  uint64_t* o_empty = s_full + 6;         // [2] per tile: epilogue read O (count 4)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int npair = S / (2 * BQ);
+  const int HD = H * D;
+  const int per_q = H * n_seq;
+  const int items = npair * per_q;
+  const int P = gridDim.x;
+  auto item_of = [&](int k) { return k * P + ((k & 1) ? (P - 1 - (int)blockIdx.x) : (int)blockIdx.x); };
+  auto decode = [&](int t, int& pr, int& h, int& b) {
+    pr = npair - 1 - t / per_q;  // heavy pairs first
+    const int rem = t % per_q;
+    h = rem % H;
+    b = rem / H;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_rows128);
+    tma_prefetch_desc(&tm_rows64);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&s_full[x], 1);
+      mbar_init(&p_full[x], 4 * HV);
+      mbar_init(&o_done[x], 1);
+      mbar_init(&o_empty[x], 4 * HV);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // PDL: prologue overlapped the previous kernel's tail
+  const uint32_t t_s[2] = {tmem, tmem + 128};
+  const uint32_t t_o[2] = {tmem + 256, tmem + 256 + D};
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int g = 0, lt = 0;
+      for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
+        int pr, h, b;
+        decode(t, pr, h, b);
+        const int row0 = b * S, qa = 2 * pr, qb = qa + 1;
+        mbar_wait(q_empty, (lt & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, 2 * L::Q_BYTES);
+#pragma unroll
+        for (int kc = 0; kc < D / 64; ++kc) {
+          tma_load_2d(sm + L::OFF_QA + kc * BQ * 128, &tm_rows128, q_full, h * D + kc * 64,
+                      row0 + qa * BQ);
+          tma_load_2d(sm + L::OFF_QB + kc * BQ * 128, &tm_rows128, q_full, h * D + kc * 64,
+                      row0 + qb * BQ);
+        }
+        for (int j = 0; j <= qb; ++j, ++g) {
+          const int st = g % NST;
+          mbar_wait(&kv_empty[st], ((g / NST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[st], 2 * L::KV_BYTES);
+          uint8_t* kd = sm + L::OFF_K + st * L::KV_BYTES;
+          uint8_t* vd = sm + L::OFF_V + st * L::KV_BYTES;
+          const int kr = row0 + j * BKV;
+#pragma unroll
+          for (int kc = 0; kc < D / 64; ++kc)
+            tma_load_2d(kd + kc * BKV * 128, &tm_rows128, &kv_full[st], HD + h * D + kc * 64, kr);
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+            for (int dc = 0; dc < D / 64; ++dc)
+              tma_load_2d(vd + (kb * (D / 64) + dc) * 8192, &tm_rows64, &kv_full[st],
+                          2 * HD + h * D + dc * 64, kr + kb * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(BQ, BKV, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(BQ, D, 0, 1);
+      const uint32_t q_base[2] = {smem_u32(sm + L::OFF_QA), smem_u32(sm + L::OFF_QB)};
+      int g = 0, lt = 0;
+      int ns[2] = {0, 0};  // S blocks issued per tile (parity of p_full waits)
+      for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
+        int pr, h, b;
+        decode(t, pr, h, b);
+        const int qa = 2 * pr, qb = qa + 1;
+        const int last[2] = {qa, qb};
+        mbar_wait(q_full, lt & 1);
+        auto issue_s = [&](int x, int j) {  // S_x(j) = Q_x K_j^T
+          const int st = (g + j) % NST;
+          mbar_wait(&kv_full[st], ((g + j) / NST) & 1);
+          tc_fence_after();
+          const uint32_t k_base = smem_u32(sm + L::OFF_K + st * L::KV_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_bf16_ss(t_s[x], desc_kmajor(q_base[x], kk, BQ), desc_kmajor(k_base, kk, BKV),
+                        idesc_s, kk > 0 ? 1u : 0u);
+          mma_commit(&s_full[x]);
+        };
+        auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P_x from TMEM
+          const int st = (g + j) % NST;
+          mbar_wait(&p_full[x], ns[x] & 1);
+          ++ns[x];
+          if (j == 0) mbar_wait(&o_empty[x], (lt & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t v_base = smem_u32(sm + L::OFF_V + st * L::KV_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk) {
+            const uint64_t bdesc = umma_desc_sw128(
+                v_base + (kk >> 2) * (D / 64) * 8192 + (kk & 3) * 2048, 8192, 1024);
+            // P keys [64h, 64h+64) sit in the S columns of half h (see the softmax)
+            const uint32_t a_tm = HV == 2 ? t_s[x] + (kk >> 2) * 64 + (kk & 3) * 8 : t_s[x] + kk * 8;
+            mma_bf16_ts(t_o[x], a_tm, bdesc, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          if (j == last[x]) mma_commit(&o_done[x]);
+        };
+        issue_s(0, 0);
+        issue_s(1, 0);
+        for (int j = 0; j <= qb; ++j) {
+          if (j <= qa) {
+            issue_pv(0, j);
+            if (j + 1 <= qa) issue_s(0, j + 1);
+          }
+          issue_pv(1, j);
+          mma_commit(&kv_empty[(g + j) % NST]);  // K_j, V_j no longer read
+          if (j + 1 <= qb) issue_s(1, j + 1);
+        }
+        mma_commit(q_empty);
+        g += qb + 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax: per tile, 4*HV warps
+    // (warp -> TMEM lane quarter wq and column half hf; with HV == 2 the halves
+    // exchange row maxima / sums through smem with a 64-thread named barrier and each
+    // half writes its P columns into its own S columns: keys [64h, 64h+64) -> S
+    // columns [64h, 64h+32))
+    const int idx = warp - 4;
+    const int x = idx / (4 * HV);
+    const int sub = idx % (4 * HV);
+    const int wq = sub & 3, hf = HV == 2 ? (sub >> 2) : 0;
+    const int r = wq * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const float sl2 = scale * LOG2E;
+    constexpr float RESCALE_T = 8.f;
+    constexpr int NCH = (BKV / 32) / HV;  // 32-column S chunks per warp
+    const uint32_t ts = t_s[x], to = t_o[x];
+    float* xch = reinterpret_cast<float*>(sm + L::OFF_X) + x * 2 * BQ;
+    auto pair_sync = [&]() {
+      if constexpr (HV == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + x * 4 + wq) : "memory");
+    };
+    int nb = 0, lt = 0;  // S blocks consumed by this tile (s_full parity)
+    for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
+      int pr, h, b;
+      decode(t, pr, h, b);
+      const int qx = 2 * pr + x;             // this warpgroup's query tile
+      const int row0 = b * S;
+      const int q = qx * BQ + r;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j <= qx; ++j) {
+        const bool diag = j == qx;
+        mbar_wait(&s_full[x], nb & 1);
+        ++nb;
+        tc_fence_after();
+        auto row_max = [&](auto diag_c) {
+          constexpr bool DG = decltype(diag_c)::value;
+          float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int cc = 0; cc < NCH; ++cc) {
+            const int c = hf * NCH + cc;
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(ts + lane_off + c * 32, v);
+            tmem_ld_wait_regs(v);
+            float xs[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              xs[i] = __uint_as_float(v[i]);
+              if (DG && c * 32 + i > r) xs[i] = -INFINITY;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              mx4[0] = fmax3(mx4[0], xs[i], xs[i + 1]);
+              mx4[1] = fmax3(mx4[1], xs[i + 2], xs[i + 3]);
+              mx4[2] = fmax3(mx4[2], xs[i + 4], xs[i + 5]);
+              mx4[3] = fmax3(mx4[3], xs[i + 6], xs[i + 7]);
+            }
+          }
+          return fmaxf(fmax3(mx4[0], mx4[1], mx4[2]), mx4[3]);
+        };
+        float mh = diag ? row_max(std::true_type{}) : row_max(std::false_type{});
+        if constexpr (HV == 2) {
+          xch[hf * BQ + r] = mh;
+          pair_sync();
+          mh = fmaxf(mh, xch[(hf ^ 1) * BQ + r]);
+          pair_sync();
+        }
+        const float mx = mh * sl2;
+        const bool move = mx > m + RESCALE_T;
+        const float m_new = move ? mx : m;
+        const float corr = move ? exp2_fast(m - m_new) : 1.f;
+        m = m_new;
+        if (j > 0 && __any_sync(0xffffffffu, move)) {  // O holds P(j-1) V_{j-1} (see above)
+#pragma unroll
+          for (int c = hf * (D / 32 / HV); c < (hf + 1) * (D / 32 / HV); ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(to + lane_off + c * 32, v);
+            tmem_ld_wait_regs(v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st_32x32b_x32(to + lane_off + c * 32, v);
+          }
+        }
+        // exponentials; P for S chunk c lands in S columns [pbase + 16(c - first), +16),
+        // inside this warp's own (already read) S columns
+        auto exp_pack = [&](auto diag_c) {
+          constexpr bool DG = decltype(diag_c)::value;
+          float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int cc = 0; cc < NCH; ++cc) {
+            const int c = hf * NCH + cc;
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(ts + lane_off + c * 32, v);
+            tmem_ld_wait_regs(v);
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float p0 = exp2_fast(fmaf(__uint_as_float(v[i]), sl2, -m));
+              const float x1 = fmaf(__uint_as_float(v[i + 1]), sl2, -m);
+              float p1 = ((i >> 1) & 1) ? exp2_poly(x1) : exp2_fast(x1);
+              if (DG && c * 32 + i > r) p0 = 0.f;
+              if (DG && c * 32 + i + 1 > r) p1 = 0.f;
+              rs4[(i >> 1) & 3] += p0 + p1;
+              pk[i >> 1] = pack_bf16(p0, p1);
+            }
+            tmem_st_32x32b_x16(ts + lane_off + hf * 64 + cc * 16, pk);
+          }
+          return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+        };
+        const float rs = diag ? exp_pack(std::true_type{}) : exp_pack(std::false_type{});
+        l = l * corr + rs;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[x]);
+      }
+      // epilogue
+      float lt_sum = l;
+      if constexpr (HV == 2) {
+        xch[hf * BQ + r] = l;
+        pair_sync();
+        lt_sum = l + xch[(hf ^ 1) * BQ + r];
+        pair_sync();
+      }
+      mbar_wait(&o_done[x], lt & 1);
+      tc_fence_after();
+      const float inv = 1.f / lt_sum;
+      __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D;
+#pragma unroll
+      for (int c = hf * (D / 32 / HV); c < (hf + 1) * (D / 32 / HV); ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(to + lane_off + c * 32, v);
+        tmem_ld_wait_regs(v);
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 pk;
+          pk.x = pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
+          pk.y = pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
+          pk.z = pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
+          pk.w = pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = pk;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[x]);
+      if (hf == 0) lse[((size_t)b * H + h) * S + q] = (m + __log2f(lt_sum)) / LOG2E;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+template <int D, int HV>
+static int run(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int ld, float scale,
+               cudaStream_t s) {
+  CUtensorMap m128, m64;
+  const uint64_t T = (uint64_t)n_seq * S;
+  if (int rc = make_tmap_bf16_2d(&m128, qkv, (uint64_t)3 * H * D, T, ld, 64, 128)) return rc;
+  if (int rc = make_tmap_bf16_2d(&m64, qkv, (uint64_t)3 * H * D, T, ld, 64, 64)) return rc;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fwd_pp_kernel<D, HV>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<D>::TOTAL);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn fwd_pp: cudaFuncSetAttribute");
+    configured = true;
+  }
+  const int items = (S / (2 * BQ)) * H * n_seq;
+  const int grid = items < num_sms() ? items : num_sms();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads_for<HV>());
+  cfg.dynamicSmemBytes = Smem<D>::TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = getenv("ZB_NO_PDL") ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fwd_pp_kernel<D, HV>, m128, m64, (__nv_bfloat16*)out,
+                                     (float*)lse, S, H, n_seq, scale);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "attn fwd_pp launch");
+}
+}  // namespace fa_pp
+
 template <int D>
 static int run_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int ld,
                    float scale, cudaStream_t s) {
@@ -741,8 +1109,19 @@ extern "C" int zb_attn_fwd_tc(const void* qkv, void* out, void* lse, int n_seq, 
   if (S % 128) return set_error(ZB_ERR_INVALID, "attn_fwd_tc: seq_len must be a multiple of 128");
   if (ld % 8 || ((uintptr_t)qkv & 15)) return set_error(ZB_ERR_INVALID, "attn_fwd_tc: bad ld/alignment");
   if (n_seq <= 0) return 0;
+  // Kernel choice (A/B: ZB_ATTN_FWD=pp|ts|1cta): pairs of query tiles per CTA when
+  // S % 256 == 0, else the two-CTA-per-SM kernel (D = 64) / the single-tile kernel.
+  static const char* pick = getenv("ZB_ATTN_FWD");
+  const bool want_pp = !pick || pick[0] == 'p';
+  if (want_pp && S % 256 == 0 && (D == 64 || D == 128))
+    return D == 64 ? (pick && pick[1] == '1'
+                          ? fa::fa_pp::run<64, 1>(qkv, out, lse, n_seq, S, H, ld, scale, s)
+                          : fa::fa_pp::run<64, 2>(qkv, out, lse, n_seq, S, H, ld, scale, s))
+                   : (pick && pick[1] == '2'
+                          ? fa::fa_pp::run<128, 2>(qkv, out, lse, n_seq, S, H, ld, scale, s)
+                          : fa::fa_pp::run<128, 1>(qkv, out, lse, n_seq, S, H, ld, scale, s));
   if (D == 64) {
-    static const bool one = getenv("ZB_ATTN_FWD_1CTA") != nullptr;  // A/B: single-CTA kernel
+    const bool one = pick && pick[0] == '1';
     if (!one) return fa::fa_ts::run(qkv, out, lse, n_seq, S, H, ld, scale, s);
     return fa::run_fwd<64>(qkv, out, lse, n_seq, S, H, ld, scale, s);
   }
