@@ -40,7 +40,7 @@ int zb_device_sync(void);
  * a_mn_major: A stored [K][lda] (M contiguous) instead of [M][lda].
  * b_mn_major: B stored [K][ldb] (N contiguous) instead of [N][ldb].
  * epilogue: 0 C=acc | 1 C=acc+bias | 2 aux=acc+bias, C=gelu(aux) | 3 C=acc+bias+R
- *           4 C=acc*gelu'(aux) | 5 C(fp32)=beta*C+acc | 6 C=acc+R
+ *           4 C=acc*gelu'(aux) | 5 C(fp32)=beta*C+acc | 6 C=acc+R | 7 C=gelu(acc+bias) (no aux)
  * Replaces the modelled per-layer compute of Fwd / Recompute / Bwd tasks
  * (simulate.py:330-367, 469-505; compute_time simulate.py:177-195). */
 int zb_gemm_bf16(const void* A, const void* B, void* C, const void* bias, const void* R,

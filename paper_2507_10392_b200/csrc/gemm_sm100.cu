@@ -42,6 +42,7 @@ enum Epilogue : int {
   EPI_GELU_BWD = 4,    // C = acc * gelu'(AUX[m,n])
   EPI_F32 = 5,         // C(fp32) = beta * C + acc
   EPI_RESID = 6,       // C = acc + R[m,n]            (bias-free residual, Llama)
+  EPI_BIAS_GELU_NA = 7,  // C = gelu(acc + bias), pre-activation not kept (forward pass)
 };
 
 struct GemmArgs {
@@ -119,7 +120,7 @@ ZB_DEVICE void epilogue_chunk(const GemmArgs& args, const uint32_t (&r)[32], int
     }
     return;
   }
-  if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID) {
+  if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID || EPI == EPI_BIAS_GELU_NA) {
     if (full) {
       const uint4* bp = reinterpret_cast<const uint4*>(args.bias + col0);
 #pragma unroll
@@ -167,6 +168,10 @@ ZB_DEVICE void epilogue_chunk(const GemmArgs& args, const uint32_t (&r)[32], int
       _Pragma("unroll") for (int j = 0; j < 32; ++j) if (col0 + j < args.N) Ap[j] = __float2bfloat16(v[j]);
     }
     // GELU of the bf16-rounded pre-activation, so forward and backward agree.
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
+  }
+  if (EPI == EPI_BIAS_GELU_NA) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
   }
@@ -294,7 +299,8 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-    if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID) {
+    if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID ||
+        EPI == EPI_BIAS_GELU_NA) {
       if (col0 + 32 <= args.N) {
         const uint4* bp = reinterpret_cast<const uint4*>(args.bias + col0);
 #pragma unroll
@@ -341,6 +347,10 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
       for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
       st_row_bf16(stg + kEpiSlot, lane, v);
     } else {
+      if (EPI == EPI_BIAS_GELU_NA) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
+      }
       // slots alternate over a running chunk count (across tiles), so the slot
       // written now was last stored two chunks ago
       slot = stg + (ecnt & 1) * kEpiSlot;
@@ -919,6 +929,7 @@ static int dispatch_epi2(int epi, const CUtensorMap& ta, const CUtensorMap& tb, 
     case EPI_GELU_BWD: return launch_gemm2<BN, A_MN, B_MN, EPI_GELU_BWD>(ta, tb, et, args, s);
     case EPI_F32: return launch_gemm2<BN, A_MN, B_MN, EPI_F32>(ta, tb, et, args, s);
     case EPI_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_RESID>(ta, tb, et, args, s);
+    case EPI_BIAS_GELU_NA: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_GELU_NA>(ta, tb, et, args, s);
   }
   return set_error(ZB_ERR_INVALID, "gemm: unknown epilogue %d", epi);
 }
@@ -934,6 +945,7 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
     case EPI_GELU_BWD: return launch_gemm<BN, A_MN, B_MN, EPI_GELU_BWD>(ta, tb, et, args, s);
     case EPI_F32: return launch_gemm<BN, A_MN, B_MN, EPI_F32>(ta, tb, et, args, s);
     case EPI_RESID: return launch_gemm<BN, A_MN, B_MN, EPI_RESID>(ta, tb, et, args, s);
+    case EPI_BIAS_GELU_NA: return launch_gemm<BN, A_MN, B_MN, EPI_BIAS_GELU_NA>(ta, tb, et, args, s);
   }
   return set_error(ZB_ERR_INVALID, "gemm: unknown epilogue %d", epi);
 }

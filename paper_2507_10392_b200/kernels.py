@@ -36,6 +36,7 @@ EPI_BIAS_RESID = 3
 EPI_GELU_BWD = 4
 EPI_F32 = 5
 EPI_RESID = 6
+EPI_BIAS_GELU_NA = 7   # C = gelu(acc + bias), no pre-activation output (forward pass)
 
 
 def _stream():

@@ -30,7 +30,7 @@ import torch
 
 from ..plan.emulated import ModelConfig
 
-EPI_BF16, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_GELU_BWD, EPI_F32, EPI_RESID = range(7)
+EPI_BF16, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_GELU_BWD, EPI_F32, EPI_RESID, EPI_BIAS_GELU_NA = range(8)
 
 
 class FlatLayout:
@@ -211,8 +211,12 @@ class GptOps:
                bias=p["proj_b"], resid=x)
         o.layernorm_fwd(a.x_mid[:n_tok], p["ln2_w"], p["ln2_b"], a.h2[:n_tok], a.mean2[:n_tok],
                         a.rstd2[:n_tok])
-        o.gemm(a.h2[:n_tok], p["fc1_w"], a.g[:n_tok], epilogue=EPI_BIAS_GELU, bias=p["fc1_b"],
-               aux=a.u[:n_tok])
+        if need_out:  # forward pass: backward reads the recompute's pre-activation, not this one
+            o.gemm(a.h2[:n_tok], p["fc1_w"], a.g[:n_tok], epilogue=EPI_BIAS_GELU_NA,
+                   bias=p["fc1_b"])
+        else:
+            o.gemm(a.h2[:n_tok], p["fc1_w"], a.g[:n_tok], epilogue=EPI_BIAS_GELU, bias=p["fc1_b"],
+                   aux=a.u[:n_tok])
         if need_out:
             o.gemm(a.g[:n_tok], p["fc2_w"], out, epilogue=EPI_BIAS_RESID, bias=p["fc2_b"],
                    resid=a.x_mid[:n_tok])

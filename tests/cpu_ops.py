@@ -11,7 +11,7 @@ import math
 
 import torch
 
-EPI_BF16, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_GELU_BWD, EPI_F32, EPI_RESID = range(7)
+EPI_BF16, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_GELU_BWD, EPI_F32, EPI_RESID, EPI_BIAS_GELU_NA = range(8)
 
 
 def _gelu(x):
@@ -32,13 +32,15 @@ def gemm(a, b, out, *, a_t=False, b_t=False, epilogue=EPI_BF16, bias=None, resid
     if epilogue == EPI_F32:
         out.copy_(acc + (beta * out if beta != 0.0 else 0.0))
         return out
-    if epilogue in (EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID):
+    if epilogue in (EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_BIAS_GELU_NA):
         acc = acc + bias.float()
     if epilogue in (EPI_BIAS_RESID, EPI_RESID):
         acc = acc + resid.float()
     if epilogue == EPI_BIAS_GELU:
         aux.copy_(acc)
         acc = _gelu(aux.float())
+    if epilogue == EPI_BIAS_GELU_NA:
+        acc = _gelu(acc.bfloat16().float())
     if epilogue == EPI_GELU_BWD:
         acc = acc * _gelu_grad(aux.float())
     out.copy_(acc)

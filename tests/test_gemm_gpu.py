@@ -101,6 +101,8 @@ def test_gemm_epilogues(cuda, epi_path, M, N, Kd):
     _close(out, acc + bias.float() + r.float())
     K.gemm(a, b, out, epilogue=K.EPI_GELU_BWD, aux=aux)
     _close(out, acc * _gelu_grad(aux.float()))
+    K.gemm(a, b, out, epilogue=K.EPI_BIAS_GELU_NA, bias=bias)
+    _close(out, _gelu((acc + bias.float()).bfloat16().float()))
     torch.cuda.synchronize()
 
 
