@@ -9,8 +9,9 @@ out = torch.empty(n * S, H * D, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(n, H, S, device="cuda")
 dout = torch.randn(n * S, H * D, device="cuda").bfloat16()
 dqkv = torch.empty_like(qkv); delta = torch.empty(n, H, S, device="cuda")
+dq_acc = torch.empty(n * S, H * D, device="cuda")
 for _ in range(2):
     K.attn_fwd(qkv, out, lse, n, S, H, D, 1 / math.sqrt(D))
-    K.attn_bwd(qkv, out, dout, lse, dqkv, None, delta, n, S, H, D, 1 / math.sqrt(D))
+    K.attn_bwd(qkv, out, dout, lse, dqkv, dq_acc, delta, n, S, H, D, 1 / math.sqrt(D))
 torch.cuda.synchronize()
 print("ok")
