@@ -178,6 +178,15 @@ int zb_peer_rs_adamw(void* const* bases, int nranks, int me, uint64_t grad_off, 
                      float weight_decay, float grad_scale, const void* step_dev,
                      zb_stream_t stream);
 
+/* ---- host: planner min-cut kernel (csrc/mincut.cpp) ---------------------------------
+ * Global minimum 2-cut of a dense symmetric float64 [n][n] graph (Stoer-Wagner),
+ * ties toward the smallest lexrank; bit-identical to the reference's only FFI,
+ * hetplan `min_cut_kernel(weights, lexrank) -> (float, sorted list[int])`
+ * (_mincut_c.pyx:16-82, bound at partition.py:26-38).  side_out must hold n entries;
+ * *side_len receives the size of the returned (sorted) shore. */
+int zb_min_cut(const double* weights, int64_t n, const int64_t* lexrank, double* cut_out,
+               int64_t* side_out, int64_t* side_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,6 +9,8 @@ the reference's (ties broken toward the smallest lexicographic vertex id).
 
 from __future__ import annotations
 
+import ctypes
+import os
 from typing import Dict, List, Tuple
 
 import numpy as np
@@ -16,7 +18,46 @@ import numpy as np
 from .graph import ClusterGraph, Partition, PartitionError, make_partition
 
 
+def _native_kernel():
+    """``zb_min_cut`` from the C-ABI library (csrc/mincut.cpp), or None when the library
+    is not built — the reference likewise prefers its compiled kernel and falls back to
+    the numpy twin (partition.py:26-38)."""
+    try:
+        from .._lib import lib
+        return lib().zb_min_cut
+    except Exception:  # noqa: BLE001 - library absent: use the restatement below
+        return None
+
+
+_NATIVE = _native_kernel() if not os.environ.get("ZB_PURE_PYTHON_MINCUT") else None
+MINCUT_BACKEND = "native" if _NATIVE is not None else "python"
+
+
 def min_cut_kernel(weights: np.ndarray, lexrank: np.ndarray) -> Tuple[float, List[int]]:
+    """Global minimum 2-cut of a dense symmetric graph: (weight, sorted side)."""
+    if _NATIVE is not None:
+        return min_cut_native(weights, lexrank)
+    return min_cut_python(weights, lexrank)
+
+
+def min_cut_native(weights: np.ndarray, lexrank: np.ndarray) -> Tuple[float, List[int]]:
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    n = w.shape[0]
+    if n < 2:
+        raise ValueError("min cut needs >= 2 vertices")
+    rank = np.ascontiguousarray(lexrank, dtype=np.int64)
+    cut = ctypes.c_double()
+    side = np.zeros(n, dtype=np.int64)
+    ln = ctypes.c_int64()
+    rc = _NATIVE(w.ctypes.data, n, rank.ctypes.data, ctypes.byref(cut), side.ctypes.data,
+                 ctypes.byref(ln))
+    if rc:
+        from .._lib import lib
+        raise ValueError(lib().zb_last_error().decode())
+    return float(cut.value), [int(x) for x in side[:ln.value]]
+
+
+def min_cut_python(weights: np.ndarray, lexrank: np.ndarray) -> Tuple[float, List[int]]:
     """Global minimum 2-cut of a dense symmetric graph: (weight, sorted side)."""
     w = np.array(weights, dtype=np.float64, copy=True)
     n = w.shape[0]

@@ -159,3 +159,23 @@ def test_split_flat_edges():
     assert s.counts == [960, 40]
     with pytest.raises(ValueError):
         P.split_flat(64, [1, 1])                          # fewer 64-element units than ranks
+
+
+def test_native_min_cut_matches_numpy_twin():
+    """zb_min_cut (csrc/mincut.cpp, the native twin of the reference's compiled
+    min_cut_kernel) is bit-identical to the numpy restatement, ties included."""
+    import numpy as np
+    from paper_2507_10392_b200.plan import mincut as MC
+    if MC._NATIVE is None:
+        pytest.skip("library not built")
+    rng = np.random.default_rng(7)
+    for trial in range(200):
+        n = int(rng.integers(2, 14))
+        if trial % 3 == 0:   # integer weights: many ties
+            w = rng.integers(0, 4, size=(n, n)).astype(np.float64)
+        else:
+            w = rng.random((n, n)) * rng.choice([1.0, 1e-3, 1e6])
+        w = np.triu(w, 1)
+        w = w + w.T
+        rank = rng.permutation(n).astype(np.int64)
+        assert MC.min_cut_native(w, rank) == MC.min_cut_python(w, rank), trial
