@@ -527,6 +527,305 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
+// Persistent fused backward (D = 64): one CTA per SM walks (key tile, head, sequence)
+// items heavy-first in boustrophedon order (the one-CTA-per-item grid had 5+ waves of
+// CTAs with 1..S/128 query tiles each).  Per item the same pipeline as
+// dkdv_kernel<64, true>; barrier parities run on global tile / item counters, the
+// Q/dO ring continues across items, and `acc_empty` hands the dK/dV accumulators
+// back to the MMA warp once the epilogue read them.
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    dkdvq_persistent_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                            const __grid_constant__ CUtensorMap tm_do,
+                            const __grid_constant__ CUtensorMap tm_dq,
+                            const float* __restrict__ lse, const float* __restrict__ delta,
+                            __nv_bfloat16* __restrict__ dqkv, int S, int H, int n_seq, int ld,
+                            float scale) {
+  using L = DkvSmem<D, true>;
+  constexpr int NST = L::NST;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t* kv_full = bar;
+  uint64_t* qo_full = bar + 1;          // [NST]
+  uint64_t* qo_empty = bar + 1 + NST;   // [NST]
+  uint64_t* s_full = bar + 1 + 2 * NST;
+  uint64_t* s_empty = s_full + 1;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* p_empty = s_full + 3;
+  uint64_t* done = s_full + 4;        // item's last MMAs complete
+  uint64_t* dqp_full = s_full + 5;    // [2]
+  uint64_t* dqp_empty = s_full + 7;   // [2]
+  uint64_t* kv_empty = s_full + 9;    // item's K / V no longer read
+  uint64_t* acc_empty = s_full + 10;  // epilogue read dK / dV (count kMath)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 11);
+  float* vec = reinterpret_cast<float*>(sm + L::OFF_VEC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqt = S / T;
+  const int HD = H * D;
+  const int per_k = H * n_seq;
+  const int items = nqt * per_k;
+  const int P = gridDim.x;
+  auto item_of = [&](int k) { return k * P + ((k & 1) ? (P - 1 - (int)blockIdx.x) : (int)blockIdx.x); };
+  auto decode = [&](int t, int& kt, int& h, int& b) {
+    kt = t / per_k;  // key tile 0 sees all nqt query tiles: heaviest first
+    const int rem = t % per_k;
+    h = rem % H;
+    b = rem / H;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&qo_full[i], 1);
+      mbar_init(&qo_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, kMath);
+    mbar_init(p_full, kMath);
+    mbar_init(p_empty, 1);
+    mbar_init(done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&dqp_full[i], 1);
+      mbar_init(&dqp_empty[i], kMath);
+    }
+    mbar_init(kv_empty, 1);
+    mbar_init(acc_empty, kMath);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
+  const uint32_t t_dqp = tmem + 256 + 2 * D;
+  griddep_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0, lt = 0;
+      for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
+        int kt, h, b;
+        decode(t, kt, h, b);
+        const int row0 = b * S, ntile = nqt - kt;
+        mbar_wait(kv_empty, (lt & 1) ^ 1);
+        mbar_arrive_expect_tx(kv_full, 2 * L::TILE);
+#pragma unroll
+        for (int kc = 0; kc < D / 64; ++kc) {
+          tma_load_2d(sm + L::OFF_K + kc * T * 128, &tm_qkv, kv_full, HD + h * D + kc * 64,
+                      row0 + kt * T);
+          tma_load_2d(sm + L::OFF_V + kc * T * 128, &tm_qkv, kv_full, 2 * HD + h * D + kc * 64,
+                      row0 + kt * T);
+        }
+        for (int i = 0; i < ntile; ++i, ++g) {
+          const int st = g % NST, qt = kt + i;
+          mbar_wait(&qo_empty[st], ((g / NST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&qo_full[st], 2 * L::TILE);
+#pragma unroll
+          for (int kc = 0; kc < D / 64; ++kc) {
+            tma_load_2d(sm + L::OFF_Q + st * L::TILE + kc * T * 128, &tm_qkv, &qo_full[st],
+                        h * D + kc * 64, row0 + qt * T);
+            tma_load_2d(sm + L::OFF_DO + st * L::TILE + kc * T * 128, &tm_do, &qo_full[st],
+                        h * D + kc * 64, row0 + qt * T);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(T, T, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(T, D, 0, 1);
+      constexpr uint32_t idesc_q = umma_idesc_bf16(T, D, 1, 1);
+      const uint32_t k_base = smem_u32(sm + L::OFF_K), v_base = smem_u32(sm + L::OFF_V);
+      const uint32_t pt_base = smem_u32(sm + L::OFF_PT), dst_base = smem_u32(sm + L::OFF_DST);
+      int g = 0, lt = 0;
+      auto issue_s = [&](int gi) {
+        const int st = gi % NST;
+        mbar_wait(&qo_full[st], (gi / NST) & 1);
+        mbar_wait(s_empty, (gi & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sm + L::OFF_Q + st * L::TILE);
+        const uint32_t do_base = smem_u32(sm + L::OFF_DO + st * L::TILE);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          mma_bf16_ss(t_st, desc_k(k_base, kk), desc_k(q_base, kk), idesc_s, kk > 0);
+          mma_bf16_ss(t_dpt, desc_k(v_base, kk), desc_k(do_base, kk), idesc_s, kk > 0);
+        }
+        mma_commit(s_full);
+      };
+      for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
+        int kt, h, b;
+        decode(t, kt, h, b);
+        const int ntile = nqt - kt;
+        mbar_wait(kv_full, lt & 1);
+        tc_fence_after();
+        issue_s(g);
+        for (int i = 0; i < ntile; ++i) {
+          const int gi = g + i, st = gi % NST;
+          if (i + 1 < ntile) issue_s(gi + 1);
+          mbar_wait(p_full, gi & 1);
+          if (i == 0) mbar_wait(acc_empty, (lt & 1) ^ 1);  // previous item's dK / dV read
+          tc_fence_after();
+          const uint32_t q_base = smem_u32(sm + L::OFF_Q + st * L::TILE);
+          const uint32_t do_base = smem_u32(sm + L::OFF_DO + st * L::TILE);
+#pragma unroll
+          for (int kk = 0; kk < T / 16; ++kk) {
+            mma_bf16_ss(t_dv, desc_k(pt_base, kk), desc_mn(do_base, kk), idesc_o, (i > 0 || kk > 0));
+            mma_bf16_ss(t_dk, desc_k(dst_base, kk), desc_mn(q_base, kk), idesc_o, (i > 0 || kk > 0));
+          }
+          const int bb = gi & 1;
+          mbar_wait(&dqp_empty[bb], ((gi >> 1) & 1) ^ 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < T / 16; ++kk)
+            mma_bf16_ss(t_dqp + bb * D, desc_mn(dst_base, kk), desc_mn(k_base, kk), idesc_q,
+                        kk > 0 ? 1u : 0u);
+          mma_commit(&dqp_full[bb]);
+          mma_commit(&qo_empty[st]);
+          mma_commit(p_empty);
+        }
+        mma_commit(kv_empty);
+        mma_commit(done);
+        g += ntile;
+      }
+    }
+  } else if (warp >= 4) {
+    const int wq = (warp - 4) & 3, half = (warp - 4) >> 2, r = wq * 32 + lane;
+    const uint32_t lo = (uint32_t)(wq * 32) << 16;
+    const float sl2 = scale * LOG2E;
+    int g = 0, lt = 0;
+    for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
+      int kt, h, b;
+      decode(t, kt, h, b);
+      const int row0 = b * S, ntile = nqt - kt;
+      auto drain_dq = [&](int j) {  // j: tile index within the item
+        uint8_t* stg = sm + L::OFF_STG + (warp - 4) * 4096;
+        const int gj = g + j, bb = gj & 1;
+        mbar_wait(&dqp_full[bb], (gj >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_dqp + bb * D + lo + half * 32, v);
+        tmem_ld_wait_regs(v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&dqp_empty[bb]);
+          bulk_wait_read<0>();
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+              make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
+                          __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(&tm_dq, stg, h * D + half * 32, row0 + (kt + j) * T + wq * 32);
+          bulk_commit();
+        }
+      };
+      for (int i = 0; i < ntile; ++i) {
+        const int gi = g + i, qt = kt + i;
+        float* vl = vec + (gi & 1) * 2 * T;
+        float* vd = vl + T;
+        const size_t vrow = ((size_t)b * H + h) * S + qt * T + r;
+        if (half == 0) {
+          vl[r] = lse[vrow] * LOG2E;
+          vd[r] = delta[vrow];
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // the eight math warps
+        mbar_wait(s_full, gi & 1);
+        mbar_wait(p_empty, (gi & 1) ^ 1);
+        tc_fence_after();
+        uint8_t* pt = sm + L::OFF_PT;
+        uint8_t* dst = sm + L::OFF_DST;
+        auto chunk = [&](int c, auto diag_c) {
+          constexpr bool DG = decltype(diag_c)::value;
+          uint32_t sv[32], dv[32];
+          tmem_ld_32x32b_x32(t_st + lo + c * 32, sv);
+          tmem_ld_32x32b_x32(t_dpt + lo + c * 32, dv);
+          tmem_ld_wait_regs(sv);
+          reg_tie(dv);
+          float p[32], ds[32];
+#pragma unroll
+          for (int t4 = 0; t4 < 32; t4 += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(vl + c * 32 + t4);
+            const float4 d4 = *reinterpret_cast<const float4*>(vd + c * 32 + t4);
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int tt = t4 + u;
+              float x = exp2_fast(fmaf(__uint_as_float(sv[tt]), sl2, -lv[u]));
+              if (DG && c * 32 + tt < r) x = 0.f;
+              p[tt] = x;
+              ds[tt] = x * (__uint_as_float(dv[tt]) - dl[u]);
+            }
+          }
+          st_row32(pt, r, c * 32, p);
+          st_row32(dst, r, c * 32, ds);
+        };
+        constexpr int CH = T / 64;
+        if (qt == kt) {
+#pragma unroll 1
+          for (int c = half * CH; c < (half + 1) * CH; ++c) chunk(c, std::true_type{});
+        } else {
+#pragma unroll 1
+          for (int c = half * CH; c < (half + 1) * CH; ++c) chunk(c, std::false_type{});
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+        if (i > 0) drain_dq(i - 1);
+      }
+      drain_dq(ntile - 1);
+      mbar_wait(done, lt & 1);
+      tc_fence_after();
+      const int kr = kt * T + r;
+      __nv_bfloat16* dk_row = dqkv + ((size_t)row0 + kr) * ld + HD + h * D;
+      __nv_bfloat16* dv_row = dk_row + HD;
+#pragma unroll
+      for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
+        uint32_t v[32], w[32];
+        tmem_ld_32x32b_x32(t_dk + lo + c * 32, v);
+        tmem_ld_32x32b_x32(t_dv + lo + c * 32, w);
+        tmem_ld_wait_regs(v);
+        reg_tie(w);
+#pragma unroll
+        for (int tt = 0; tt < 32; tt += 8) {
+          uint4 a, bq;
+          a.x = pack_bf16(__uint_as_float(v[tt]) * scale, __uint_as_float(v[tt + 1]) * scale);
+          a.y = pack_bf16(__uint_as_float(v[tt + 2]) * scale, __uint_as_float(v[tt + 3]) * scale);
+          a.z = pack_bf16(__uint_as_float(v[tt + 4]) * scale, __uint_as_float(v[tt + 5]) * scale);
+          a.w = pack_bf16(__uint_as_float(v[tt + 6]) * scale, __uint_as_float(v[tt + 7]) * scale);
+          bq.x = pack_bf16(__uint_as_float(w[tt]), __uint_as_float(w[tt + 1]));
+          bq.y = pack_bf16(__uint_as_float(w[tt + 2]), __uint_as_float(w[tt + 3]));
+          bq.z = pack_bf16(__uint_as_float(w[tt + 4]), __uint_as_float(w[tt + 5]));
+          bq.w = pack_bf16(__uint_as_float(w[tt + 6]), __uint_as_float(w[tt + 7]));
+          *reinterpret_cast<uint4*>(dk_row + c * 32 + tt) = a;
+          *reinterpret_cast<uint4*>(dv_row + c * 32 + tt) = bq;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+      g += ntile;
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
 // dq (bf16, pitch ld, scaled) = dq_accum (fp32, pitch H*D)
 __global__ void dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dqkv,
                                   int rows, int HD, int ld, float scale) {
@@ -601,8 +900,25 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     attr[0].val.programmaticStreamSerializationAllowed = getenv("ZB_NO_PDL") ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, dkdv_kernel<D, true>, mq, mo, mdq, (const float*)lse,
-                                       (const float*)delta, (__nv_bfloat16*)dqkv, S, H, ld, scale);
+    static const bool grid_items = getenv("ZB_ATTN_BWD_GRID") != nullptr;  // A/B: one CTA per item
+    cudaError_t e;
+    if (grid_items) {
+      e = cudaLaunchKernelEx(&cfg, dkdv_kernel<D, true>, mq, mo, mdq, (const float*)lse,
+                             (const float*)delta, (__nv_bfloat16*)dqkv, S, H, ld, scale);
+    } else {
+      static bool cfg_p = false;
+      if (!cfg_p) {
+        e = cudaFuncSetAttribute(dkdvq_persistent_kernel<D>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 DkvSmem<D, true>::TOTAL);
+        if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: cudaFuncSetAttribute");
+        cfg_p = true;
+      }
+      const int items = (S / T) * H * n_seq;
+      cfg.gridDim = dim3(items < num_sms() ? items : num_sms());
+      e = cudaLaunchKernelEx(&cfg, dkdvq_persistent_kernel<D>, mq, mo, mdq, (const float*)lse,
+                             (const float*)delta, (__nv_bfloat16*)dqkv, S, H, n_seq, ld, scale);
+    }
     if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc fused launch");
     const int64_t n8 = (int64_t)Tn * (HD / 8);
     int cg = (int)((n8 + 255) / 256);
