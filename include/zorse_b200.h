@@ -79,6 +79,13 @@ int zb_layernorm_fwd(const void* x, const void* w, const void* b, void* y, void*
 int zb_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mean,
                      const void* rstd, void* dx, void* dw, void* db, const void* dres, int rows,
                      int d, zb_stream_t stream);
+/* Same, and (db_res, db_out non-NULL, dres required) the column sums of dres and of the
+ * dx output accumulated into db_res / db_out: the bias gradients of the linear layers
+ * whose output gradients they are (GPT block: fc2 and the attention projection),
+ * folded into the dw / db column pass instead of two zb_bias_grad launches. */
+int zb_layernorm_bwd_ex(const void* dy, const void* x, const void* w, const void* mean,
+                        const void* rstd, void* dx, void* dw, void* db, const void* dres,
+                        void* db_res, void* db_out, int rows, int d, zb_stream_t stream);
 /* out[t] = wte[tok[t]] + wpe[t % seq]  (tok: int32; wpe may be NULL). */
 int zb_embedding_fwd(const void* tok, const void* wte, const void* wpe, void* out, int rows, int d,
                      int seq, zb_stream_t stream);

@@ -271,77 +271,85 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(
 }
 
 // dw[c] += sum_r dy[r,c] * (x[r,c] - mean[r]) * rstd[r];  db[c] += sum_r dy[r,c]
+// EXTRA: also db_res[c] += sum_r dres[r,c] and db_out[c] += sum_r dx[r,c] — the bias
+// gradients of the linear layers whose output gradients are dres / dx (GPT block:
+// fc2 and attention projection), folded into this column pass.
+template <bool EXTRA>
 __global__ void __launch_bounds__(256) layernorm_bwd_wb_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in, float* __restrict__ dw,
-    float* __restrict__ db, int rows, int d, int rows_per_block) {
+    float* __restrict__ db, const __nv_bfloat16* __restrict__ dres,
+    const __nv_bfloat16* __restrict__ dxo, float* __restrict__ db_res, float* __restrict__ db_out,
+    int rows, int d, int rows_per_block) {
+  constexpr int NV = EXTRA ? 32 : 16;  // accumulated values per column vector
   const int cv = blockIdx.x * 32 + (threadIdx.x & 31);  // column vector (8 cols)
   const int rl = threadIdx.x >> 5;                       // 0..7
   const int r0 = blockIdx.y * rows_per_block;
   const int r1 = min(rows, r0 + rows_per_block);
-  float aw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.f;
   const bool ok = cv * 8 < d;
+  auto add_row = [&](const uint4& qd, const uint4& qx, float mu, float rs, const uint4& qr,
+                     const uint4& qo) {
+    const uint32_t *di = &qd.x, *xi = &qx.x, *ri = &qr.x, *oi = &qo.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]);
+      acc[2 * k] += dv.x * ((xv.x - mu) * rs);
+      acc[2 * k + 1] += dv.y * ((xv.y - mu) * rs);
+      acc[8 + 2 * k] += dv.x;
+      acc[8 + 2 * k + 1] += dv.y;
+      if (EXTRA) {
+        const float2 rv = unpack_bf16(ri[k]), ov = unpack_bf16(oi[k]);
+        acc[16 + 2 * k] += rv.x;
+        acc[16 + 2 * k + 1] += rv.y;
+        acc[24 + 2 * k] += ov.x;
+        acc[24 + 2 * k + 1] += ov.y;
+      }
+    }
+  };
   if (ok) {
     int r = r0 + rl;
+    const uint4 z = make_uint4(0, 0, 0, 0);
     for (; r + 24 < r1; r += 32) {
-      uint4 qd[4], qx[4];
+      uint4 qd[4], qx[4], qr[4], qo[4];
       float mu[4], rs[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const size_t o = (size_t)(r + 8 * u) * d + cv * 8;
         qd[u] = *reinterpret_cast<const uint4*>(dy + o);
         qx[u] = *reinterpret_cast<const uint4*>(x + o);
+        qr[u] = EXTRA ? *reinterpret_cast<const uint4*>(dres + o) : z;
+        qo[u] = EXTRA ? *reinterpret_cast<const uint4*>(dxo + o) : z;
         mu[u] = mean_in[r + 8 * u];
         rs[u] = rstd_in[r + 8 * u];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t *di = &qd[u].x, *xi = &qx[u].x;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]);
-          aw[2 * k] += dv.x * ((xv.x - mu[u]) * rs[u]);
-          aw[2 * k + 1] += dv.y * ((xv.y - mu[u]) * rs[u]);
-          ab[2 * k] += dv.x;
-          ab[2 * k + 1] += dv.y;
-        }
-      }
+      for (int u = 0; u < 4; ++u) add_row(qd[u], qx[u], mu[u], rs[u], qr[u], qo[u]);
     }
     for (; r < r1; r += 8) {
       const size_t o = (size_t)r * d + cv * 8;
-      const uint4 q1 = *reinterpret_cast<const uint4*>(dy + o);
-      const uint4 q2 = *reinterpret_cast<const uint4*>(x + o);
-      const float mu = mean_in[r], rs = rstd_in[r];
-      const uint32_t *di = &q1.x, *xi = &q2.x;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]);
-        aw[2 * k] += dv.x * ((xv.x - mu) * rs);
-        aw[2 * k + 1] += dv.y * ((xv.y - mu) * rs);
-        ab[2 * k] += dv.x;
-        ab[2 * k + 1] += dv.y;
-      }
+      add_row(*reinterpret_cast<const uint4*>(dy + o), *reinterpret_cast<const uint4*>(x + o),
+              mean_in[r], rstd_in[r],
+              EXTRA ? *reinterpret_cast<const uint4*>(dres + o) : z,
+              EXTRA ? *reinterpret_cast<const uint4*>(dxo + o) : z);
     }
   }
-  __shared__ float red[8][32][17];
+  __shared__ float red[8][32][NV + 1];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    red[rl][threadIdx.x & 31][k] = aw[k];
-    red[rl][threadIdx.x & 31][8 + k] = ab[k];
-  }
+  for (int k = 0; k < NV; ++k) red[rl][threadIdx.x & 31][k] = acc[k];
   __syncthreads();
-  // 256 threads reduce the 32 x 16 values over the 8 row lanes
-  for (int idx = threadIdx.x; idx < 32 * 16; idx += blockDim.x) {
-    const int c = idx >> 4, k = idx & 15;
+  // 256 threads reduce the 32 x NV values over the 8 row lanes
+  for (int idx = threadIdx.x; idx < 32 * NV; idx += blockDim.x) {
+    const int c = idx / NV, k = idx % NV;
     const int col_v = blockIdx.x * 32 + c;
     if (col_v * 8 >= d) continue;
     float t = 0.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) t += red[j][c][k];
-    if (k < 8)
-      atomicAdd(&dw[col_v * 8 + k], t);
-    else
-      atomicAdd(&db[col_v * 8 + (k - 8)], t);
+    float* dst = k < 8 ? dw : (k < 16 ? db : (k < 24 ? db_res : db_out));
+    atomicAdd(&dst[col_v * 8 + (k & 7)], t);
   }
 }
 
@@ -587,9 +595,9 @@ extern "C" int zb_layernorm_fwd(const void* x, const void* w, const void* b, voi
   return launched("layernorm_fwd");
 }
 
-extern "C" int zb_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mean,
-                                const void* rstd, void* dx, void* dw, void* db, const void* dres,
-                                int rows, int d, cudaStream_t s) {
+static int layernorm_bwd_impl(const void* dy, const void* x, const void* w, const void* mean,
+                              const void* rstd, void* dx, void* dw, void* db, const void* dres,
+                              void* db_res, void* db_out, int rows, int d, cudaStream_t s) {
   if (d % 8) return set_error(ZB_ERR_INVALID, "layernorm: d must be a multiple of 8");
   if (d > 5120) return set_error(ZB_ERR_UNSUPPORTED, "layernorm_bwd: d > 5120");
   if (rows <= 0) return 0;
@@ -616,9 +624,19 @@ extern "C" int zb_layernorm_bwd(const void* dy, const void* x, const void* w, co
     int rpb = (rows + rblocks - 1) / rblocks;
     rpb = ((rpb + 7) / 8) * 8;
     rblocks = (rows + rpb - 1) / rpb;
-    layernorm_bwd_wb_kernel<<<dim3(cblocks, rblocks), 256, 0, s>>>(
-        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)mean, (const float*)rstd,
-        (float*)dw, (float*)db, rows, d, rpb);
+    if (db_res || db_out) {
+      if (!db_res || !db_out || !dres)
+        return set_error(ZB_ERR_INVALID, "layernorm_bwd: db_res / db_out need dres and each other");
+      layernorm_bwd_wb_kernel<true><<<dim3(cblocks, rblocks), 256, 0, s>>>(
+          (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)mean,
+          (const float*)rstd, (float*)dw, (float*)db, (const __nv_bfloat16*)dres,
+          (const __nv_bfloat16*)dx, (float*)db_res, (float*)db_out, rows, d, rpb);
+    } else {
+      layernorm_bwd_wb_kernel<false><<<dim3(cblocks, rblocks), 256, 0, s>>>(
+          (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)mean,
+          (const float*)rstd, (float*)dw, (float*)db, nullptr, nullptr, nullptr, nullptr, rows,
+          d, rpb);
+    }
     return launched("layernorm_bwd");
   }
   // One CTA per SM (measured: more CTAs lose to the per-CTA reduction), each warp
@@ -642,6 +660,22 @@ extern "C" int zb_layernorm_bwd(const void* dy, const void* x, const void* w, co
   else if (vpl <= 10) go(layernorm_bwd_kernel<10>);
   else if (vpl <= 20) go(layernorm_bwd_kernel<20>);
   return launched("layernorm_bwd");
+}
+
+extern "C" int zb_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mean,
+                                const void* rstd, void* dx, void* dw, void* db, const void* dres,
+                                int rows, int d, cudaStream_t s) {
+  return layernorm_bwd_impl(dy, x, w, mean, rstd, dx, dw, db, dres, nullptr, nullptr, rows, d, s);
+}
+
+extern "C" int zb_layernorm_bwd_ex(const void* dy, const void* x, const void* w, const void* mean,
+                                   const void* rstd, void* dx, void* dw, void* db,
+                                   const void* dres, void* db_res, void* db_out, int rows, int d,
+                                   cudaStream_t s) {
+  static const bool fused = getenv("ZB_LN_BWD_FUSED") != nullptr;
+  if (fused && (db_res || db_out))
+    return set_error(ZB_ERR_UNSUPPORTED, "layernorm_bwd_ex: not with ZB_LN_BWD_FUSED");
+  return layernorm_bwd_impl(dy, x, w, mean, rstd, dx, dw, db, dres, db_res, db_out, rows, d, s);
 }
 
 extern "C" int zb_embedding_fwd(const void* tok, const void* wte, const void* wpe, void* out,

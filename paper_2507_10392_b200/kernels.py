@@ -12,7 +12,8 @@ import torch
 from ._lib import call as _call
 
 # Device kernel launches issued per C-ABI entry point (for the bench's gpu_launches).
-_LAUNCHES_PER_CALL = {"zb_attn_bwd": 3, "zb_attn_bwd_tc": 3, "zb_layernorm_bwd": 2}
+_LAUNCHES_PER_CALL = {"zb_attn_bwd": 3, "zb_attn_bwd_tc": 3, "zb_layernorm_bwd": 2,
+                      "zb_layernorm_bwd_ex": 2}
 _launches = [0]
 
 
@@ -92,10 +93,16 @@ def layernorm_fwd(x, w, b, y, mean, rstd, eps=1e-5):
          None, rows, d, float(eps), _stream())
 
 
-def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None):
-    """dx (+)= LN'(dy); dw, db (fp32) += parameter grads.  dx_accum: residual grad to add."""
-    _need_cuda(dy, x, w, mean, rstd, dx, dw, db, dx_accum)
+def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None, db_accum=None, db_out=None):
+    """dx (+)= LN'(dy); dw, db (fp32) += parameter grads.  dx_accum: residual grad to add.
+    db_accum / db_out (fp32, optional, together): += column sums of dx_accum / of dx."""
+    _need_cuda(dy, x, w, mean, rstd, dx, dw, db, dx_accum, db_accum, db_out)
     rows, d = x.shape
+    if db_accum is not None or db_out is not None:
+        call("zb_layernorm_bwd_ex", _ptr(dy), _ptr(x), _ptr(w), _ptr(mean), _ptr(rstd), _ptr(dx),
+             _ptr(dw), _ptr(db), _ptr(dx_accum), _ptr(db_accum), _ptr(db_out), rows, d,
+             _stream())
+        return
     call("zb_layernorm_bwd", _ptr(dy), _ptr(x), _ptr(w), _ptr(mean), _ptr(rstd), _ptr(dx),
          _ptr(dw), _ptr(db), _ptr(dx_accum), rows, d, _stream())
 

@@ -230,16 +230,16 @@ class GptOps:
         n = n_tok
         # MLP: out = x_mid + g W2^T + b2
         o.gemm(dy, a.g[:n], gr["fc2_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
-        o.bias_grad(dy, gr["fc2_b"])
+        # fc2 / proj bias grads: column sums of dy / dx_mid, folded into LN2's backward
         o.gemm(dy, p["fc2_w"], a.u[:n], b_t=True, epilogue=EPI_GELU_BWD, aux=a.u[:n])  # du (in place)
         o.gemm(a.u[:n], a.h2[:n], gr["fc1_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         o.bias_grad(a.u[:n], gr["fc1_b"])
         o.gemm(a.u[:n], p["fc1_w"], s.dh[:n], b_t=True)
         o.layernorm_bwd(s.dh[:n], a.x_mid[:n], p["ln2_w"], a.mean2[:n], a.rstd2[:n], s.dx_mid[:n],
-                        gr["ln2_w"], gr["ln2_b"], dx_accum=dy)
+                        gr["ln2_w"], gr["ln2_b"], dx_accum=dy, db_accum=gr["fc2_b"],
+                        db_out=gr["proj_b"])
         # attention: x_mid = x + attn W_o^T + b_o
         o.gemm(s.dx_mid[:n], a.attn[:n], gr["proj_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
-        o.bias_grad(s.dx_mid[:n], gr["proj_b"])
         o.gemm(s.dx_mid[:n], p["proj_w"], s.da[:n], b_t=True)
         o.attn_bwd(a.qkv[:n], a.attn[:n], s.da[:n], a.lse[:n_seq], s.dqkv[:n],
                    s.dq_accum[:n] if s.dq_accum is not None else None,

@@ -21,7 +21,8 @@ from paper_2507_10392_b200 import kernels
 from paper_2507_10392_b200.runtime.data import synthetic_batch
 from paper_2507_10392_b200.runtime.trainer import ZorseTrainer
 
-EPI = {0: "bf16", 1: "bias", 2: "bias+gelu", 3: "bias+resid", 4: "gelu'", 5: "f32+=", 6: "resid"}
+EPI = {0: "bf16", 1: "bias", 2: "bias+gelu", 3: "bias+resid", 4: "gelu'", 5: "f32+=", 6: "resid",
+       7: "bias+gelu (no aux)"}
 
 
 class Timed:

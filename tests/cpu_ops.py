@@ -57,7 +57,7 @@ def layernorm_fwd(x, w, b, y, mean, rstd, eps=1e-5):
     rstd.copy_(rs)
 
 
-def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None):
+def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None, db_accum=None, db_out=None):
     xh = (x.float() - mean[:, None]) * rstd[:, None]
     g = dy.float() * w.float()
     mg = g.mean(-1, keepdim=True)
@@ -68,6 +68,9 @@ def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None):
     dw += (dy.float() * xh).sum(0)
     db += dy.float().sum(0)
     dx.copy_(out)
+    if db_accum is not None:
+        db_accum += dx_accum.float().sum(0)
+        db_out += dx.float().sum(0)
 
 
 def embedding_fwd(tokens, wte, wpe, out, seq_len):

@@ -41,6 +41,15 @@ def test_layernorm_fwd_bwd(cuda, rows, d):
     assert rel(dx, xf.grad + dres.float()) < 1e-2
     assert rel(dw, wf.grad) < 1e-3
     assert rel(db, bf.grad) < 1e-3
+    # folded bias gradients: column sums of the residual grad and of the output
+    dw.zero_(); db.zero_()
+    db_res = torch.full((d,), 0.5, device="cuda")
+    db_out = torch.full((d,), -0.25, device="cuda")
+    K.layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=dres, db_accum=db_res, db_out=db_out)
+    torch.cuda.synchronize()
+    assert rel(dw, wf.grad) < 1e-3 and rel(db, bf.grad) < 1e-3
+    assert rel(db_res, 0.5 + dres.float().sum(0)) < 1e-3
+    assert rel(db_out, -0.25 + dx.float().sum(0)) < 1e-3
 
 
 def test_embedding(cuda):
