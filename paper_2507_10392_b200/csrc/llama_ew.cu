@@ -54,9 +54,6 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
                                    const float* __restrict__ rstd_in, __nv_bfloat16* dx,
                                    float* __restrict__ dw, const __nv_bfloat16* dres, int rows,
                                    int d) {
-  extern __shared__ float sdw[];
-  for (int i = threadIdx.x; i < d; i += blockDim.x) sdw[i] = 0.f;
-  __syncthreads();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nv = d >> 3;
@@ -74,8 +71,6 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
         float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
         const float h0 = xv.x * rstd, h1 = xv.y * rstd;
         sgx += dv.x * wv.x * h0 + dv.y * wv.y * h1;
-        atomicAdd(&sdw[v * 8 + 2 * k], dv.x * h0);
-        atomicAdd(&sdw[v * 8 + 2 * k + 1], dv.y * h1);
       }
     }
     const float mgx = warp_sum(sgx) / d;
@@ -98,8 +93,70 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
       dxr[v] = o;
     }
   }
+}
+
+// dw[c] += sum_r dy[r,c] * x[r,c] * rstd[r]: column reduction (32 column vectors x 8
+// row lanes per CTA, 4 loads in flight; the per-row kernel above no longer does
+// shared-memory atomics per element).
+__global__ void __launch_bounds__(256) rmsnorm_bwd_w_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const float* __restrict__ rstd_in, float* __restrict__ dw, int rows, int d,
+    int rows_per_block) {
+  const int cv = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int rl = threadIdx.x >> 5;
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (cv * 8 < d) {
+    int r = r0 + rl;
+    for (; r + 24 < r1; r += 32) {
+      uint4 qd[4], qx[4];
+      float rs[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t o = (size_t)(r + 8 * u) * d + cv * 8;
+        qd[u] = *reinterpret_cast<const uint4*>(dy + o);
+        qx[u] = *reinterpret_cast<const uint4*>(x + o);
+        rs[u] = rstd_in[r + 8 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t *di = &qd[u].x, *xi = &qx[u].x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]);
+          acc[2 * k] += dv.x * (xv.x * rs[u]);
+          acc[2 * k + 1] += dv.y * (xv.y * rs[u]);
+        }
+      }
+    }
+    for (; r < r1; r += 8) {
+      const size_t o = (size_t)r * d + cv * 8;
+      const uint4 qd = *reinterpret_cast<const uint4*>(dy + o);
+      const uint4 qx = *reinterpret_cast<const uint4*>(x + o);
+      const float rs = rstd_in[r];
+      const uint32_t *di = &qd.x, *xi = &qx.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]);
+        acc[2 * k] += dv.x * (xv.x * rs);
+        acc[2 * k + 1] += dv.y * (xv.y * rs);
+      }
+    }
+  }
+  __shared__ float red[8][32][9];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[rl][threadIdx.x & 31][k] = acc[k];
   __syncthreads();
-  for (int i = threadIdx.x; i < d; i += blockDim.x) atomicAdd(&dw[i], sdw[i]);
+  if (rl == 0 && cv * 8 < d) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t += red[j][threadIdx.x & 31][k];
+      atomicAdd(&dw[cv * 8 + k], t);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ RoPE
@@ -215,15 +272,21 @@ extern "C" int zb_rmsnorm_bwd(const void* dy, const void* x, const void* w, cons
                               cudaStream_t s) {
   if (d % 8) return set_error(ZB_ERR_INVALID, "rmsnorm: d must be a multiple of 8");
   if (rows <= 0) return 0;
-  int blocks = (rows + 63) / 64;
-  if (blocks > 2 * num_sms()) blocks = 2 * num_sms();
-  const size_t smem = (size_t)d * sizeof(float);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  rmsnorm_bwd_kernel<<<blocks, 256, smem, s>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
-                                               (const __nv_bfloat16*)w, (const float*)rstd,
-                                               (__nv_bfloat16*)dx, (float*)dw,
-                                               (const __nv_bfloat16*)dres, rows, d);
+  // dx: one warp per row at full occupancy; dw: column reduction
+  rmsnorm_bwd_kernel<<<(rows + 7) / 8, 256, 0, s>>>((const __nv_bfloat16*)dy,
+                                                    (const __nv_bfloat16*)x,
+                                                    (const __nv_bfloat16*)w, (const float*)rstd,
+                                                    (__nv_bfloat16*)dx, (float*)dw,
+                                                    (const __nv_bfloat16*)dres, rows, d);
+  const int cblocks = (d / 8 + 31) / 32;
+  int rblocks = (2 * num_sms() + cblocks - 1) / cblocks;
+  if (rblocks > rows / 64) rblocks = rows / 64 > 0 ? rows / 64 : 1;
+  int rpb = (rows + rblocks - 1) / rblocks;
+  rpb = ((rpb + 7) / 8) * 8;
+  rblocks = (rows + rpb - 1) / rpb;
+  rmsnorm_bwd_w_kernel<<<dim3(cblocks, rblocks), 256, 0, s>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)rstd, (float*)dw, rows,
+      d, rpb);
   return launched2("rmsnorm_bwd");
 }
 

@@ -13,7 +13,7 @@ from ._lib import call as _call
 
 # Device kernel launches issued per C-ABI entry point (for the bench's gpu_launches).
 _LAUNCHES_PER_CALL = {"zb_attn_bwd": 3, "zb_attn_bwd_tc": 3, "zb_layernorm_bwd": 2,
-                      "zb_layernorm_bwd_ex": 2}
+                      "zb_layernorm_bwd_ex": 2, "zb_rmsnorm_bwd": 2}
 _launches = [0]
 
 
