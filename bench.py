@@ -9,8 +9,9 @@ from the planner on an emulated-heterogeneity profile (half b200, half
 half-speed b200h), 8 sequences per GPU on average (weak scaling; at N=8 this
 is exactly config 2: global batch 64, shares 11x4 / 5x4).
 
-ours      : the B200 executor (tcgen05 GEMMs, flash attention, fused AdamW,
-            NCCL AG-v/RS-v) — value = whole-job tokens/s, device-timed,
+ours      : the B200 executor (tcgen05 GEMMs and flash attention, AG-v and fused
+            RS-v + AdamW over NVLink peer memory; --collectives nccl for the NCCL
+            baseline) — value = whole-job tokens/s, device-timed,
             max over ranks; e2e = same metric through ZorseTrainer.step with
             the batch in pinned host memory and the loss read back each step.
 reference : the reference has no training step (hetplan is a planner +
@@ -127,6 +128,7 @@ class TimedOps:
     def __init__(self, ops):
         self.ops = ops
         self.records = []
+        self.bytes = []
 
     def __getattr__(self, name):
         return getattr(self.ops, name)
@@ -143,6 +145,9 @@ class TimedOps:
         r = self.ops.gemm(a, b, out, **kw)
         e.record()
         self.records.append((s, e, 2.0 * M * N * K))
+        # algorithmic DRAM bytes: A and B read once, C written once (+ read for beta)
+        c_bytes = M * N * out.element_size() * (2 if kw.get("beta", 0.0) else 1)
+        self.bytes.append(2.0 * (M * K + N * K) + c_bytes)
         return r
 
 
@@ -392,7 +397,11 @@ def run_ours(args):
                          "peak_source": f"{src} bf16_tflops_sustained",
                          "gemm_share_of_step": g_ms / (ms / args.steps),
                          "launches_per_step": n_launch, "timing_mode": mode,
-                         "algorithmic_flops_per_step": g_flops},
+                         "algorithmic_flops_per_step": g_flops,
+                         "algorithmic_bytes_per_launch": (sum(timed.bytes) / len(timed.bytes)
+                                                          if timed.bytes else None),
+                         "traffic_source": "profiles/gemm_traffic.json (ncu dram bytes, cold "
+                                           "cache, every GEMM launch of one step)"},
             "clocks": clocks.summary(),
         }
         if coll is not None:
