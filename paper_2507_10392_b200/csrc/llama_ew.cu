@@ -164,25 +164,42 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_w_kernel(
 // i < D/2:  (a, b) = (x[i], x[i + D/2]) -> (a cos - b sin, a sin + b cos),
 // angle = pos * theta^(-2i/D), pos = row % S.  inverse=1 rotates by -angle
 // (the gradient of the rotation).
-__global__ void rope_kernel(__nv_bfloat16* qkv, int rows, int S, int H, int D, int ld,
-                            float theta, int inverse) {
+__global__ void __launch_bounds__(256) rope_kernel(__nv_bfloat16* qkv, int rows, int S, int H,
+                                                   int D, int ld, float theta, int inverse) {
+  // thread = (row, q/k head, 8 consecutive rotation pairs): two 16-byte loads / stores,
+  // inverse frequencies from a per-CTA table
+  __shared__ float inv_freq[128];
   const int half = D / 2;
-  const long long total = (long long)rows * 2 * H * half;
+  for (int c = threadIdx.x; c < half; c += blockDim.x)
+    inv_freq[c] = exp2f(-(2.f * c / D) * log2f(theta));
+  __syncthreads();
+  const int groups = half / 8;
+  const long long total = (long long)rows * 2 * H * groups;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(i % half);
-    long long t = i / half;
+    const int g = (int)(i % groups);
+    const long long t = i / groups;
     const int hh = (int)(t % (2 * H));  // 0..H-1: q heads, H..2H-1: k heads
     const int row = (int)(t / (2 * H));
-    const int pos = row % S;
-    const float inv_freq = exp2f(-(2.f * c / D) * log2f(theta));
-    float sn, cs;
-    sincosf(pos * inv_freq, &sn, &cs);
-    if (inverse) sn = -sn;
-    __nv_bfloat16* p = qkv + (size_t)row * ld + hh * D;
-    const float a = __bfloat162float(p[c]), b = __bfloat162float(p[c + half]);
-    p[c] = __float2bfloat16(a * cs - b * sn);
-    p[c + half] = __float2bfloat16(a * sn + b * cs);
+    const float pos = (float)(row % S);
+    __nv_bfloat16* p = qkv + (size_t)row * ld + hh * D + g * 8;
+    uint4 qa = *reinterpret_cast<const uint4*>(p), qb = *reinterpret_cast<const uint4*>(p + half);
+    uint32_t *ai = &qa.x, *bi = &qb.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 a = unpack_bf16(ai[k]), b = unpack_bf16(bi[k]);
+      float s0, c0, s1, c1;
+      sincosf(pos * inv_freq[g * 8 + 2 * k], &s0, &c0);
+      sincosf(pos * inv_freq[g * 8 + 2 * k + 1], &s1, &c1);
+      if (inverse) {
+        s0 = -s0;
+        s1 = -s1;
+      }
+      ai[k] = pack_bf16(a.x * c0 - b.x * s0, a.y * c1 - b.y * s1);
+      bi[k] = pack_bf16(a.x * s0 + b.x * c0, a.y * s1 + b.y * c1);
+    }
+    *reinterpret_cast<uint4*>(p) = qa;
+    *reinterpret_cast<uint4*>(p + half) = qb;
   }
 }
 
@@ -292,9 +309,10 @@ extern "C" int zb_rmsnorm_bwd(const void* dy, const void* x, const void* w, cons
 
 extern "C" int zb_rope(void* qkv, int rows, int S, int H, int D, int ld, float theta, int inverse,
                        cudaStream_t s) {
-  if (D % 2) return set_error(ZB_ERR_INVALID, "rope: head_dim must be even");
+  if (D % 16 || D > 256) return set_error(ZB_ERR_INVALID, "rope: head_dim must be a multiple of 16, <= 256");
+  if (ld % 8 || ((uintptr_t)qkv & 15)) return set_error(ZB_ERR_INVALID, "rope: 16-byte aligned rows needed");
   if (rows <= 0) return 0;
-  long long n = (long long)rows * 2 * H * (D / 2);
+  long long n = (long long)rows * 2 * H * (D / 16);
   rope_kernel<<<grid_for2(n, 256), 256, 0, s>>>((__nv_bfloat16*)qkv, rows, S, H, D, ld, theta,
                                                 inverse);
   return launched2("rope");

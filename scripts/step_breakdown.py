@@ -56,8 +56,28 @@ class Timed:
         return wrapped
 
 
+def _llama_workload():
+    """Two Llama-7B layers (d 4096, f 11008, 32 heads x 128, seq 2048), 4 sequences."""
+    from paper_2507_10392_b200 import plan as P
+    from paper_2507_10392_b200.plan import emulated as E
+    cfg = E.ModelConfig("llama7b-2L", "llama", 2, 4096, 32, 32000, 2048, d_ff=11008)
+    prof = E.profile_from_json(E.profile_json(E.dp_group_nodes(1)))
+    rt = P.fit_runtime_model(prof)
+    gb = 4
+    ctx = P.CostContext(graph=P.build_cluster_graph(prof), runtime=rt, model=cfg.model_spec(),
+                        workload=P.WorkloadSpec(gb, cfg.seq_len))
+    plan = P.build_plan(ctx, prof, P.make_partition(ctx.graph, [[d.id for d in prof.devices]]),
+                        1, [cfg.n_layer], P.Strategy.INTERLEAVED, P.cluster_fingerprint(prof),
+                        "transformer")
+    P.attach_routing(plan, rt, "transformer")
+    return cfg, plan, ctx, gb
+
+
 def main():
-    cfg, plan, ctx, gb = bench.build_workload(1)
+    if os.environ.get("ZB_BREAKDOWN_MODEL") == "llama":
+        cfg, plan, ctx, gb = _llama_workload()
+    else:
+        cfg, plan, ctx, gb = bench.build_workload(1)
     tr = ZorseTrainer(plan, ctx, cfg)
     ex = tr.exec
     tr.load(synthetic_batch(cfg.vocab, cfg.seq_len, gb, 1, pin=True))

@@ -189,9 +189,9 @@ def test_rmsnorm(cuda, rows, d):
     assert rel(dw, wf.grad) < 1e-3
 
 
-def test_rope_roundtrip_and_reference(cuda):
+@pytest.mark.parametrize("n,S,H,D", [(2, 128, 4, 128), (1, 2048, 2, 128), (2, 256, 3, 64)])
+def test_rope_roundtrip_and_reference(cuda, n, S, H, D):
     torch.manual_seed(7)
-    n, S, H, D = 2, 128, 4, 128
     qkv = torch.randn(n * S, 3 * H * D, device="cuda").bfloat16()
     orig = qkv.clone()
     K.rope(qkv, S, H, D)
