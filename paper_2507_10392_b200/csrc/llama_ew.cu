@@ -173,14 +173,11 @@ __global__ void __launch_bounds__(256) rope_kernel(__nv_bfloat16* qkv, int rows,
   for (int c = threadIdx.x; c < half; c += blockDim.x)
     inv_freq[c] = exp2f(-(2.f * c / D) * log2f(theta));
   __syncthreads();
-  const int groups = half / 8;
-  const long long total = (long long)rows * 2 * H * groups;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(i % groups);
-    const long long t = i / groups;
-    const int hh = (int)(t % (2 * H));  // 0..H-1: q heads, H..2H-1: k heads
-    const int row = (int)(t / (2 * H));
+  const unsigned groups = half / 8, heads2 = 2 * H;
+  const unsigned total = (unsigned)rows * heads2 * groups;  // < 2^31, checked on the host
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned t = i / groups, g = i - t * groups;
+    const unsigned row = t / heads2, hh = t - row * heads2;  // hh < H: q heads, else k heads
     const float pos = (float)(row % S);
     __nv_bfloat16* p = qkv + (size_t)row * ld + hh * D + g * 8;
     uint4 qa = *reinterpret_cast<const uint4*>(p), qb = *reinterpret_cast<const uint4*>(p + half);
@@ -205,13 +202,13 @@ __global__ void __launch_bounds__(256) rope_kernel(__nv_bfloat16* qkv, int rows,
 
 // ------------------------------------------------------------------ SwiGLU
 // gu rows = [gate(f) | up(f)];  out = silu(gate) * up.
+// (32-bit index math: the host checks rows * f / 8 < 2^31)
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
                                   __nv_bfloat16* __restrict__ out, int rows, int f) {
-  const int nv = f >> 3;
-  const long long total = (long long)rows * nv;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int row = (int)(i / nv), v = (int)(i % nv);
+  const unsigned nv = f >> 3;
+  const unsigned total = (unsigned)rows * nv;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned row = i / nv, v = i - row * nv;
     const __nv_bfloat16* r = gu + (size_t)row * 2 * f;
     const uint4 g = reinterpret_cast<const uint4*>(r)[v];
     const uint4 u = reinterpret_cast<const uint4*>(r + f)[v];
@@ -221,7 +218,7 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       float2 a = unpack_bf16(gi[k]), b = unpack_bf16(ui[k]);
-      const float s0 = a.x / (1.f + __expf(-a.x)), s1 = a.y / (1.f + __expf(-a.y));
+      const float s0 = __fdividef(a.x, 1.f + __expf(-a.x)), s1 = __fdividef(a.y, 1.f + __expf(-a.y));
       oi[k] = pack_bf16(s0 * b.x, s1 * b.y);
     }
     reinterpret_cast<uint4*>(out + (size_t)row * f)[v] = o;
@@ -232,11 +229,10 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
 // May run in place (dgu == gu).
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* gu, const __nv_bfloat16* __restrict__ dout,
                                   __nv_bfloat16* dgu, int rows, int f) {
-  const int nv = f >> 3;
-  const long long total = (long long)rows * nv;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int row = (int)(i / nv), v = (int)(i % nv);
+  const unsigned nv = f >> 3;
+  const unsigned total = (unsigned)rows * nv;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned row = i / nv, v = i - row * nv;
     const __nv_bfloat16* r = gu + (size_t)row * 2 * f;
     const uint4 g = reinterpret_cast<const uint4*>(r)[v];
     const uint4 u = reinterpret_cast<const uint4*>(r + f)[v];
@@ -247,7 +243,7 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* gu, const __nv_bfloat16* 
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       float2 a = unpack_bf16(gi[k]), b = unpack_bf16(ui[k]), dd = unpack_bf16(di[k]);
-      const float sg0 = 1.f / (1.f + __expf(-a.x)), sg1 = 1.f / (1.f + __expf(-a.y));
+      const float sg0 = __frcp_rn(1.f + __expf(-a.x)), sg1 = __frcp_rn(1.f + __expf(-a.y));
       const float si0 = a.x * sg0, si1 = a.y * sg1;
       const float ds0 = sg0 * (1.f + a.x * (1.f - sg0)), ds1 = sg1 * (1.f + a.y * (1.f - sg1));
       ogi[k] = pack_bf16(dd.x * b.x * ds0, dd.y * b.y * ds1);
@@ -312,6 +308,8 @@ extern "C" int zb_rope(void* qkv, int rows, int S, int H, int D, int ld, float t
   if (D % 16 || D > 256) return set_error(ZB_ERR_INVALID, "rope: head_dim must be a multiple of 16, <= 256");
   if (ld % 8 || ((uintptr_t)qkv & 15)) return set_error(ZB_ERR_INVALID, "rope: 16-byte aligned rows needed");
   if (rows <= 0) return 0;
+  if ((long long)rows * 2 * H * (D / 16) >= (1ll << 31))
+    return set_error(ZB_ERR_UNSUPPORTED, "rope: too many elements for one launch");
   long long n = (long long)rows * 2 * H * (D / 16);
   rope_kernel<<<grid_for2(n, 256), 256, 0, s>>>((__nv_bfloat16*)qkv, rows, S, H, D, ld, theta,
                                                 inverse);
@@ -321,6 +319,8 @@ extern "C" int zb_rope(void* qkv, int rows, int S, int H, int D, int ld, float t
 extern "C" int zb_swiglu_fwd(const void* gu, void* out, int rows, int f, cudaStream_t s) {
   if (f % 8) return set_error(ZB_ERR_INVALID, "swiglu: f must be a multiple of 8");
   if (rows <= 0) return 0;
+  if ((long long)rows * (f / 8) >= (1ll << 31))
+    return set_error(ZB_ERR_UNSUPPORTED, "swiglu: too many elements for one launch");
   swiglu_fwd_kernel<<<grid_for2((long long)rows * (f / 8), 256), 256, 0, s>>>(
       (const __nv_bfloat16*)gu, (__nv_bfloat16*)out, rows, f);
   return launched2("swiglu_fwd");
@@ -330,6 +330,8 @@ extern "C" int zb_swiglu_bwd(const void* gu, const void* dout, void* dgu, int ro
                              cudaStream_t s) {
   if (f % 8) return set_error(ZB_ERR_INVALID, "swiglu: f must be a multiple of 8");
   if (rows <= 0) return 0;
+  if ((long long)rows * (f / 8) >= (1ll << 31))
+    return set_error(ZB_ERR_UNSUPPORTED, "swiglu: too many elements for one launch");
   swiglu_bwd_kernel<<<grid_for2((long long)rows * (f / 8), 256), 256, 0, s>>>(
       (const __nv_bfloat16*)gu, (const __nv_bfloat16*)dout, (__nv_bfloat16*)dgu, rows, f);
   return launched2("swiglu_bwd");
