@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master,
                                                     __nv_bfloat16* __restrict__ param,
                                                     float* __restrict__ sumsq, int64_t n,
                                                     AdamParams a) {
+  pdl_enter();
   resolve_step(a);
   float ss = 0.f;
   const int64_t n4 = n >> 2;
@@ -70,7 +71,10 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master,
 
 using namespace zb;
 
-__global__ void step_inc_kernel(int* step) { *step += 1; }
+__global__ void step_inc_kernel(int* step) {
+  pdl_enter();
+  *step += 1;
+}
 
 // step <= 0 with step_dev != NULL: the step number is read from device memory.
 static int adamw_impl(void* master, void* exp_avg, void* exp_avg_sq, const void* grad,
@@ -95,9 +99,9 @@ static int adamw_impl(void* master, void* exp_avg, void* exp_avg_sq, const void*
   int64_t want = (n / 4 + 255) / 256;
   int64_t cap = (int64_t)num_sms() * 8;
   int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
-  adamw_kernel<<<grid, 256, 0, s>>>((float*)master, (float*)exp_avg, (float*)exp_avg_sq,
-                                    (const float*)grad, (__nv_bfloat16*)param_bf16, (float*)sumsq,
-                                    n, a);
+  launch_pdl_k(adamw_kernel, dim3(grid), dim3(256), 0, s, (float*)master, (float*)exp_avg,
+               (float*)exp_avg_sq, (const float*)grad, (__nv_bfloat16*)param_bf16, (float*)sumsq, n,
+               a);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_cuda_error(e, "adamw");
 }
@@ -121,7 +125,7 @@ extern "C" int zb_adamw_shard_dstep(void* master, void* exp_avg, void* exp_avg_s
 }
 
 extern "C" int zb_step_increment(void* step_dev, cudaStream_t s) {
-  step_inc_kernel<<<1, 1, 0, s>>>((int*)step_dev);
+  launch_pdl_k(step_inc_kernel, dim3(1), dim3(1), 0, s, (int*)step_dev);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_cuda_error(e, "step_increment");
 }

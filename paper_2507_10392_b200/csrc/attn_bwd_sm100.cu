@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
   const uint32_t t_dqp = tmem + 256 + 2 * D;  // FQ: [2][D] columns
   griddep_wait();  // PDL: prologue overlapped the previous kernel's tail
+  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -604,6 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
   const uint32_t t_dqp = tmem + 256 + 2 * D;
   griddep_wait();
+  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -826,9 +828,51 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
+// delta[b,h,q] = sum_d dO[t,h,d] * O[t,h,d]  (t = b*S + q), and — when dq_accum is
+// given — zero that (t, h) slice of the fp32 dQ accumulator in the same pass (it is
+// TMA reduce-added into by the fused backward).  D/8 threads per (t, h), one 16-byte
+// load of each operand per thread; (t, h) pairs are h-major so the delta writes of a
+// warp are contiguous.  Replaces a one-warp-per-row kernel (19 us at GPT-2 small)
+// plus a separate memset of the accumulator.
+template <int D>
+__global__ void __launch_bounds__(256) delta_zero_kernel(const __nv_bfloat16* __restrict__ o,
+                                                         const __nv_bfloat16* __restrict__ dout,
+                                                         float* __restrict__ delta,
+                                                         float* __restrict__ dq_accum, int T,
+                                                         int S, int H) {
+  pdl_enter();
+  constexpr int TPR = D / 8;  // threads per (t, h)
+  const int gid = blockIdx.x * (blockDim.x / TPR) + threadIdx.x / TPR;
+  const int sub = threadIdx.x % TPR;
+  if (gid >= T * H) return;
+  const int h = gid / T, t = gid - h * T;
+  const size_t off = (size_t)t * H * D + h * D + sub * 8;
+  const uint4 a = *reinterpret_cast<const uint4*>(o + off);
+  const uint4 g = *reinterpret_cast<const uint4*>(dout + off);
+  const uint32_t *ai = &a.x, *gi = &g.x;
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 x = unpack_bf16(ai[k]), y = unpack_bf16(gi[k]);
+    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+  }
+#pragma unroll
+  for (int m = TPR / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (dq_accum) {
+    float4* z = reinterpret_cast<float4*>(dq_accum + off);
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (sub == 0) {
+    const int b = t / S, q = t - b * S;
+    delta[((size_t)b * H + h) * S + q] = acc;
+  }
+}
+
 // dq (bf16, pitch ld, scaled) = dq_accum (fp32, pitch H*D)
 __global__ void dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dqkv,
                                   int rows, int HD, int ld, float scale) {
+  pdl_enter();
   const int per_row = HD / 8;
   const int64_t n = (int64_t)rows * per_row;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -852,11 +896,14 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
   const int Tn = n_seq * S;
   static const bool two_pass = getenv("ZB_ATTN_BWD_TWO_PASS") != nullptr;  // A/B
   const bool fused = D == 64 && dq_accum && !two_pass;
-  if (fused) {  // before the delta kernel, so the PDL launch below follows a kernel
-    cudaError_t e = cudaMemsetAsync(dq_accum, 0, (size_t)Tn * H * D * 4, s);
-    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: dq_accum memset");
+  {
+    const int per_cta = 256 / (D / 8);
+    cudaError_t e = launch_pdl_k(delta_zero_kernel<D>, dim3((Tn * H + per_cta - 1) / per_cta),
+                                 dim3(256), 0, s, (const __nv_bfloat16*)out,
+                                 (const __nv_bfloat16*)dout, (float*)delta,
+                                 fused ? (float*)dq_accum : (float*)nullptr, Tn, S, H);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: delta");
   }
-  if (int rc = launch_attn_delta(out, dout, delta, Tn, S, H, D, s)) return rc;
   CUtensorMap mq, mo, mdq;
   if (int rc = make_tmap_bf16_2d(&mq, qkv, (uint64_t)3 * H * D, Tn, ld, 64, T)) return rc;
   if (int rc = make_tmap_bf16_2d(&mo, dout, (uint64_t)H * D, Tn, (uint64_t)H * D, 64, T)) return rc;
@@ -923,9 +970,8 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     const int64_t n8 = (int64_t)Tn * (HD / 8);
     int cg = (int)((n8 + 255) / 256);
     if (cg > num_sms() * 8) cg = num_sms() * 8;
-    dq_convert_kernel<<<cg, 256, 0, s>>>((const float*)dq_accum, (__nv_bfloat16*)dqkv, Tn, HD, ld,
-                                         scale);
-    e = cudaGetLastError();
+    e = launch_pdl_k(dq_convert_kernel, dim3(cg), dim3(256), 0, s, (const float*)dq_accum,
+                     (__nv_bfloat16*)dqkv, Tn, HD, ld, scale);
     return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_bwd_tc fused launch");
   }
   if (only != 1)

@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_s = tmem + COL_S, t_p = tmem + COL_P, t_o = tmem + COL_O;
   griddep_wait();  // PDL: prologue overlapped the previous kernel's tail
+  griddep_launch();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -794,6 +795,7 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   griddep_wait();  // PDL: prologue overlapped the previous kernel's tail
+  griddep_launch();
   const uint32_t t_s[2] = {tmem, tmem + 128};
   const uint32_t t_o[2] = {tmem + 256, tmem + 256 + D};
 

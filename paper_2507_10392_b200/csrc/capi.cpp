@@ -1,6 +1,7 @@
 // C-ABI plumbing for libzorse_b200: thread-local error strings, device queries,
 // and the driver entry point used to encode TMA tensor maps.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -21,6 +22,11 @@ int set_error(int code, const char* fmt, ...) {
 
 int set_cuda_error(cudaError_t e, const char* where) {
   return set_error(ZB_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool pdl_enabled() {
+  static const bool on = getenv("ZB_NO_PDL") == nullptr;
+  return on;
 }
 
 int num_sms() {

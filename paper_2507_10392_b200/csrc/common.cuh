@@ -190,6 +190,20 @@ ZB_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::
 // prefetch) while its predecessor's last CTAs drain; it must wait here before
 // touching memory the predecessor produces or consumes.
 ZB_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the next PDL-launched kernel of the stream start its prologue.  Issued by
+// every CTA right after its own griddep_wait (and after any TMEM allocation), so a
+// dependent grid is only launched once every CTA of this grid is resident and owns
+// its TMEM: a dependent CTA that lands beside it can never take TMEM this grid
+// still needs.  Visibility is unaffected: the dependent's griddep_wait still waits
+// for this whole grid to complete.
+ZB_DEVICE void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// Both, for kernels without a prologue worth overlapping.
+ZB_DEVICE void pdl_enter() {
+  griddep_wait();
+  griddep_launch();
+}
 
 ZB_DEVICE void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
     const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y,
     float* __restrict__ mean_out, float* __restrict__ rstd_out, int rows, int d, float eps) {
+  pdl_enter();
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
     const __nv_bfloat16* __restrict__ w, const float* __restrict__ mean_in,
     const float* __restrict__ rstd_in, __nv_bfloat16* dx, float* __restrict__ dw,
     float* __restrict__ db, const __nv_bfloat16* dres, int rows, int d) {
+  pdl_enter();
   extern __shared__ float sh[];  // [16][warps][32] block-reduction staging
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
@@ -213,6 +215,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(
     const __nv_bfloat16* __restrict__ w, const float* __restrict__ mean_in,
     const float* __restrict__ rstd_in, __nv_bfloat16* dx, const __nv_bfloat16* dres, int rows,
     int d) {
+  pdl_enter();
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -281,6 +284,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_wb_kernel(
     float* __restrict__ db, const __nv_bfloat16* __restrict__ dres,
     const __nv_bfloat16* __restrict__ dxo, float* __restrict__ db_res, float* __restrict__ db_out,
     int rows, int d, int rows_per_block) {
+  pdl_enter();
   constexpr int NV = EXTRA ? 32 : 16;  // accumulated values per column vector
   const int cv = blockIdx.x * 32 + (threadIdx.x & 31);  // column vector (8 cols)
   const int rl = threadIdx.x >> 5;                       // 0..7
@@ -358,6 +362,7 @@ __global__ void embedding_fwd_kernel(const int* __restrict__ tok,
                                      const __nv_bfloat16* __restrict__ wte,
                                      const __nv_bfloat16* __restrict__ wpe,
                                      __nv_bfloat16* __restrict__ out, int rows, int d, int seq) {
+  pdl_enter();
   const int nv = d >> 3;
   const size_t total = (size_t)rows * nv;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
@@ -382,6 +387,7 @@ __global__ void embedding_bwd_kernel(const int* __restrict__ tok,
                                      const __nv_bfloat16* __restrict__ dout,
                                      float* __restrict__ dwte, float* __restrict__ dwpe, int rows,
                                      int d, int seq) {
+  pdl_enter();
   const int nv = d >> 3;
   const size_t total = (size_t)rows * nv;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
@@ -413,6 +419,7 @@ __global__ void __launch_bounds__(XENT_THREADS) xent_kernel(const __nv_bfloat16*
                                                           float* __restrict__ loss_sum,
                                                           __nv_bfloat16* dlogits, int V, int ld,
                                                           float scale) {
+  pdl_enter();
   const int row = blockIdx.x;
   const __nv_bfloat16* lr = logits + (size_t)row * ld;
   __nv_bfloat16* gr = dlogits + (size_t)row * ld;
@@ -488,6 +495,7 @@ __global__ void __launch_bounds__(XENT_THREADS) xent_kernel(const __nv_bfloat16*
 // each thread keeps 4 row loads in flight.
 __global__ void bias_grad_kernel(const __nv_bfloat16* __restrict__ dy, float* __restrict__ db,
                                  int rows, int n, int ld, int rows_per_block) {
+  pdl_enter();
   const int cv = blockIdx.x * 32 + (threadIdx.x & 31);  // column vector (8 cols)
   const int rl = threadIdx.x >> 5;                       // 0..7
   const int r0 = blockIdx.y * rows_per_block;
@@ -541,17 +549,20 @@ __global__ void bias_grad_kernel(const __nv_bfloat16* __restrict__ dy, float* __
 // ------------------------------------------------------------------ small ops
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ d,
                                      int64_t n) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     d[i] = __float2bfloat16(s[i]);
 }
 __global__ void fill_f32_kernel(float* __restrict__ p, float v, int64_t n) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
 }
 __global__ void add_bf16_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b,
                                 __nv_bfloat16* o, int64_t n) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     o[i] = __float2bfloat16(__bfloat162float(a[i]) + __bfloat162float(b[i]));
@@ -580,9 +591,9 @@ extern "C" int zb_layernorm_fwd(const void* x, const void* w, const void* b, voi
   const int threads = 256, per = threads / 32;
   const int vpl = (d / 8 + 31) / 32;
   auto go = [&](auto kern) {
-    kern<<<(rows + per - 1) / per, threads, 0, s>>>(
-        (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, (const __nv_bfloat16*)b,
-        (__nv_bfloat16*)y, (float*)mean, (float*)rstd, rows, d, eps);
+    launch_pdl_k(kern, dim3((rows + per - 1) / per), dim3(threads), 0, s, (const __nv_bfloat16*)x,
+                 (const __nv_bfloat16*)w, (const __nv_bfloat16*)b, (__nv_bfloat16*)y, (float*)mean,
+                 (float*)rstd, rows, d, eps);
   };
   if (vpl <= 1) go(layernorm_fwd_kernel<1>);
   else if (vpl <= 2) go(layernorm_fwd_kernel<2>);
@@ -606,10 +617,10 @@ static int layernorm_bwd_impl(const void* dy, const void* x, const void* w, cons
   static const bool fused = getenv("ZB_LN_BWD_FUSED") != nullptr;  // A/B: single-kernel variant
   if (!fused) {
     auto go1 = [&](auto kern) {
-      kern<<<(rows + per - 1) / per, threads, 0, s>>>(
-          (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w,
-          (const float*)mean, (const float*)rstd, (__nv_bfloat16*)dx, (const __nv_bfloat16*)dres,
-          rows, d);
+      launch_pdl_k(kern, dim3((rows + per - 1) / per), dim3(threads), 0, s,
+                   (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w,
+                   (const float*)mean, (const float*)rstd, (__nv_bfloat16*)dx,
+                   (const __nv_bfloat16*)dres, rows, d);
     };
     if (vpl <= 1) go1(layernorm_bwd_dx_kernel<1>);
     else if (vpl <= 2) go1(layernorm_bwd_dx_kernel<2>);
@@ -627,15 +638,15 @@ static int layernorm_bwd_impl(const void* dy, const void* x, const void* w, cons
     if (db_res || db_out) {
       if (!db_res || !db_out || !dres)
         return set_error(ZB_ERR_INVALID, "layernorm_bwd: db_res / db_out need dres and each other");
-      layernorm_bwd_wb_kernel<true><<<dim3(cblocks, rblocks), 256, 0, s>>>(
-          (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)mean,
-          (const float*)rstd, (float*)dw, (float*)db, (const __nv_bfloat16*)dres,
-          (const __nv_bfloat16*)dx, (float*)db_res, (float*)db_out, rows, d, rpb);
+      launch_pdl_k(layernorm_bwd_wb_kernel<true>, dim3(cblocks, rblocks), dim3(256), 0, s,
+                   (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)mean,
+                   (const float*)rstd, (float*)dw, (float*)db, (const __nv_bfloat16*)dres,
+                   (const __nv_bfloat16*)dx, (float*)db_res, (float*)db_out, rows, d, rpb);
     } else {
-      layernorm_bwd_wb_kernel<false><<<dim3(cblocks, rblocks), 256, 0, s>>>(
-          (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)mean,
-          (const float*)rstd, (float*)dw, (float*)db, nullptr, nullptr, nullptr, nullptr, rows,
-          d, rpb);
+      launch_pdl_k(layernorm_bwd_wb_kernel<false>, dim3(cblocks, rblocks), dim3(256), 0, s,
+                   (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)mean,
+                   (const float*)rstd, (float*)dw, (float*)db, nullptr, nullptr, nullptr, nullptr,
+                   rows, d, rpb);
     }
     return launched("layernorm_bwd");
   }
@@ -647,10 +658,10 @@ static int layernorm_bwd_impl(const void* dy, const void* x, const void* w, cons
   auto go = [&](auto kern) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<blocks, threads, smem, s>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
-                                       (const __nv_bfloat16*)w, (const float*)mean,
-                                       (const float*)rstd, (__nv_bfloat16*)dx, (float*)dw,
-                                       (float*)db, (const __nv_bfloat16*)dres, rows, d);
+    launch_pdl_k(kern, dim3(blocks), dim3(threads), smem, s, (const __nv_bfloat16*)dy,
+                 (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, (const float*)mean,
+                 (const float*)rstd, (__nv_bfloat16*)dx, (float*)dw, (float*)db,
+                 (const __nv_bfloat16*)dres, rows, d);
   };
   if (vpl <= 1) go(layernorm_bwd_kernel<1>);
   else if (vpl <= 2) go(layernorm_bwd_kernel<2>);
@@ -683,9 +694,9 @@ extern "C" int zb_embedding_fwd(const void* tok, const void* wte, const void* wp
   if (d % 8) return set_error(ZB_ERR_INVALID, "embedding: d must be a multiple of 8");
   if (rows <= 0) return 0;
   int64_t n = (int64_t)rows * (d / 8);
-  embedding_fwd_kernel<<<grid_for(n, 256), 256, 0, s>>>(
-      (const int*)tok, (const __nv_bfloat16*)wte, (const __nv_bfloat16*)wpe, (__nv_bfloat16*)out,
-      rows, d, seq);
+  launch_pdl_k(embedding_fwd_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, (const int*)tok,
+               (const __nv_bfloat16*)wte, (const __nv_bfloat16*)wpe, (__nv_bfloat16*)out, rows, d,
+               seq);
   return launched("embedding_fwd");
 }
 
@@ -694,8 +705,8 @@ extern "C" int zb_embedding_bwd(const void* tok, const void* dout, void* dwte, v
   if (d % 8) return set_error(ZB_ERR_INVALID, "embedding: d must be a multiple of 8");
   if (rows <= 0) return 0;
   int64_t n = (int64_t)rows * (d / 8);
-  embedding_bwd_kernel<<<grid_for(n, 256), 256, 0, s>>>(
-      (const int*)tok, (const __nv_bfloat16*)dout, (float*)dwte, (float*)dwpe, rows, d, seq);
+  launch_pdl_k(embedding_bwd_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, (const int*)tok,
+               (const __nv_bfloat16*)dout, (float*)dwte, (float*)dwpe, rows, d, seq);
   return launched("embedding_bwd");
 }
 
@@ -704,9 +715,8 @@ extern "C" int zb_xent_fwd_bwd(const void* logits, const void* labels, void* los
                                cudaStream_t s) {
   if (V % 8 || ld % 8) return set_error(ZB_ERR_INVALID, "xent: V and ld must be multiples of 8");
   if (rows <= 0) return 0;
-  xent_kernel<<<rows, XENT_THREADS, 0, s>>>((const __nv_bfloat16*)logits, (const int*)labels,
-                                            (float*)loss_sum, (__nv_bfloat16*)dlogits, V, ld,
-                                            scale);
+  launch_pdl_k(xent_kernel, dim3(rows), dim3(XENT_THREADS), 0, s, (const __nv_bfloat16*)logits,
+               (const int*)labels, (float*)loss_sum, (__nv_bfloat16*)dlogits, V, ld, scale);
   return launched("xent");
 }
 
@@ -722,26 +732,27 @@ extern "C" int zb_bias_grad(const void* dy, void* db, int rows, int n, int ld, c
   int rpb = (rows + rblocks - 1) / rblocks;
   rpb = ((rpb + 7) / 8) * 8;
   rblocks = (rows + rpb - 1) / rpb;
-  bias_grad_kernel<<<dim3(cblocks, rblocks), 256, 0, s>>>((const __nv_bfloat16*)dy, (float*)db,
-                                                          rows, n, ld, rpb);
+  launch_pdl_k(bias_grad_kernel, dim3(cblocks, rblocks), dim3(256), 0, s,
+               (const __nv_bfloat16*)dy, (float*)db, rows, n, ld, rpb);
   return launched("bias_grad");
 }
 
 extern "C" int zb_cast_f32_bf16(const void* src, void* dst, int64_t n, cudaStream_t s) {
   if (n <= 0) return 0;
-  cast_f32_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>((const float*)src, (__nv_bfloat16*)dst, n);
+  launch_pdl_k(cast_f32_bf16_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, (const float*)src,
+               (__nv_bfloat16*)dst, n);
   return launched("cast_f32_bf16");
 }
 
 extern "C" int zb_fill_f32(void* p, float v, int64_t n, cudaStream_t s) {
   if (n <= 0) return 0;
-  fill_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>((float*)p, v, n);
+  launch_pdl_k(fill_f32_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, (float*)p, v, n);
   return launched("fill_f32");
 }
 
 extern "C" int zb_add_bf16(const void* a, const void* b, void* o, int64_t n, cudaStream_t s) {
   if (n <= 0) return 0;
-  add_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>((const __nv_bfloat16*)a,
-                                                   (const __nv_bfloat16*)b, (__nv_bfloat16*)o, n);
+  launch_pdl_k(add_bf16_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, (const __nv_bfloat16*)a,
+               (const __nv_bfloat16*)b, (__nv_bfloat16*)o, n);
   return launched("add_bf16");
 }

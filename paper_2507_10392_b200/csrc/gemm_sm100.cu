@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_wait();  // prologue above overlapped the previous kernel's tail (PDL launch)
+  griddep_launch();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -630,6 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_wait();  // prologue above overlapped the previous kernel's tail (PDL launch)
+  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {

@@ -13,6 +13,7 @@ __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
                                    const __nv_bfloat16* __restrict__ w,
                                    __nv_bfloat16* __restrict__ y, float* __restrict__ rstd_out,
                                    int rows, int d, float eps) {
+  pdl_enter();
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -54,6 +55,7 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
                                    const float* __restrict__ rstd_in, __nv_bfloat16* dx,
                                    float* __restrict__ dw, const __nv_bfloat16* dres, int rows,
                                    int d) {
+  pdl_enter();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nv = d >> 3;
@@ -102,6 +104,7 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_w_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ rstd_in, float* __restrict__ dw, int rows, int d,
     int rows_per_block) {
+  pdl_enter();
   const int cv = blockIdx.x * 32 + (threadIdx.x & 31);
   const int rl = threadIdx.x >> 5;
   const int r0 = blockIdx.y * rows_per_block;
@@ -166,6 +169,7 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_w_kernel(
 // (the gradient of the rotation).
 __global__ void __launch_bounds__(256) rope_kernel(__nv_bfloat16* qkv, int rows, int S, int H,
                                                    int D, int ld, float theta, int inverse) {
+  pdl_enter();
   // thread = (row, q/k head, 8 consecutive rotation pairs): two 16-byte loads / stores,
   // inverse frequencies from a per-CTA table
   __shared__ float inv_freq[128];
@@ -205,6 +209,7 @@ __global__ void __launch_bounds__(256) rope_kernel(__nv_bfloat16* qkv, int rows,
 // (32-bit index math: the host checks rows * f / 8 < 2^31)
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
                                   __nv_bfloat16* __restrict__ out, int rows, int f) {
+  pdl_enter();
   const unsigned nv = f >> 3;
   const unsigned total = (unsigned)rows * nv;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -229,6 +234,7 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
 // May run in place (dgu == gu).
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* gu, const __nv_bfloat16* __restrict__ dout,
                                   __nv_bfloat16* dgu, int rows, int f) {
+  pdl_enter();
   const unsigned nv = f >> 3;
   const unsigned total = (unsigned)rows * nv;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -274,9 +280,8 @@ extern "C" int zb_rmsnorm_fwd(const void* x, const void* w, void* y, void* rstd,
                               float eps, cudaStream_t s) {
   if (d % 8) return set_error(ZB_ERR_INVALID, "rmsnorm: d must be a multiple of 8");
   if (rows <= 0) return 0;
-  rmsnorm_fwd_kernel<<<(rows + 7) / 8, 256, 0, s>>>((const __nv_bfloat16*)x,
-                                                     (const __nv_bfloat16*)w, (__nv_bfloat16*)y,
-                                                     (float*)rstd, rows, d, eps);
+  launch_pdl_k(rmsnorm_fwd_kernel, dim3((rows + 7) / 8), dim3(256), 0, s, (const __nv_bfloat16*)x,
+               (const __nv_bfloat16*)w, (__nv_bfloat16*)y, (float*)rstd, rows, d, eps);
   return launched2("rmsnorm_fwd");
 }
 
@@ -286,20 +291,18 @@ extern "C" int zb_rmsnorm_bwd(const void* dy, const void* x, const void* w, cons
   if (d % 8) return set_error(ZB_ERR_INVALID, "rmsnorm: d must be a multiple of 8");
   if (rows <= 0) return 0;
   // dx: one warp per row at full occupancy; dw: column reduction
-  rmsnorm_bwd_kernel<<<(rows + 7) / 8, 256, 0, s>>>((const __nv_bfloat16*)dy,
-                                                    (const __nv_bfloat16*)x,
-                                                    (const __nv_bfloat16*)w, (const float*)rstd,
-                                                    (__nv_bfloat16*)dx, (float*)dw,
-                                                    (const __nv_bfloat16*)dres, rows, d);
+  launch_pdl_k(rmsnorm_bwd_kernel, dim3((rows + 7) / 8), dim3(256), 0, s, (const __nv_bfloat16*)dy,
+               (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, (const float*)rstd,
+               (__nv_bfloat16*)dx, (float*)dw, (const __nv_bfloat16*)dres, rows, d);
   const int cblocks = (d / 8 + 31) / 32;
   int rblocks = (2 * num_sms() + cblocks - 1) / cblocks;
   if (rblocks > rows / 64) rblocks = rows / 64 > 0 ? rows / 64 : 1;
   int rpb = (rows + rblocks - 1) / rblocks;
   rpb = ((rpb + 7) / 8) * 8;
   rblocks = (rows + rpb - 1) / rpb;
-  rmsnorm_bwd_w_kernel<<<dim3(cblocks, rblocks), 256, 0, s>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)rstd, (float*)dw, rows,
-      d, rpb);
+  launch_pdl_k(rmsnorm_bwd_w_kernel, dim3(cblocks, rblocks), dim3(256), 0, s,
+               (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const float*)rstd, (float*)dw,
+               rows, d, rpb);
   return launched2("rmsnorm_bwd");
 }
 
@@ -311,8 +314,8 @@ extern "C" int zb_rope(void* qkv, int rows, int S, int H, int D, int ld, float t
   if ((long long)rows * 2 * H * (D / 16) >= (1ll << 31))
     return set_error(ZB_ERR_UNSUPPORTED, "rope: too many elements for one launch");
   long long n = (long long)rows * 2 * H * (D / 16);
-  rope_kernel<<<grid_for2(n, 256), 256, 0, s>>>((__nv_bfloat16*)qkv, rows, S, H, D, ld, theta,
-                                                inverse);
+  launch_pdl_k(rope_kernel, dim3(grid_for2(n, 256)), dim3(256), 0, s, (__nv_bfloat16*)qkv, rows, S,
+               H, D, ld, theta, inverse);
   return launched2("rope");
 }
 
@@ -321,8 +324,8 @@ extern "C" int zb_swiglu_fwd(const void* gu, void* out, int rows, int f, cudaStr
   if (rows <= 0) return 0;
   if ((long long)rows * (f / 8) >= (1ll << 31))
     return set_error(ZB_ERR_UNSUPPORTED, "swiglu: too many elements for one launch");
-  swiglu_fwd_kernel<<<grid_for2((long long)rows * (f / 8), 256), 256, 0, s>>>(
-      (const __nv_bfloat16*)gu, (__nv_bfloat16*)out, rows, f);
+  launch_pdl_k(swiglu_fwd_kernel, dim3(grid_for2((long long)rows * (f / 8), 256)), dim3(256), 0, s,
+               (const __nv_bfloat16*)gu, (__nv_bfloat16*)out, rows, f);
   return launched2("swiglu_fwd");
 }
 
@@ -332,7 +335,7 @@ extern "C" int zb_swiglu_bwd(const void* gu, const void* dout, void* dgu, int ro
   if (rows <= 0) return 0;
   if ((long long)rows * (f / 8) >= (1ll << 31))
     return set_error(ZB_ERR_UNSUPPORTED, "swiglu: too many elements for one launch");
-  swiglu_bwd_kernel<<<grid_for2((long long)rows * (f / 8), 256), 256, 0, s>>>(
-      (const __nv_bfloat16*)gu, (const __nv_bfloat16*)dout, (__nv_bfloat16*)dgu, rows, f);
+  launch_pdl_k(swiglu_bwd_kernel, dim3(grid_for2((long long)rows * (f / 8), 256)), dim3(256), 0, s,
+               (const __nv_bfloat16*)gu, (const __nv_bfloat16*)dout, (__nv_bfloat16*)dgu, rows, f);
   return launched2("swiglu_bwd");
 }

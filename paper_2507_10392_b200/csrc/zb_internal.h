@@ -27,4 +27,25 @@ int make_tmap_bf16_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t 
 // delta[b,h,q] = sum_d dO*O (attention backward preprocessing, attn.cu).
 int launch_attn_delta(const void* o, const void* dout, void* delta, int T, int S, int H, int D,
                       cudaStream_t s);
+
+// Programmatic dependent launch (PDL) on `stream`: the kernel may be scheduled while
+// its predecessor drains (once every predecessor CTA executed griddep_launch()), and
+// must call griddep_wait() (common.cuh pdl_enter) before touching global memory.
+// ZB_NO_PDL=1 turns the attribute off (plain stream order) for A/B runs.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                         cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 }  // namespace zb
