@@ -1231,6 +1231,15 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
     return set_error(ZB_ERR_INVALID, "gemm: lda/ldb must be multiples of 8 elements");
   if (((uintptr_t)A & 15) || ((uintptr_t)B & 15))
     return set_error(ZB_ERR_INVALID, "gemm: A/B must be 16-byte aligned");
+  if (epilogue < EPI_BF16 || epilogue > EPI_BIAS_GELU_NA)
+    return set_error(ZB_ERR_INVALID, "gemm: unknown epilogue %d", epilogue);
+  const bool needs_bias = epilogue == EPI_BIAS || epilogue == EPI_BIAS_GELU ||
+                          epilogue == EPI_BIAS_RESID || epilogue == EPI_BIAS_GELU_NA;
+  if (needs_bias && !bias) return set_error(ZB_ERR_INVALID, "gemm: epilogue %d needs bias", epilogue);
+  if ((epilogue == EPI_BIAS_GELU || epilogue == EPI_GELU_BWD) && !aux)
+    return set_error(ZB_ERR_INVALID, "gemm: epilogue %d needs aux", epilogue);
+  if ((epilogue == EPI_BIAS_RESID || epilogue == EPI_RESID) && !R)
+    return set_error(ZB_ERR_INVALID, "gemm: epilogue %d needs a residual", epilogue);
   const char* fenv = getenv("ZB_GEMM_CTAS");  // 1|2 pins 1-CTA / 2-CTA tiles (benchmarking)
   const int force = fenv ? atoi(fenv) : 0;
   const char* e1 = getenv("ZB_GEMM_BN");      // benchmarking overrides

@@ -18,7 +18,7 @@ if epi == 5:
     c = torch.zeros(M, N, device="cuda"); kw.update(epilogue=5, beta=1.0)
 else:
     c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16); kw.update(epilogue=epi)
-    if epi in (1, 2, 3): kw["bias"] = r(N)
+    if epi in (1, 2, 3, 7): kw["bias"] = r(N)
     if epi in (2, 4): kw["aux"] = r(M, N)
     if epi == 3: kw["resid"] = r(M, N)
 for _ in range(3):

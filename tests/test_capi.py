@@ -41,3 +41,14 @@ def test_error_path_without_gpu():
     assert rc == 1001
     assert b"bad shape" in lib.zb_last_error()
     assert lib.zb_version() == 1
+
+
+def test_gemm_rejects_missing_epilogue_operands_without_gpu():
+    lib = _lib.lib()
+    a = ctypes.c_void_p(1 << 20)  # 16-byte aligned dummies: never dereferenced
+    for epi, what in ((1, b"needs bias"), (7, b"needs bias"), (4, b"needs aux"),
+                      (6, b"needs a residual"), (9, b"unknown epilogue")):
+        rc = lib.zb_gemm_bf16(a, a, a, None, None, None, 128, 128, 64, 64, 64, 128, 0, 0, 0, 0,
+                              epi, 0.0, None)
+        assert rc == 1001, epi
+        assert what in lib.zb_last_error(), (epi, lib.zb_last_error())
