@@ -58,7 +58,24 @@ struct GemmArgs {
   int splits;      // K splits (1 unless EPI_F32 with beta == 1)
   int kb_per_split;
   int tma_epi;     // 1: TMA-store epilogue (aligned C / R / aux, beta in {0, 1})
+  int n_fastest;   // tile raster: 1 = consecutive units walk N (A panel read once)
 };
+
+// Tile raster.  M-fastest (default): the CTAs in flight share B column panels and
+// sweep all of A, which must stay L2-resident between n-columns.  N-fastest: the
+// CTAs in flight cover every n-tile of a few A row panels, so A streams from HBM
+// once and B must stay resident — chosen when A is the larger operand and does not
+// fit in L2 (LM-head dgrad / wgrad: A = the [tokens, vocab] logits gradient, 824 MB
+// at GPT-2 small, read 3-4x from HBM under the M-fastest raster).
+__device__ __forceinline__ void tile_mn(const GemmArgs& a, int tile, int& mt, int& nt) {
+  if (a.n_fastest) {
+    nt = tile % a.num_n_tiles;
+    mt = tile / a.num_n_tiles;
+  } else {
+    mt = tile % a.num_m_tiles;
+    nt = tile / a.num_m_tiles;
+  }
+}
 
 constexpr int BM = 128;
 // 2-CTA (cta_group::2) tiles are used by default for long-K GEMMs (K >= 2048) whose B
@@ -439,8 +456,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tile = unit % num_tiles;
         const int kb0 = (unit / num_tiles) * args.kb_per_split;
         const int kb1 = min(num_kb, kb0 + args.kb_per_split);
-        const int m0 = (tile % args.num_m_tiles) * BM;
-        const int n0 = (tile / args.num_m_tiles) * BN;
+        int mt, nt;
+        tile_mn(args, tile, mt, nt);
+        const int m0 = mt * BM;
+        const int n0 = nt * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
@@ -521,8 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
         const int tile = unit % num_tiles;
         const int acc = local & 1;
-        const int m0 = (tile % args.num_m_tiles) * BM;
-        const int n0 = (tile / args.num_m_tiles) * BN;
+        int mt, nt;
+        tile_mn(args, tile, mt, nt);
+        const int m0 = mt * BM;
+        const int n0 = nt * BN;
         epilogue_tma<EPI>(args, maps, stg, ebar, eph, ecnt,
                           tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN, &tfull_bar[acc],
                           (local >> 1) & 1, m0 + ew * 32, n0, half * (BN / 64),
@@ -535,8 +556,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tile = unit % num_tiles;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      const int m0 = (tile % args.num_m_tiles) * BM;
-      const int n0 = (tile / args.num_m_tiles) * BN;
+      int mt, nt;
+      tile_mn(args, tile, mt, nt);
+      const int m0 = mt * BM;
+      const int n0 = nt * BN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + ew * 32 + lane;
@@ -641,8 +664,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int tile = unit % num_tiles;
         const int kb0 = (unit / num_tiles) * args.kb_per_split;
         const int kb1 = min(num_kb, kb0 + args.kb_per_split);
-        const int m0 = (tile % args.num_m_tiles) * 256 + (int)rank * 128;
-        const int n0 = (tile / args.num_m_tiles) * BN + (int)rank * (BN / 2);
+        int mt, nt;
+        tile_mn(args, tile, mt, nt);
+        const int m0 = mt * 256 + (int)rank * 128;
+        const int n0 = nt * BN + (int)rank * (BN / 2);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           // Only the leader arrives (with both CTAs' bytes).  The follower's TMA
@@ -722,8 +747,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int unit = cluster; unit < num_units; unit += nclusters, ++local) {
         const int tile = unit % num_tiles;
         const int acc = local & 1;
-        const int m0 = (tile % args.num_m_tiles) * 256 + (int)rank * 128;
-        const int n0 = (tile / args.num_m_tiles) * BN;
+        int mt, nt;
+        tile_mn(args, tile, mt, nt);
+        const int m0 = mt * 256 + (int)rank * 128;
+        const int n0 = nt * BN;
         epilogue_tma<EPI>(args, maps, stg, ebar, eph, ecnt,
                           tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN, &tfull_bar[acc],
                           (local >> 1) & 1, m0 + ew * 32, n0, half * (BN / 64),
@@ -742,8 +769,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int tile = unit % num_tiles;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      const int m0 = (tile % args.num_m_tiles) * 256 + (int)rank * 128;
-      const int n0 = (tile / args.num_m_tiles) * BN;
+      int mt, nt;
+      tile_mn(args, tile, mt, nt);
+      const int m0 = mt * 256 + (int)rank * 128;
+      const int n0 = nt * BN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + ew * 32 + lane;
@@ -1080,6 +1109,12 @@ static int launch_choice(const GemmCall& g, const GemmChoice& ch, void* C, void*
   args.ldc = g.ldc; args.ldr = g.ldr; args.ldaux = g.ldaux;
   args.beta = g.beta;
   args.splits = ch.splits;
+  {
+    const uint64_t a_bytes = (uint64_t)g.M * g.K * 2, b_bytes = (uint64_t)g.N * g.K * 2;
+    const char* re = getenv("ZB_GEMM_RASTER");  // 0|1 pins the raster (benchmarking)
+    const int raster = re ? atoi(re) : -1;
+    args.n_fastest = raster >= 0 ? raster : (a_bytes > b_bytes && a_bytes > (64ull << 20));
+  }
   const int epilogue = g.epilogue;
   {
     const int celem = (epilogue == EPI_F32) ? 4 : 8;  // elements per 16 bytes
