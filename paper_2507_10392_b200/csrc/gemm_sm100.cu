@@ -22,6 +22,16 @@
 #include "common.cuh"
 #include "zb_internal.h"
 
+#ifndef ZB_EPI_PF_BIAS
+#define ZB_EPI_PF_BIAS 1
+#endif
+#ifndef ZB_EPI_PF_TMEM
+#define ZB_EPI_PF_TMEM 0
+#endif
+#ifndef ZB_GEMM_EXP
+#define ZB_GEMM_EXP 0  // 0 = product; 1/2/3 = timing experiments (separate builds)
+#endif
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -291,8 +301,29 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
       tma_load_2d(stg, tm_in, &ebar[0], n0 + cb * 32, row0);
     }
   }
+  constexpr bool BIAS = (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID ||
+                         EPI == EPI_BIAS_GELU_NA);
+  // Bias vectors of a chunk (same for every row) are loaded one chunk ahead, so the
+  // global-load latency never sits on the chunk's critical path.
+  auto load_bias = [&](int c, uint4 (&q)[4]) {
+    const int col = n0 + c * 32;
+    if (col + 32 <= args.N) {
+      const uint4* bp = reinterpret_cast<const uint4*>(args.bias + col);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q[j] = bp[j];
+    }
+  };
+  uint4 bq[4];
+  if (BIAS && ZB_EPI_PF_BIAS) load_bias(cb, bq);
   mbar_wait(tfull, tfull_parity);
   tc_fence_after();
+#if ZB_EPI_PF_TMEM
+  // Accumulator chunks software-pipelined: chunk c+1's TMEM load is in flight while
+  // chunk c is processed.
+  uint32_t r[32];
+  tmem_ld_32x32b_x32(tacc + cb * 32, r);
+  tmem_ld_wait_regs(r);
+#endif
 #pragma unroll 1
   for (int c = cb; c < ce; ++c) {
     const int k = c - cb;
@@ -304,25 +335,37 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
       mbar_arrive_expect_tx(&ebar[ns], kEpiSlot);
       tma_load_2d(stg + ns * kEpiSlot, tm_in, &ebar[ns], col0 + 32, row0);
     }
+    uint4 bn[4];
+    if (BIAS && ZB_EPI_PF_BIAS && c + 1 < ce) load_bias(c + 1, bn);
     __syncwarp();
+#if ZB_EPI_PF_TMEM
+    uint32_t rn[32];
+    if (c + 1 < ce) {
+      tmem_ld_32x32b_x32(tacc + (c + 1) * 32, rn);
+    } else {  // every TMEM read of this accumulator has retired
+      tc_fence_before();
+      __syncwarp();
+      release();
+    }
+#else
     uint32_t r[32];
     tmem_ld_32x32b_x32(tacc + c * 32, r);
-    tmem_ld_wait();
+    tmem_ld_wait_regs(r);
     if (c + 1 == ce) {
       tc_fence_before();
       __syncwarp();
       release();
     }
+#endif
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-    if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID ||
-        EPI == EPI_BIAS_GELU_NA) {
+    if (BIAS) {
       if (col0 + 32 <= args.N) {
         const uint4* bp = reinterpret_cast<const uint4*>(args.bias + col0);
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {
-          const uint4 q = bp[j / 8];
+          const uint4 q = ZB_EPI_PF_BIAS ? bq[j / 8] : bp[j / 8];
           float2 f0 = unpack_bf16(q.x), f1 = unpack_bf16(q.y), f2 = unpack_bf16(q.z),
                  f3 = unpack_bf16(q.w);
           v[j] += f0.x; v[j + 1] += f0.y; v[j + 2] += f1.x; v[j + 3] += f1.y;
@@ -388,10 +431,23 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
         tma_store_2d(maps.aux, stg, col0, row0);
         tma_store_2d(maps.C, stg + kEpiSlot, col0, row0);
       } else {
+#if ZB_GEMM_EXP != 1  // experiment 1: no output stores
         tma_store_2d(maps.C, slot, col0, row0);
+#endif
       }
       bulk_commit();
     }
+    if (BIAS && ZB_EPI_PF_BIAS) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bq[j] = bn[j];
+    }
+#if ZB_EPI_PF_TMEM
+    if (c + 1 < ce) {
+      tmem_ld_wait_regs(rn);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r[j] = rn[j];
+    }
+#endif
   }
 }
 
@@ -462,6 +518,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n0 = nt * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
+#if ZB_GEMM_EXP == 3  // experiment: no operand loads (time without TMA traffic)
+          mbar_arrive(&full_bar[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+#endif
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           uint8_t* a_dst = smA + stage * Cfg::A_BYTES;
           uint8_t* b_dst = smB + stage * Cfg::B_BYTES;
@@ -516,7 +580,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                    : umma_desc_sw128(a_addr + k * 32, 16, 1024);
             uint64_t b_desc = B_MN ? umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024)
                                    : umma_desc_sw128(b_addr + k * 32, 16, 1024);
+#if ZB_GEMM_EXP != 2  // experiment 2: no MMAs (time without tensor work)
             mma_bf16_ss(d_tmem, a_desc, b_desc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+#endif
           }
           mma_commit(&empty_bar[stage]);  // smem slot free once these MMAs retire
           if (++stage == S) {
