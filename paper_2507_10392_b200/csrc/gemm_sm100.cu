@@ -8,9 +8,9 @@
 // dgrad (B MN-major) and wgrad (A and B MN-major) run through the same pipeline
 // without any transpose pass.
 //
-// Roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread),
-// warp 2 = TMEM allocator, warps 4..11 = epilogue (TMEM -> registers -> global;
-// two warps per TMEM lane quarter, each draining half of the tile's columns).
+// Roles (128 + 32 * kEpiWarps threads): warp 0 = TMA producer, warp 1 = MMA issuer (one
+// thread), warp 2 = TMEM allocator, warps 4.. = epilogue (TMEM -> registers -> global;
+// kEpiWarps / 4 warps per TMEM lane quarter, each draining a run of the tile's columns).
 // Work units are (tile, K-split); with split-K (fp32-accumulate epilogue only)
 // partial tiles are combined with vectorised fp32 reductions (red.global.add.v4).
 // Pipelines: S-stage smem ring (full/empty mbarriers), 2-deep TMEM accumulator
@@ -93,17 +93,29 @@ constexpr int BM = 128;
 // K-major, B MN-major) measured faster on 1-CTA tiles (profiles/r01_gemm_1cta_vs_2cta.txt).
 constexpr bool kPairTilesDefault = true;
 constexpr int BK = 64;
-constexpr int kThreads = 384;
-constexpr int kEpiWarps = 8;
+#ifndef ZB_EPI_WARPS
+#define ZB_EPI_WARPS 8
+#endif
+// Epilogue warps: kEpiWarps / 4 per TMEM lane quarter, each draining a contiguous run
+// of the tile's 32-column chunks (the K = 768 GEMMs of the step are bound by the
+// per-chunk epilogue chain, so more warps per quarter = more chains in flight).
+constexpr int kEpiWarps = ZB_EPI_WARPS;
+static_assert(kEpiWarps % 4 == 0, "epilogue warps come in lane-quarter groups");
+constexpr int kEpiParts = kEpiWarps / 4;
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kSmemMax = 232448;  // max dynamic shared memory per block (227 KB)
+// Chunk range [cb, ce) of epilogue part p for a tile of `nch` 32-column chunks.
+__host__ __device__ constexpr int epi_cb(int p, int nch) { return p * nch / kEpiParts; }
 
 template <int BN>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 192 ? 4 : 6);
+  static constexpr int EPI_BYTES = kEpiWarps * 4096;  // per-epilogue-warp TMA staging
+  static constexpr int FIT = (kSmemMax - 1536 - EPI_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = FIT < 8 ? FIT : 8;
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;  // two accumulators, pow2 alloc
-  static constexpr int EPI_BYTES = 8 * 4096;  // per-epilogue-warp TMA staging
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
@@ -596,7 +608,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = (warp - 4) & 3;     // TMEM lane quarter this warp may access
-    const int half = (warp - 4) >> 2;  // which half of the tile's columns it drains
+    const int part = (warp - 4) >> 2;  // which run of the tile's column chunks it drains
+    const int cb = epi_cb(part, BN / 32), ce = epi_cb(part + 1, BN / 32);
     int local = 0;
     if (args.tma_epi) {
       const EpiMaps maps{&tmC, &tmAux, &tmR};
@@ -612,8 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n0 = nt * BN;
         epilogue_tma<EPI>(args, maps, stg, ebar, eph, ecnt,
                           tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN, &tfull_bar[acc],
-                          (local >> 1) & 1, m0 + ew * 32, n0, half * (BN / 64),
-                          (half + 1) * (BN / 64), lane,
+                          (local >> 1) & 1, m0 + ew * 32, n0, cb, ce, lane,
                           [&] { if (lane == 0) mbar_arrive(&tempty_bar[acc]); });
       }
       if (lane == 0) bulk_wait_all();
@@ -631,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = m0 + ew * 32 + lane;
       const bool row_ok = row < args.M;
 #pragma unroll 1
-      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+      for (int c = cb; c < ce; ++c) {
         __syncwarp();
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
@@ -663,9 +675,10 @@ struct Gemm2Cfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 6 : (BN == 192 ? 6 : 8);
+  static constexpr int EPI_BYTES = kEpiWarps * 4096;
+  static constexpr int FIT = (kSmemMax - 1536 - EPI_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = FIT < 8 ? FIT : 8;
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
-  static constexpr int EPI_BYTES = 8 * 4096;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
 };
 
@@ -803,7 +816,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = (warp - 4) & 3;
-    const int half = (warp - 4) >> 2;
+    const int part = (warp - 4) >> 2;
+    const int cb = epi_cb(part, BN / 32), ce = epi_cb(part + 1, BN / 32);
     int local = 0;
     if (args.tma_epi) {
       const EpiMaps maps{&tmC, &tmAux, &tmR};
@@ -819,8 +833,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int n0 = nt * BN;
         epilogue_tma<EPI>(args, maps, stg, ebar, eph, ecnt,
                           tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN, &tfull_bar[acc],
-                          (local >> 1) & 1, m0 + ew * 32, n0, half * (BN / 64),
-                          (half + 1) * (BN / 64), lane, [&] {
+                          (local >> 1) & 1, m0 + ew * 32, n0, cb, ce, lane, [&] {
                             if (lane == 0) {
                               if (leader)
                                 mbar_arrive(&tempty_bar[acc]);
@@ -844,7 +857,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int row = m0 + ew * 32 + lane;
       const bool row_ok = row < args.M;
 #pragma unroll 1
-      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+      for (int c = cb; c < ce; ++c) {
         __syncwarp();
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);

@@ -23,6 +23,7 @@ Activation layout: token-major [tokens, d] bf16; a microbatch slice of
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Tuple
 
@@ -187,6 +188,48 @@ def alloc_bwd_scratch(cfg: ModelConfig, n_tok: int, device) -> BwdScratch:
                                 if cfg.head_dim == 64 else None))
 
 
+class WgradLane:
+    """Weight-gradient GEMMs of a block backward on a second CUDA stream.
+
+    In a linear layer's backward only the data gradient (dgrad) is on the critical
+    path; the weight gradient (wgrad) is read by nothing until the ministage's
+    ReduceScatter / optimizer.  Forking each wgrad off the compute stream (after the
+    producer of its operands) lets its CTAs fill the SMs the dgrad chain leaves idle
+    (wave tails, small HBM-bound kernels).  ``join`` at the end of the block makes
+    the compute stream wait for every forked GEMM before the block's buffers are
+    reused (the next block's recompute overwrites them).  CPU tensors (tests' torch
+    twin) and ZB_WGRAD_LANE=0 run everything inline."""
+
+    def __init__(self):
+        self.stream = None
+        self.pending = False
+        self.enabled = os.environ.get("ZB_WGRAD_LANE", "1") != "0"
+
+    def fork(self, t: torch.Tensor):
+        """Context for one wgrad launch, ordered after the compute stream's work so far."""
+        if not (self.enabled and t.is_cuda):
+            return _Inline()
+        if self.stream is None:
+            self.stream = torch.cuda.Stream(device=t.device)
+        main = torch.cuda.current_stream(t.device)
+        self.stream.wait_stream(main)
+        self.pending = True
+        return torch.cuda.stream(self.stream)
+
+    def join(self, t: torch.Tensor) -> None:
+        if self.pending:
+            torch.cuda.current_stream(t.device).wait_stream(self.stream)
+            self.pending = False
+
+
+class _Inline:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 class GptOps:
     """Composes one rank's transformer math out of kernel calls."""
 
@@ -195,6 +238,7 @@ class GptOps:
             raise NotImplementedError(f"model family {cfg.family!r} is not wired yet")
         self.cfg, self.ops = cfg, ops
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
+        self.wlane = WgradLane()
 
     def layer_fwd(self, p: Dict[str, torch.Tensor], x: torch.Tensor, out: torch.Tensor,
                   a: LayerActs, n_tok: int, need_out: bool = True) -> None:
@@ -228,27 +272,36 @@ class GptOps:
         o, cfg = self.ops, self.cfg
         n_seq = n_tok // cfg.seq_len
         n = n_tok
+        w = self.wlane  # weight grads off the critical path (operands are not rewritten
+        #                  before the join at the end of the block)
         # MLP: out = x_mid + g W2^T + b2
-        o.gemm(dy, a.g[:n], gr["fc2_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        with w.fork(dy):
+            o.gemm(dy, a.g[:n], gr["fc2_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         # fc2 / proj bias grads: column sums of dy / dx_mid, folded into LN2's backward
         o.gemm(dy, p["fc2_w"], a.u[:n], b_t=True, epilogue=EPI_GELU_BWD, aux=a.u[:n])  # du (in place)
-        o.gemm(a.u[:n], a.h2[:n], gr["fc1_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
-        o.bias_grad(a.u[:n], gr["fc1_b"])
+        with w.fork(dy):
+            o.gemm(a.u[:n], a.h2[:n], gr["fc1_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+            o.bias_grad(a.u[:n], gr["fc1_b"])
         o.gemm(a.u[:n], p["fc1_w"], s.dh[:n], b_t=True)
         o.layernorm_bwd(s.dh[:n], a.x_mid[:n], p["ln2_w"], a.mean2[:n], a.rstd2[:n], s.dx_mid[:n],
                         gr["ln2_w"], gr["ln2_b"], dx_accum=dy, db_accum=gr["fc2_b"],
                         db_out=gr["proj_b"])
         # attention: x_mid = x + attn W_o^T + b_o
-        o.gemm(s.dx_mid[:n], a.attn[:n], gr["proj_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        with w.fork(dy):
+            o.gemm(s.dx_mid[:n], a.attn[:n], gr["proj_w"], a_t=True, b_t=True, epilogue=EPI_F32,
+                   beta=1.0)
         o.gemm(s.dx_mid[:n], p["proj_w"], s.da[:n], b_t=True)
         o.attn_bwd(a.qkv[:n], a.attn[:n], s.da[:n], a.lse[:n_seq], s.dqkv[:n],
                    s.dq_accum[:n] if s.dq_accum is not None else None,
                    s.delta[:n_seq], n_seq, cfg.seq_len, cfg.n_head, cfg.head_dim, self.scale)
-        o.gemm(s.dqkv[:n], a.h1[:n], gr["qkv_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
-        o.bias_grad(s.dqkv[:n], gr["qkv_b"])
+        with w.fork(dy):
+            o.gemm(s.dqkv[:n], a.h1[:n], gr["qkv_w"], a_t=True, b_t=True, epilogue=EPI_F32,
+                   beta=1.0)
+            o.bias_grad(s.dqkv[:n], gr["qkv_b"])
         o.gemm(s.dqkv[:n], p["qkv_w"], s.dh[:n], b_t=True)
         o.layernorm_bwd(s.dh[:n], x, p["ln1_w"], a.mean1[:n], a.rstd1[:n], dx, gr["ln1_w"],
                         gr["ln1_b"], dx_accum=s.dx_mid[:n])
+        w.join(dy)
 
     def embed_fwd(self, p, tokens, out, n_tok):
         self.ops.embedding_fwd(tokens[:n_tok], p["wte"], p["wpe"], out, self.cfg.seq_len)
@@ -265,6 +318,7 @@ class GptOps:
         o.layernorm_fwd(x, p["lnf_w"], p["lnf_b"], hf[:n], mean[:n], rstd[:n])
         o.gemm(hf[:n], p["head_w"], logits[:n])
         o.xent_fwd_bwd(logits[:n], labels[:n], loss_sum, logits[:n], scale)
+        # (LM-head wgrad inline: forking it measured neutral; both GEMMs fill the GPU)
         o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         o.gemm(logits[:n], p["head_w"], dhf[:n], b_t=True)
         o.layernorm_bwd(dhf[:n], x, p["lnf_w"], mean[:n], rstd[:n], dx, gr["lnf_w"], gr["lnf_b"])
@@ -279,6 +333,7 @@ class LlamaOps:
     def __init__(self, cfg: ModelConfig, ops):
         self.cfg, self.ops = cfg, ops
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
+        self.wlane = WgradLane()
 
     def layer_fwd(self, p, x, out, a: LlamaActs, n_tok: int, need_out: bool = True) -> None:
         o, cfg = self.ops, self.cfg
@@ -300,23 +355,31 @@ class LlamaOps:
         o, cfg = self.ops, self.cfg
         n = n_tok
         n_seq = n // cfg.seq_len
+        w = self.wlane  # see GptOps.layer_bwd
+        # down-proj wgrad stays inline: its dgrad overwrites the operand m in place
         o.gemm(dy, a.m[:n], gr["down_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         o.gemm(dy, p["down_w"], a.m[:n], b_t=True)                 # dm (m no longer needed)
         o.swiglu_bwd(a.gu[:n], a.m[:n], a.gu[:n])                  # d[gate|up] in place
-        o.gemm(a.gu[:n], a.h2[:n], gr["gu_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        with w.fork(dy):
+            o.gemm(a.gu[:n], a.h2[:n], gr["gu_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         o.gemm(a.gu[:n], p["gu_w"], s.dh[:n], b_t=True)
         o.rmsnorm_bwd(s.dh[:n], a.x_mid[:n], p["mlp_norm"], a.rstd2[:n], s.dx_mid[:n],
                       gr["mlp_norm"], dx_accum=dy)
-        o.gemm(s.dx_mid[:n], a.attn[:n], gr["o_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        with w.fork(dy):
+            o.gemm(s.dx_mid[:n], a.attn[:n], gr["o_w"], a_t=True, b_t=True, epilogue=EPI_F32,
+                   beta=1.0)
         o.gemm(s.dx_mid[:n], p["o_w"], s.da[:n], b_t=True)
         o.attn_bwd(a.qkv[:n], a.attn[:n], s.da[:n], a.lse[:n_seq], s.dqkv[:n],
                    s.dq_accum[:n] if s.dq_accum is not None else None,
                    s.delta[:n_seq], n_seq, cfg.seq_len, cfg.n_head, cfg.head_dim, self.scale)
         o.rope(s.dqkv[:n], cfg.seq_len, cfg.n_head, cfg.head_dim, self.ROPE_THETA, inverse=True)
-        o.gemm(s.dqkv[:n], a.h1[:n], gr["qkv_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        with w.fork(dy):
+            o.gemm(s.dqkv[:n], a.h1[:n], gr["qkv_w"], a_t=True, b_t=True, epilogue=EPI_F32,
+                   beta=1.0)
         o.gemm(s.dqkv[:n], p["qkv_w"], s.dh[:n], b_t=True)
         o.rmsnorm_bwd(s.dh[:n], x, p["attn_norm"], a.rstd1[:n], dx, gr["attn_norm"],
                       dx_accum=s.dx_mid[:n])
+        w.join(dy)
 
     def embed_fwd(self, p, tokens, out, n_tok):
         self.ops.embedding_fwd(tokens[:n_tok], p["wte"], None, out, self.cfg.seq_len)
@@ -331,6 +394,7 @@ class LlamaOps:
         o.rmsnorm_fwd(x, p["norm_w"], hf[:n], rstd[:n])
         o.gemm(hf[:n], p["head_w"], logits[:n])
         o.xent_fwd_bwd(logits[:n], labels[:n], loss_sum, logits[:n], scale)
+        # (LM-head wgrad inline: forking it measured neutral; both GEMMs fill the GPU)
         o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
         o.gemm(logits[:n], p["head_w"], dhf[:n], b_t=True)
         o.rmsnorm_bwd(dhf[:n], x, p["norm_w"], rstd[:n], dx, gr["norm_w"])
