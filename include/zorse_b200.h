@@ -86,6 +86,13 @@ int zb_layernorm_bwd(const void* dy, const void* x, const void* w, const void* m
 int zb_layernorm_bwd_ex(const void* dy, const void* x, const void* w, const void* mean,
                         const void* rstd, void* dx, void* dw, void* db, const void* dres,
                         void* db_res, void* db_out, int rows, int d, zb_stream_t stream);
+/* zb_layernorm_bwd_ex split in its two launches: phase 1 = dx only, phase 2 = the dw / db
+ * (and db_res / db_out) column pass only, which reads dx — the caller orders phase 2 after
+ * phase 1 (e.g. on a second stream behind an event); phase 0 = both. */
+int zb_layernorm_bwd_phase(const void* dy, const void* x, const void* w, const void* mean,
+                           const void* rstd, void* dx, void* dw, void* db, const void* dres,
+                           void* db_res, void* db_out, int rows, int d, int phase,
+                           zb_stream_t stream);
 /* out[t] = wte[tok[t]] + wpe[t % seq]  (tok: int32; wpe may be NULL). */
 int zb_embedding_fwd(const void* tok, const void* wte, const void* wpe, void* out, int rows, int d,
                      int seq, zb_stream_t stream);

@@ -24,6 +24,7 @@ SIGNATURES = {
     "zb_layernorm_fwd": [P, P, P, P, P, P, P, I, I, F, P],
     "zb_layernorm_bwd": [P, P, P, P, P, P, P, P, P, I, I, P],
     "zb_layernorm_bwd_ex": [P, P, P, P, P, P, P, P, P, P, P, I, I, P],
+    "zb_layernorm_bwd_phase": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, P],
     "zb_embedding_fwd": [P, P, P, P, I, I, I, P],
     "zb_embedding_bwd": [P, P, P, P, I, I, I, P],
     "zb_xent_fwd_bwd": [P, P, P, P, I, I, I, F, P],

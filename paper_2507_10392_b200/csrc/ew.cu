@@ -606,29 +606,35 @@ extern "C" int zb_layernorm_fwd(const void* x, const void* w, const void* b, voi
   return launched("layernorm_fwd");
 }
 
+// phase: 0 = both launches, 1 = the dx kernel only, 2 = the dw / db column pass only
+// (split variant; lets the caller run the column pass on another stream).
 static int layernorm_bwd_impl(const void* dy, const void* x, const void* w, const void* mean,
                               const void* rstd, void* dx, void* dw, void* db, const void* dres,
-                              void* db_res, void* db_out, int rows, int d, cudaStream_t s) {
+                              void* db_res, void* db_out, int rows, int d, cudaStream_t s,
+                              int phase = 0) {
   if (d % 8) return set_error(ZB_ERR_INVALID, "layernorm: d must be a multiple of 8");
   if (d > 5120) return set_error(ZB_ERR_UNSUPPORTED, "layernorm_bwd: d > 5120");
+  if (phase < 0 || phase > 2) return set_error(ZB_ERR_INVALID, "layernorm_bwd: phase %d", phase);
   if (rows <= 0) return 0;
   const int threads = 256, per = threads / 32;
   const int vpl = (d / 8 + 31) / 32;  // column vectors per lane
   static const bool fused = getenv("ZB_LN_BWD_FUSED") != nullptr;  // A/B: single-kernel variant
-  if (!fused) {
+  if (!fused || phase != 0) {
     auto go1 = [&](auto kern) {
       launch_pdl_k(kern, dim3((rows + per - 1) / per), dim3(threads), 0, s,
                    (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w,
                    (const float*)mean, (const float*)rstd, (__nv_bfloat16*)dx,
                    (const __nv_bfloat16*)dres, rows, d);
     };
-    if (vpl <= 1) go1(layernorm_bwd_dx_kernel<1>);
+    if (phase == 2) {
+    } else if (vpl <= 1) go1(layernorm_bwd_dx_kernel<1>);
     else if (vpl <= 2) go1(layernorm_bwd_dx_kernel<2>);
     else if (vpl <= 3) go1(layernorm_bwd_dx_kernel<3>);
     else if (vpl <= 4) go1(layernorm_bwd_dx_kernel<4>);
     else if (vpl <= 7) go1(layernorm_bwd_dx_kernel<7>);
     else if (vpl <= 10) go1(layernorm_bwd_dx_kernel<10>);
     else go1(layernorm_bwd_dx_kernel<20>);
+    if (phase == 1) return launched("layernorm_bwd dx");
     const int cblocks = (d / 8 + 31) / 32;
     int rblocks = (2 * num_sms() + cblocks - 1) / cblocks;
     if (rblocks > rows / 64) rblocks = rows / 64 > 0 ? rows / 64 : 1;
@@ -687,6 +693,14 @@ extern "C" int zb_layernorm_bwd_ex(const void* dy, const void* x, const void* w,
   if (fused && (db_res || db_out))
     return set_error(ZB_ERR_UNSUPPORTED, "layernorm_bwd_ex: not with ZB_LN_BWD_FUSED");
   return layernorm_bwd_impl(dy, x, w, mean, rstd, dx, dw, db, dres, db_res, db_out, rows, d, s);
+}
+
+extern "C" int zb_layernorm_bwd_phase(const void* dy, const void* x, const void* w,
+                                      const void* mean, const void* rstd, void* dx, void* dw,
+                                      void* db, const void* dres, void* db_res, void* db_out,
+                                      int rows, int d, int phase, cudaStream_t s) {
+  return layernorm_bwd_impl(dy, x, w, mean, rstd, dx, dw, db, dres, db_res, db_out, rows, d, s,
+                            phase);
 }
 
 extern "C" int zb_embedding_fwd(const void* tok, const void* wte, const void* wpe, void* out,

@@ -93,11 +93,18 @@ def layernorm_fwd(x, w, b, y, mean, rstd, eps=1e-5):
          None, rows, d, float(eps), _stream())
 
 
-def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None, db_accum=None, db_out=None):
+def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None, db_accum=None, db_out=None,
+                  phase=0):
     """dx (+)= LN'(dy); dw, db (fp32) += parameter grads.  dx_accum: residual grad to add.
-    db_accum / db_out (fp32, optional, together): += column sums of dx_accum / of dx."""
+    db_accum / db_out (fp32, optional, together): += column sums of dx_accum / of dx.
+    phase 1 / 2: only the dx launch / only the (dw, db, db_accum, db_out) column pass."""
     _need_cuda(dy, x, w, mean, rstd, dx, dw, db, dx_accum, db_accum, db_out)
     rows, d = x.shape
+    if phase:
+        call("zb_layernorm_bwd_phase", _ptr(dy), _ptr(x), _ptr(w), _ptr(mean), _ptr(rstd),
+             _ptr(dx), _ptr(dw), _ptr(db), _ptr(dx_accum), _ptr(db_accum), _ptr(db_out), rows, d,
+             int(phase), _stream())
+        return
     if db_accum is not None or db_out is not None:
         call("zb_layernorm_bwd_ex", _ptr(dy), _ptr(x), _ptr(w), _ptr(mean), _ptr(rstd), _ptr(dx),
              _ptr(dw), _ptr(db), _ptr(dx_accum), _ptr(db_accum), _ptr(db_out), rows, d,

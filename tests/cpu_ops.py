@@ -57,17 +57,21 @@ def layernorm_fwd(x, w, b, y, mean, rstd, eps=1e-5):
     rstd.copy_(rs)
 
 
-def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None, db_accum=None, db_out=None):
+def layernorm_bwd(dy, x, w, mean, rstd, dx, dw, db, dx_accum=None, db_accum=None, db_out=None,
+                  phase=0):
     xh = (x.float() - mean[:, None]) * rstd[:, None]
-    g = dy.float() * w.float()
-    mg = g.mean(-1, keepdim=True)
-    mgx = (g * xh).mean(-1, keepdim=True)
-    out = rstd[:, None] * (g - mg - xh * mgx)
-    if dx_accum is not None:
-        out = out + dx_accum.float()
+    if phase != 2:
+        g = dy.float() * w.float()
+        mg = g.mean(-1, keepdim=True)
+        mgx = (g * xh).mean(-1, keepdim=True)
+        out = rstd[:, None] * (g - mg - xh * mgx)
+        if dx_accum is not None:
+            out = out + dx_accum.float()
+        dx.copy_(out)
+    if phase == 1:
+        return
     dw += (dy.float() * xh).sum(0)
     db += dy.float().sum(0)
-    dx.copy_(out)
     if db_accum is not None:
         db_accum += dx_accum.float().sum(0)
         db_out += dx.float().sum(0)

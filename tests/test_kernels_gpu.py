@@ -50,6 +50,18 @@ def test_layernorm_fwd_bwd(cuda, rows, d):
     assert rel(dw, wf.grad) < 1e-3 and rel(db, bf.grad) < 1e-3
     assert rel(db_res, 0.5 + dres.float().sum(0)) < 1e-3
     assert rel(db_out, -0.25 + dx.float().sum(0)) < 1e-3
+    # the same split in its two launches (zb_layernorm_bwd_phase 1 then 2)
+    dx2 = torch.empty_like(x)
+    dw2, db2 = torch.zeros(d, device="cuda"), torch.zeros(d, device="cuda")
+    db_res2, db_out2 = torch.zeros(d, device="cuda"), torch.zeros(d, device="cuda")
+    for ph in (1, 2):
+        K.layernorm_bwd(dy, x, w, mean, rstd, dx2, dw2, db2, dx_accum=dres, db_accum=db_res2,
+                        db_out=db_out2, phase=ph)
+    torch.cuda.synchronize()
+    assert torch.equal(dx2, dx)
+    assert rel(dw2, wf.grad) < 1e-3 and rel(db2, bf.grad) < 1e-3
+    assert rel(db_res2, dres.float().sum(0)) < 1e-3
+    assert rel(db_out2, dx.float().sum(0)) < 1e-3
 
 
 def test_embedding(cuda):
