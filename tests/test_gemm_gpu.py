@@ -122,3 +122,32 @@ def test_gemm_f32_store_and_accumulate(cuda, epi_path, M, N, Kd):
     K.gemm(dy, x, c2, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=1.0)
     torch.cuda.synchronize()
     _close(c2, ref, tol=1e-3)
+
+
+@pytest.mark.parametrize("raster", ["0", "1"])
+@pytest.mark.parametrize("ctas", ["1", "2"])
+@pytest.mark.parametrize("M,N,Kd,lay", [(1000, 392, 4096, "dgrad"), (640, 264, 2048, "tn"),
+                                        (2944, 384, 1024, "wgrad")])
+def test_gemm_tile_rasters(cuda, monkeypatch, raster, ctas, M, N, Kd, lay):
+    """Both tile rasters (M-fastest; N-fastest, used when A outgrows L2) and both CTA
+    modes, on ragged shapes, against torch fp32 (ZB_GEMM_RASTER / ZB_GEMM_CTAS pin them)."""
+    monkeypatch.setenv("ZB_GEMM_RASTER", raster)
+    monkeypatch.setenv("ZB_GEMM_CTAS", ctas)
+    torch.manual_seed(5)
+    if lay == "tn":
+        a, b = _rand(M, Kd), _rand(N, Kd)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        K.gemm(a, b, out)
+        ref = a.float() @ b.float().t()
+    elif lay == "dgrad":
+        a, b = _rand(M, Kd), _rand(Kd, N)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        K.gemm(a, b, out, b_t=True)
+        ref = a.float() @ b.float()
+    else:
+        a, b = _rand(Kd, M), _rand(Kd, N)
+        out = torch.full((M, N), 0.5, device="cuda")
+        K.gemm(a, b, out, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=1.0)
+        ref = 0.5 + a.float().t() @ b.float()
+    torch.cuda.synchronize()
+    _close(out, ref, tol=1e-3 if lay == "wgrad" else 2e-2)
