@@ -330,6 +330,25 @@ ZB_DEVICE void tma_load_2d_2cta(void* smem_dst, const CUtensorMap* m, uint64_t* 
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
       : "memory");
 }
+// Same, multicast: the box lands at the same smem offset in every CTA of `mask`, and
+// each destination's completion bytes go to ITS pair leader's barrier.
+ZB_DEVICE void tma_load_2d_2cta_mc(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c0,
+                                   int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "h"(mask)
+      : "memory");
+}
+// Commit the pair's MMAs to the barrier at the same smem offset in every CTA of `mask`.
+ZB_DEVICE void mma_commit_2cta_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 // Arrive on the barrier at the same smem offset in cluster CTA `cta`.
 ZB_DEVICE void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
   asm volatile(

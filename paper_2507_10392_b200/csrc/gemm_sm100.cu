@@ -682,8 +682,14 @@ struct Gemm2Cfg {
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
 };
 
-template <int BN, int A_MN, int B_MN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// MC = CTA pairs per cluster (cluster dims 2 * MC, set at launch).  MC = 2: the two pairs
+// compute the two adjacent n-tiles of one m-tile and share its A operand: each CTA loads
+// half of its 128 A rows and multicasts it to the same-rank CTA of the other pair, so A
+// crosses L2 -> SM once per cluster (25% less operand traffic per SM at BN = 256).  A
+// stage is refilled only after both pairs' MMAs released it (empty barrier count MC,
+// commits multicast to the whole cluster).
+template <int BN, int A_MN, int B_MN, int EPI, int MC>
+__global__ void __launch_bounds__(kThreads, 1)
     gemm2cta_kernel(const __grid_constant__ CUtensorMap tmA,
                     const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC,
@@ -706,19 +712,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1;        // rank within the CTA pair
+  const int pr = (int)(crank >> 1);      // pair within the cluster (MC = 2)
   const bool leader = rank == 0;
-  const int num_tiles = args.num_m_tiles * args.num_n_tiles;  // m tiles of 256 rows
+  const uint32_t lead_rank = crank & ~1u;  // this pair's leader in the cluster
+  const int nv = args.num_n_tiles / MC;  // n-tile groups (one n-tile per pair)
+  const int num_tiles = args.num_m_tiles * nv;  // m tiles of 256 rows x n-tile groups
   const int num_units = num_tiles * args.splits;
   const int num_kb = (args.K + BK - 1) / BK;
-  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int cluster = blockIdx.x / (2 * MC), nclusters = gridDim.x / (2 * MC);
+  auto coords = [&](int tile, int& mt, int& nt) {
+    int g;
+    if (args.n_fastest) {
+      g = tile % nv;
+      mt = tile / nv;
+    } else {
+      mt = tile % args.num_m_tiles;
+      g = tile / args.num_m_tiles;
+    }
+    nt = g * MC + pr;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full_bar[i], 1);   // leader's expect_tx (both CTAs' TMA bytes land here)
-      mbar_init(&empty_bar[i], 1);  // multicast MMA commit
+      mbar_init(&empty_bar[i], MC);  // one multicast MMA commit per pair
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
@@ -744,7 +765,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int kb0 = (unit / num_tiles) * args.kb_per_split;
         const int kb1 = min(num_kb, kb0 + args.kb_per_split);
         int mt, nt;
-        tile_mn(args, tile, mt, nt);
+        coords(tile, mt, nt);
         const int m0 = mt * 256 + (int)rank * 128;
         const int n0 = nt * BN + (int)rank * (BN / 2);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -757,7 +778,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t* a_dst = smA + stage * Cfg::A_BYTES;
           uint8_t* b_dst = smB + stage * Cfg::B_BYTES;
           const int k0 = kb * BK;
-          if (A_MN) {
+          if (MC == 2) {  // this CTA's half of the shared A rows, to both pairs
+            const uint16_t mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));
+            if (A_MN)
+              tma_load_2d_2cta_mc(a_dst + pr * (64 * BK * 2), &tmA, &full_bar[stage],
+                                  m0 + pr * 64, k0, mask);
+            else
+              tma_load_2d_2cta_mc(a_dst + pr * (64 * 128), &tmA, &full_bar[stage], k0,
+                                  m0 + pr * 64, mask);
+          } else if (A_MN) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
               tma_load_2d_2cta(a_dst + j * (64 * BK * 2), &tmA, &full_bar[stage], m0 + j * 64, k0);
@@ -805,13 +834,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                    : umma_desc_sw128(b_addr + k * 32, 16, 1024);
             mma_bf16_ss_2cta(d_tmem, a_desc, b_desc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          mma_commit_2cta(&empty_bar[stage]);
+          mma_commit_2cta_mask(&empty_bar[stage], (uint16_t)((1u << (2 * MC)) - 1));
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_2cta(&tfull_bar[acc]);
+        mma_commit_2cta_mask(&tfull_bar[acc], (uint16_t)(3u << lead_rank));
       }
     }
   } else if (warp >= 4) {
@@ -828,7 +857,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int tile = unit % num_tiles;
         const int acc = local & 1;
         int mt, nt;
-        tile_mn(args, tile, mt, nt);
+        coords(tile, mt, nt);
         const int m0 = mt * 256 + (int)rank * 128;
         const int n0 = nt * BN;
         epilogue_tma<EPI>(args, maps, stg, ebar, eph, ecnt,
@@ -838,7 +867,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                               if (leader)
                                 mbar_arrive(&tempty_bar[acc]);
                               else
-                                mbar_arrive_remote(&tempty_bar[acc], 0);
+                                mbar_arrive_remote(&tempty_bar[acc], lead_rank);
                             }
                           });
       }
@@ -849,7 +878,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       int mt, nt;
-      tile_mn(args, tile, mt, nt);
+      coords(tile, mt, nt);
       const int m0 = mt * 256 + (int)rank * 128;
       const int n0 = nt * BN;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -871,7 +900,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (leader)
           mbar_arrive(&tempty_bar[acc]);
         else
-          mbar_arrive_remote(&tempty_bar[acc], 0);
+          mbar_arrive_remote(&tempty_bar[acc], lead_rank);
       }
     }
   }
@@ -935,6 +964,28 @@ static cudaError_t launch_pdl(Kern kern, dim3 grid, int smem, cudaStream_t strea
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Same with a thread-block-cluster dimension (the 2-CTA kernels: 2 or 4 CTAs).
+template <typename Kern, typename... Args>
+static cudaError_t launch_pdl_cluster(Kern kern, dim3 grid, int smem, cudaStream_t stream,
+                                      int cluster_x, Args... args) {
+  static const bool off = getenv("ZB_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cluster_x;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int BN, int A_MN, int B_MN, int EPI>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm& et,
                        GemmArgs args, cudaStream_t stream) {
@@ -964,14 +1015,14 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm
 }
 
 // Co-resident 2-CTA clusters for a kernel with `smem` bytes of dynamic shared memory.
-static int max_active_pairs(const void* kern, int smem) {
+static int max_active_pairs(const void* kern, int smem, int csize = 2) {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = csize;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3(2 * (num_sms() / 2));
+  cfg.gridDim = dim3(csize * (num_sms() / csize));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.attrs = attr;
@@ -979,27 +1030,27 @@ static int max_active_pairs(const void* kern, int smem) {
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
     cudaGetLastError();
-    n = num_sms() / 2;
+    n = num_sms() / csize;
   }
-  return n < num_sms() / 2 ? n : num_sms() / 2;
+  return n < num_sms() / csize ? n : num_sms() / csize;
 }
 
 // Slots for the tile cost model (all 2-CTA configurations use ~225 KB of smem).
 static int pair_slots() {
   static int n = 0;
   if (!n) {
-    auto k = gemm2cta_kernel<256, 0, 0, EPI_BF16>;
+    auto k = gemm2cta_kernel<256, 0, 0, EPI_BF16, 1>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg<256>::SMEM_BYTES);
     n = max_active_pairs((const void*)k, Gemm2Cfg<256>::SMEM_BYTES);
   }
   return n;
 }
 
-template <int BN, int A_MN, int B_MN, int EPI>
+template <int BN, int A_MN, int B_MN, int EPI, int MC>
 static int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm& et,
                         GemmArgs args, cudaStream_t stream) {
   using Cfg = Gemm2Cfg<BN>;
-  auto kern = gemm2cta_kernel<BN, A_MN, B_MN, EPI>;
+  auto kern = gemm2cta_kernel<BN, A_MN, B_MN, EPI, MC>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -1009,37 +1060,40 @@ static int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const EpiT
   }
   args.num_m_tiles = (args.M + 255) / 256;
   args.num_n_tiles = (args.N + BN - 1) / BN;
-  const int tiles = args.num_m_tiles * args.num_n_tiles;
+  if (args.num_n_tiles % MC)
+    return set_error(ZB_ERR_INVALID, "gemm: multicast pairs need an even n-tile count");
+  const int tiles = args.num_m_tiles * (args.num_n_tiles / MC);
   const int num_kb = (args.K + BK - 1) / BK;
   // A persistent grid must be fully co-resident: not every SM pair can host a
   // cluster (GPC shapes), so ask the occupancy API instead of assuming sms / 2.
   static int max_clusters = 0;
-  if (!max_clusters) max_clusters = max_active_pairs((const void*)kern, Cfg::SMEM_BYTES);
+  if (!max_clusters)
+    max_clusters = max_active_pairs((const void*)kern, Cfg::SMEM_BYTES, 2 * MC);
   const int pairs = max_clusters;
   const int splits = (EPI == EPI_F32 && args.beta == 1.f) ? (args.splits > 0 ? args.splits : 1) : 1;
   args.kb_per_split = (num_kb + splits - 1) / splits;
   args.splits = (num_kb + args.kb_per_split - 1) / args.kb_per_split;
   const int units = tiles * args.splits;
   const int clusters = units < pairs ? units : pairs;
-  cudaError_t e = launch_pdl(kern, dim3(2 * clusters), Cfg::SMEM_BYTES, stream, ta, tb, et.c,
-                             et.aux, et.r, args);
+  cudaError_t e = launch_pdl_cluster(kern, dim3(2 * MC * clusters), Cfg::SMEM_BYTES, stream,
+                                     2 * MC, ta, tb, et.c, et.aux, et.r, args);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "gemm2cta launch");
   return 0;
 }
 
-template <int BN, int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN, int MC = 1>
 static int dispatch_epi2(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const EpiTm& et,
                          GemmArgs args, cudaStream_t s) {
   switch (epi) {
-    case EPI_BF16: return launch_gemm2<BN, A_MN, B_MN, EPI_BF16>(ta, tb, et, args, s);
-    case EPI_BIAS: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS>(ta, tb, et, args, s);
-    case EPI_BIAS_GELU: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_GELU>(ta, tb, et, args, s);
-    case EPI_BIAS_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_RESID>(ta, tb, et, args, s);
-    case EPI_GELU_BWD: return launch_gemm2<BN, A_MN, B_MN, EPI_GELU_BWD>(ta, tb, et, args, s);
-    case EPI_F32: return launch_gemm2<BN, A_MN, B_MN, EPI_F32>(ta, tb, et, args, s);
-    case EPI_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_RESID>(ta, tb, et, args, s);
-    case EPI_BIAS_GELU_NA: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_GELU_NA>(ta, tb, et, args, s);
+    case EPI_BF16: return launch_gemm2<BN, A_MN, B_MN, EPI_BF16, MC>(ta, tb, et, args, s);
+    case EPI_BIAS: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS, MC>(ta, tb, et, args, s);
+    case EPI_BIAS_GELU: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_GELU, MC>(ta, tb, et, args, s);
+    case EPI_BIAS_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_RESID, MC>(ta, tb, et, args, s);
+    case EPI_GELU_BWD: return launch_gemm2<BN, A_MN, B_MN, EPI_GELU_BWD, MC>(ta, tb, et, args, s);
+    case EPI_F32: return launch_gemm2<BN, A_MN, B_MN, EPI_F32, MC>(ta, tb, et, args, s);
+    case EPI_RESID: return launch_gemm2<BN, A_MN, B_MN, EPI_RESID, MC>(ta, tb, et, args, s);
+    case EPI_BIAS_GELU_NA: return launch_gemm2<BN, A_MN, B_MN, EPI_BIAS_GELU_NA, MC>(ta, tb, et, args, s);
   }
   return set_error(ZB_ERR_INVALID, "gemm: unknown epilogue %d", epi);
 }
@@ -1144,7 +1198,7 @@ static void tune_cache_load() {
   GemmChoice c;
   while (fscanf(f, "%d %d %d %d %d %d %d %d %d %d %d", &k.M, &k.N, &k.K, &k.a_mn, &k.b_mn, &k.epi,
                 &k.beta1, &k.ldc, &c.pair, &c.bn, &c.splits) == 11)
-    if ((c.bn == 128 || c.bn == 192 || c.bn == 256) && c.splits >= 1 && (c.pair == 0 || c.pair == 1))
+    if ((c.bn == 128 || c.bn == 192 || c.bn == 256) && c.splits >= 1 && (c.pair >= 0 && c.pair <= 2))
       g_tuned[k] = c;
   fclose(f);
 }
@@ -1171,7 +1225,8 @@ static int launch_choice(const GemmCall& g, const GemmChoice& ch, void* C, void*
   if (g.a_mn)
     rc = make_tmap(&ta, g.A, (uint64_t)g.M, (uint64_t)g.K, (uint64_t)g.lda, BK);
   else
-    rc = make_tmap(&ta, g.A, (uint64_t)g.K, (uint64_t)g.M, (uint64_t)g.lda, BM);
+    rc = make_tmap(&ta, g.A, (uint64_t)g.K, (uint64_t)g.M, (uint64_t)g.lda,
+                   pair == 2 ? BM / 2 : BM);  // multicast pairs: half the rows per CTA
   if (rc) return rc;
   if (g.b_mn)
     rc = make_tmap(&tb, g.B, (uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.ldb, BK);
@@ -1229,6 +1284,20 @@ static int launch_choice(const GemmCall& g, const GemmChoice& ch, void* C, void*
     args.tma_epi = ok ? 1 : 0;
   }
   const int key = g.a_mn * 2 + g.b_mn;
+  if (pair == 2) {
+    if (BN == 256) {
+      switch (key) {
+        case 0: return dispatch_epi2<256, 0, 0, 2>(epilogue, ta, tb, et, args, stream);
+        case 1: return dispatch_epi2<256, 0, 1, 2>(epilogue, ta, tb, et, args, stream);
+        case 3: return dispatch_epi2<256, 1, 1, 2>(epilogue, ta, tb, et, args, stream);
+      }
+    } else if (BN == 192) {
+      switch (key) {
+        case 0: return dispatch_epi2<192, 0, 0, 2>(epilogue, ta, tb, et, args, stream);
+      }
+    }
+    return set_error(ZB_ERR_INVALID, "gemm: unsupported multicast-pair layout");
+  }
   if (pair) {
     if (BN == 256) {
       switch (key) {
@@ -1286,6 +1355,9 @@ static GemmChoice tune_choice(const GemmCall& g, const GemmChoice& model, void* 
       cands.push_back({0, bn, sp});
       if (g.M >= 256 && bn != 128 && !(g.b_mn && !g.a_mn) && !(g.b_mn && bn == 192))
         cands.push_back({1, bn, sp});
+      // multicast pairs: two CTA pairs share the A tile (even n-tile count)
+      if (g.M >= 256 && bn != 128 && !(g.b_mn && bn == 192) && ((g.N + bn - 1) / bn) % 2 == 0)
+        cands.push_back({2, bn, sp});
     }
   const size_t esz = g.epilogue == EPI_F32 ? 4 : 2;
   void *c = nullptr, *x = nullptr;
@@ -1364,7 +1436,9 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
   const bool tune = !(e4 && atoi(e4) == 0) && !force && !fbn && !fsp;
   GemmCall g{A, B, bias, R, M, N, K, lda, ldb, ldc, ldr, ldaux, a_mn_major, b_mn_major,
              epilogue, beta};
-  GemmChoice ch = model_choice(M, N, K, a_mn_major, b_mn_major, epilogue, beta, force);
+  GemmChoice ch = model_choice(M, N, K, a_mn_major, b_mn_major, epilogue, beta,
+                               force == 4 ? 2 : force);
+  if (force == 4) ch.pair = 2;  // ZB_GEMM_CTAS=4: two CTA pairs sharing A (multicast)
   if (fbn == 128 || fbn == 256 || (fbn == 192 && !(ch.pair && b_mn_major))) ch.bn = fbn;
   if (fsp > 0 && epilogue == EPI_F32 && beta == 1.f) ch.splits = fsp;
   const char* how = "model";
@@ -1389,7 +1463,7 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
   }
   if (dbg)
     fprintf(stderr, "zb_gemm M=%d N=%d K=%d a_mn=%d b_mn=%d epi=%d -> %s BN=%d splits=%d (%s)\n",
-            M, N, K, a_mn_major, b_mn_major, epilogue, ch.pair ? "2cta" : "1cta", ch.bn,
+            M, N, K, a_mn_major, b_mn_major, epilogue, ch.pair == 2 ? "2x2cta" : ch.pair ? "2cta" : "1cta", ch.bn,
             ch.splits, how);
   return launch_choice(g, ch, C, aux, stream);
 }

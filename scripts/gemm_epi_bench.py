@@ -28,7 +28,7 @@ T = 8192
 shapes = [(T, 3072, 768, "tn", [0, 1, 7, 2]), (T, 2304, 768, "tn", [0, 1]), (T, 768, 3072, "tn", [0, 3]),
           (T, 768, 768, "tn", [0, 3]), (T, 3072, 768, "dgrad", [0, 4]), (T, 768, 3072, "dgrad", [0]),
           (T, 768, 50304, "dgrad", [0])]
-cfgs = [("1", "256"), ("1", "192"), ("1", "128"), ("2", "256"), ("2", "192")]
+cfgs = [("1", "256"), ("1", "192"), ("1", "128"), ("2", "256"), ("2", "192"), ("4", "256"), ("4", "192")]
 for M, N, Kd, lay, epis in shapes:
     if lay == "tn":
         a, b, kw0 = r(M, Kd), r(N, Kd), {}
@@ -46,7 +46,7 @@ for M, N, Kd, lay, epis in shapes:
             kw["resid"] = res
         row = {"shape": [M, N, Kd], "layout": lay, "epi": epi}
         for ctas, bn in cfgs:
-            if ctas == "2" and bn == "192" and lay == "dgrad":
+            if ctas in ("2", "4") and bn == "192" and lay == "dgrad":
                 continue
             os.environ["ZB_GEMM_CTAS"], os.environ["ZB_GEMM_BN"] = ctas, bn
             try:

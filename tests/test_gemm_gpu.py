@@ -151,3 +151,56 @@ def test_gemm_tile_rasters(cuda, monkeypatch, raster, ctas, M, N, Kd, lay):
         ref = 0.5 + a.float().t() @ b.float()
     torch.cuda.synchronize()
     _close(out, ref, tol=1e-3 if lay == "wgrad" else 2e-2)
+
+
+@pytest.mark.parametrize("bn", ["256", "192"])
+@pytest.mark.parametrize("M,N,Kd,lay,epi", [(512, 512, 256, "tn", 0), (1000, 768, 3072, "tn", 3),
+                                            (8192, 3072, 768, "tn", 7), (1024, 1024, 2048, "dgrad", 0),
+                                            (2304, 1024, 4096, "wgrad", 5), (768, 1536, 768, "tn", 2)])
+def test_gemm_multicast_pairs(cuda, monkeypatch, bn, M, N, Kd, lay, epi):
+    """Two CTA pairs per cluster sharing the A tile through TMA multicast
+    (ZB_GEMM_CTAS=4), every layout and the epilogue families, vs torch fp32."""
+    n_tiles = (N + int(bn) - 1) // int(bn)
+    if n_tiles % 2 or (lay != "tn" and bn == "192"):
+        pytest.skip("multicast pairs need an even n-tile count (MN-major B: BN 256)")
+    monkeypatch.setenv("ZB_GEMM_CTAS", "4")
+    monkeypatch.setenv("ZB_GEMM_BN", bn)
+    torch.manual_seed(7)
+    bias = _rand(N, scale=0.5)
+    if lay == "tn":
+        a, b = _rand(M, Kd, scale=0.5), _rand(N, Kd, scale=0.5)
+        ref = a.float() @ b.float().t()
+        kw = {}
+    elif lay == "dgrad":
+        a, b = _rand(M, Kd, scale=0.5), _rand(Kd, N, scale=0.5)
+        ref = a.float() @ b.float()
+        kw = {"b_t": True}
+    else:
+        a, b = _rand(Kd, M, scale=0.5), _rand(Kd, N, scale=0.5)
+        ref = a.float().t() @ b.float()
+        kw = {"a_t": True, "b_t": True}
+    if epi == 5:
+        out = torch.full((M, N), 0.25, device="cuda")
+        K.gemm(a, b, out, epilogue=5, beta=1.0, **kw)
+        torch.cuda.synchronize()
+        _close(out, ref + 0.25, tol=1e-3)
+        return
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    if epi == 0:
+        K.gemm(a, b, out, **kw)
+        exp = ref
+    elif epi == 3:
+        r = _rand(M, N)
+        K.gemm(a, b, out, epilogue=3, bias=bias, resid=r, **kw)
+        exp = ref + bias.float() + r.float()
+    elif epi == 7:
+        K.gemm(a, b, out, epilogue=7, bias=bias, **kw)
+        exp = _gelu(ref + bias.float())
+    else:  # 2: pre-activation to aux, GELU to out
+        aux = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        K.gemm(a, b, out, epilogue=2, bias=bias, aux=aux, **kw)
+        torch.cuda.synchronize()
+        _close(aux, ref + bias.float())
+        exp = _gelu(ref + bias.float())
+    torch.cuda.synchronize()
+    _close(out, exp)
