@@ -2,7 +2,7 @@
 # Single-GPU round-end evidence (round 1, second session): tests, smoke, bench (both
 # arms), ncu launch list of the bench command, GEMM DRAM traffic, full ncu captures of
 # the top kernels, in-step breakdown.
-O=gpurun_out/r1b_final1
+O=gpurun_out/r1b_final1b
 mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -q -x > $O/gpu_tests.log 2>&1; echo "tests rc=$?" >> $O/summary.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/summary.log
