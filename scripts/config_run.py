@@ -3,6 +3,7 @@ product path for a few steps; report tokens/s and loss.  torchrun, 1 process/GPU
 
   torchrun --nproc-per-node 4 scripts/config_run.py xl_1+3      (config 3 shape on 4 GPUs)
   torchrun --nproc-per-node 4 scripts/config_run.py llama7b_2x2 (config 4: 1F1B, seq 2048)
+  torchrun --nproc-per-node 4 scripts/config_run.py llama13b_plan4 (config 5: planner layout)
 """
 import json
 import os
@@ -35,6 +36,10 @@ RUNS = {
     "llama7b_4x2": dict(cfg=E.LLAMA_7B, nodes=E.CONFIG_NODES["llama7b-4x2"],
                         groups=[[f"n{i}-0", f"n{i}-1"] for i in range(4)], gb=32, M=8,
                         counts=[1, 1, 1, 1], strategy="pp-zero3", schedule="1f1b"),
+    # config 5: Llama-13B, planner-chosen layout (plan_training) on an emulated-kinds node
+    # (half full-speed b200, half half-speed b200h; 8 GPUs -> 4)
+    "llama13b_plan4": dict(cfg=E.LLAMA_13B, nodes=[("n0", ["b200", "b200", "b200h", "b200h"])],
+                           gb=16, planner=True, schedule="gpipe"),
 }
 
 
@@ -51,9 +56,15 @@ def main():
     rt = P.fit_runtime_model(prof)
     ctx = P.CostContext(graph=P.build_cluster_graph(prof), runtime=rt, model=cfg.model_spec(),
                         workload=P.WorkloadSpec(r["gb"], cfg.seq_len))
-    plan = P.build_plan(ctx, prof, P.make_partition(ctx.graph, r["groups"]), r["M"], r["counts"],
-                        P.Strategy(r["strategy"]), P.cluster_fingerprint(prof), "transformer")
-    P.attach_routing(plan, rt, "transformer")
+    if r.get("planner"):   # the reference's full search picks stages, shares and M
+        plan, _ = P.plan_training(prof, ctx.model, ctx.workload, rt)
+        r["strategy"] = plan.strategy.value
+    else:
+        plan = P.build_plan(ctx, prof, P.make_partition(ctx.graph, r["groups"]), r["M"],
+                            r["counts"], P.Strategy(r["strategy"]), P.cluster_fingerprint(prof),
+                            "transformer")
+    if plan.routing is None:
+        P.attach_routing(plan, rt, "transformer")
     t0 = time.time()
     coll = os.environ.get("ZB_COLLECTIVES", "peer")
     tr = ZorseTrainer(plan, ctx, cfg, world_rank=rank, world_size=world, schedule=r["schedule"],
