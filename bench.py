@@ -317,7 +317,8 @@ def run_ours(args):
     loss = trainer.loss_device().item()
 
     # ---------------- e2e through the public API (pinned host batch, loss D2H) ----
-    e2e_steps = max(2, min(args.steps, 5))
+    # as many steps as the device-timed region, so both see the same clock / power state
+    e2e_steps = max(2, args.steps)
     barrier()
     torch.cuda.synchronize()
     e0 = time.perf_counter()
