@@ -37,6 +37,11 @@ def _rel(a, b):
     (E.ModelConfig("llama-tiny", "llama", 2, 512, 4, 4096, 256, d_ff=1376), 4, 2, [2], "zorse", False),
     (E.ModelConfig("llama-hd128", "llama", 2, 1024, 8, 4096, 512, d_ff=2752), 2, 1, [1], "pp-zero3",
      False),
+    # Llama-13B widths (BASELINE config 5): d 5120, 40 heads of 128, d_ff 13824.  bf16
+    # activations over K = 13824 drift further from fp32 after one update: the step-2
+    # gradient bound is the multi-GPU one (rel-L2 <= 5e-2 with cosine >= 0.998)
+    (E.ModelConfig("llama13b-width", "llama", 1, 5120, 40, 2048, 256, d_ff=13824), 2, 1, [1],
+     "zorse", False),
     # activation offload to pinned host memory (OffloadAct / LoadAct on the host stream)
     (E.TINY_GPT, 8, 4, [1], "zorse", True),
 ])
@@ -53,8 +58,15 @@ def test_training_steps_match_oracle(cuda, cfg, gb, n_mb, counts, strategy, offl
         ref_loss, ref_grads = gpt_cpu.loss_and_grads(cfg, params, b)
         gpt_cpu.adamw(params, ref_grads, state, step)
         assert abs(loss - ref_loss) / ref_loss < 1e-2, (step, loss, ref_loss)
+        wide = cfg.d_model >= 4096
         for u, g in tr.exec.captured.items():
-            assert _rel(g.cpu(), ref_grads[u]) < 3e-2, (step, u, _rel(g.cpu(), ref_grads[u]))
+            r = _rel(g.cpu(), ref_grads[u])
+            if wide and step > 1:
+                cos = torch.nn.functional.cosine_similarity(g.cpu().flatten(),
+                                                            ref_grads[u].flatten(), dim=0).item()
+                assert r < 5e-2 and cos >= 0.998, (step, u, r, cos)
+            else:
+                assert r < 3e-2, (step, u, r)
     for u, pu in tr.exec.units.items():
         err = (pu.master.cpu() - params[u]).abs().max().item()
         assert err < 5e-3, (u, err)
