@@ -22,12 +22,6 @@
 #include "common.cuh"
 #include "zb_internal.h"
 
-#ifndef ZB_EPI_PF_BIAS
-#define ZB_EPI_PF_BIAS 1
-#endif
-#ifndef ZB_EPI_PF_TMEM
-#define ZB_EPI_PF_TMEM 0
-#endif
 #ifndef ZB_GEMM_EXP
 #define ZB_GEMM_EXP 0  // 0 = product; 1/2/3 = timing experiments (separate builds)
 #endif
@@ -326,16 +320,9 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
     }
   };
   uint4 bq[4];
-  if (BIAS && ZB_EPI_PF_BIAS) load_bias(cb, bq);
+  if (BIAS) load_bias(cb, bq);
   mbar_wait(tfull, tfull_parity);
   tc_fence_after();
-#if ZB_EPI_PF_TMEM
-  // Accumulator chunks software-pipelined: chunk c+1's TMEM load is in flight while
-  // chunk c is processed.
-  uint32_t r[32];
-  tmem_ld_32x32b_x32(tacc + cb * 32, r);
-  tmem_ld_wait_regs(r);
-#endif
 #pragma unroll 1
   for (int c = cb; c < ce; ++c) {
     const int k = c - cb;
@@ -348,18 +335,8 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
       tma_load_2d(stg + ns * kEpiSlot, tm_in, &ebar[ns], col0 + 32, row0);
     }
     uint4 bn[4];
-    if (BIAS && ZB_EPI_PF_BIAS && c + 1 < ce) load_bias(c + 1, bn);
+    if (BIAS && c + 1 < ce) load_bias(c + 1, bn);
     __syncwarp();
-#if ZB_EPI_PF_TMEM
-    uint32_t rn[32];
-    if (c + 1 < ce) {
-      tmem_ld_32x32b_x32(tacc + (c + 1) * 32, rn);
-    } else {  // every TMEM read of this accumulator has retired
-      tc_fence_before();
-      __syncwarp();
-      release();
-    }
-#else
     uint32_t r[32];
     tmem_ld_32x32b_x32(tacc + c * 32, r);
     tmem_ld_wait_regs(r);
@@ -368,16 +345,14 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
       __syncwarp();
       release();
     }
-#endif
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
     if (BIAS) {
       if (col0 + 32 <= args.N) {
-        const uint4* bp = reinterpret_cast<const uint4*>(args.bias + col0);
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {
-          const uint4 q = ZB_EPI_PF_BIAS ? bq[j / 8] : bp[j / 8];
+          const uint4 q = bq[j / 8];
           float2 f0 = unpack_bf16(q.x), f1 = unpack_bf16(q.y), f2 = unpack_bf16(q.z),
                  f3 = unpack_bf16(q.w);
           v[j] += f0.x; v[j + 1] += f0.y; v[j + 2] += f1.x; v[j + 3] += f1.y;
@@ -449,17 +424,10 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
       }
       bulk_commit();
     }
-    if (BIAS && ZB_EPI_PF_BIAS) {
+    if (BIAS) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) bq[j] = bn[j];
     }
-#if ZB_EPI_PF_TMEM
-    if (c + 1 < ce) {
-      tmem_ld_wait_regs(rn);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) r[j] = rn[j];
-    }
-#endif
   }
 }
 
