@@ -52,3 +52,12 @@ def test_gemm_rejects_missing_epilogue_operands_without_gpu():
                               epi, 0.0, None)
         assert rc == 1001, epi
         assert what in lib.zb_last_error(), (epi, lib.zb_last_error())
+
+
+def test_layernorm_bwd_phase_validates_without_gpu():
+    lib = _lib.lib()
+    a = ctypes.c_void_p(1 << 20)
+    rc = lib.zb_layernorm_bwd_phase(a, a, a, a, a, a, a, a, None, None, None, 64, 768, 3, None)
+    assert rc == 1001 and b"phase" in lib.zb_last_error()
+    rc = lib.zb_layernorm_bwd_phase(a, a, a, a, a, a, a, a, None, None, None, 64, 770, 1, None)
+    assert rc == 1001 and b"multiple of 8" in lib.zb_last_error()
