@@ -10,14 +10,15 @@ half-speed b200h), 8 sequences per GPU on average (weak scaling; at N=8 this
 is exactly config 2: global batch 64, shares 11x4 / 5x4).
 
 ours      : the B200 executor (tcgen05 GEMMs and flash attention, AG-v and fused
-            RS-v + AdamW over NVLink peer memory; --collectives nccl for the NCCL
-            baseline) — value = whole-job tokens/s, device-timed,
+            RS-v + AdamW over NVLink peer memory) — value = whole-job tokens/s, device-timed,
             max over ranks; e2e = same metric through ZorseTrainer.step with
             the batch in pinned host memory and the loss read back each step.
 reference : the reference has no training step (hetplan is a planner +
             simulator); its CPU path for this metric is the oracle port
-            (oracle/gpt_cpu.py, fp32 torch on all host cores), timed on a
-            bounded sample of the same workload, rank 0 only.
+            (oracle/gpt_cpu.py, fp32 torch on all host cores): K timed + W warm-up
+            full training steps of 8 x 1024 tokens (the whole N=1 step; a bounded
+            sample of the 8N-sequence batch at N>1), rank 0 only, no product code
+            in the process.
 """
 
 from __future__ import annotations
@@ -48,6 +49,7 @@ def _peaks():
 
 
 def build_workload(n_gpus: int, per_gpu_batch: int = 8):
+    """GPT-2 small, one stage x an n_gpus-rank uneven ZeRO-3 DP group (product planner)."""
     from paper_2507_10392_b200 import plan as P
     from paper_2507_10392_b200.plan import emulated as E
 
@@ -151,48 +153,70 @@ class TimedOps:
         return r
 
 
-def cpu_reference_sample(cfg, seconds_budget: float = 20.0):
-    """Oracle port (fp32 torch CPU) on a bounded sample: steps of 1 sequence."""
+PER_GPU_BATCH = 8
+
+
+def oracle_steps(steps: int, warmup: int, n_seq: int):
+    """The CPU path of this metric: oracle/gpt_cpu.py (fp32 torch on every host core;
+    the reference itself has no training step) doing full training steps — forward,
+    backward and AdamW over all 124M parameters — on batches of ``n_seq`` x 1024
+    synthetic tokens of the bench workload.  Imports nothing from the product (its
+    CUDA library stays out of this process).  Returns (tokens/s, seconds per timed
+    step, threads)."""
     from oracle import gpt_cpu
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
+    cfg = gpt_cpu.GPT2_SMALL
     params = gpt_cpu.init_params(cfg, 1234)
     state = {}
-    tokens = 0
-    t0 = time.perf_counter()
-    step = 0
-    while True:
-        step += 1
-        batch = gpt_cpu.synthetic_batch(cfg, 1, step)
-        _, grads = gpt_cpu.loss_and_grads(cfg, params, batch)
+    for step in range(1, warmup + 1):
+        _, grads = gpt_cpu.loss_and_grads(cfg, params, gpt_cpu.synthetic_batch(cfg, n_seq, step))
         gpt_cpu.adamw(params, grads, state, step)
-        tokens += cfg.seq_len
-        el = time.perf_counter() - t0
-        if el > seconds_budget * 0.5 or step >= 3:
-            break
-    return {"value": tokens / el, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"{step} oracle step(s) of 1 x {cfg.seq_len} tokens (fp32 fwd+bwd+AdamW, "
-                      f"{cfg.name}) on {threads} host threads, {el:.1f} s"}
+    t0 = time.perf_counter()
+    for step in range(warmup + 1, warmup + steps + 1):
+        _, grads = gpt_cpu.loss_and_grads(cfg, params, gpt_cpu.synthetic_batch(cfg, n_seq, step))
+        gpt_cpu.adamw(params, grads, state, step)
+    el = time.perf_counter() - t0
+    return steps * n_seq * cfg.seq_len / el, el / steps, threads
+
+
+def cpu_baseline_sample():
+    """Bounded CPU sample for the GPU arm's cpu_baseline (rank 0, N=1): one warm-up
+    and one timed oracle step of the full N=1 workload (8 x 1024 tokens)."""
+    v, s_per, threads = oracle_steps(1, 1, PER_GPU_BATCH)
+    return {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"1 timed (+1 warm-up) oracle training step of {PER_GPU_BATCH} x 1024 tokens "
+                      f"(GPT-2 small fp32 fwd+bwd+AdamW, oracle/gpt_cpu.py) on {threads} host "
+                      f"threads, {s_per:.1f} s/step"}
 
 
 def run_reference(args):
-    from paper_2507_10392_b200.plan import emulated as E
-
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cfg, plan, ctx, gb = build_workload(args.gpus)
-    base = cpu_reference_sample(cfg, seconds_budget=30.0)
-    v = base["value"]
+    gb = PER_GPU_BATCH * args.gpus
+    # N=1: every step is the full workload step (8 x 1024 tokens).  N>1: the global
+    # batch is 8N sequences; each CPU step is a bounded sample of 8 of them (the
+    # tokens/s rate of a full step, which would take N times longer).
+    v, s_per, threads = oracle_steps(args.steps, args.warmup, PER_GPU_BATCH)
+    sample = (f"{args.steps} timed + {args.warmup} warm-up oracle training steps, each "
+              f"{PER_GPU_BATCH} x 1024 tokens (" +
+              ("the full N=1 step" if args.gpus == 1 else
+               f"a bounded sample of the {gb}-sequence global batch") +
+              f"), GPT-2 small fp32 fwd+bwd+AdamW (oracle/gpt_cpu.py), {threads} host threads")
     line = {
         "impl": "reference", "metric": "training tokens/sec (device-timed)", "value": v,
         "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": gb * cfg.seq_len / v * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} 1 stage x {args.gpus}-rank uneven ZeRO-3 DP",
-                   "global_batch": gb, "seq_len": cfg.seq_len, "parallelism": f"dp{args.gpus}"},
-        "cpu_baseline": dict(base, value=v),
+        "ms_per_step": s_per * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (uniform tokens, random init)",
+        "config": {"workload": f"gpt2-small-124m (L12 d768 s1024) 1 stage x {args.gpus}-rank "
+                               "uneven ZeRO-3 DP, planner shares",
+                   "model": "gpt2-small-124m", "global_batch": gb, "seq_len": 1024,
+                   "tokens_per_timed_step": PER_GPU_BATCH * 1024,
+                   "parallelism": f"dp{args.gpus}"},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": sample},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -275,8 +299,7 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg, plan, ctx, gb = build_workload(args.gpus)
-    trainer = ZorseTrainer(plan, ctx, cfg, world_rank=rank, world_size=world,
-                           collectives=args.collectives)
+    trainer = ZorseTrainer(plan, ctx, cfg, world_rank=rank, world_size=world)
     ex = trainer.exec
     batch = synthetic_batch(cfg.vocab, cfg.seq_len, gb, 1, pin=True)
     h2d = trainer.load(batch)
@@ -399,7 +422,7 @@ def run_ours(args):
                 "parallelism": f"dp{world}", "shares": [plan.groups[0].shares[d]
                                                          for d in plan.groups[0].device_ids],
                 "n_microbatches": plan.n_microbatches, "ministages": len(plan.groups[0].ministage_sizes),
-                "collectives": args.collectives if world > 1 else None,
+                "collectives": "nvlink peer memory" if world > 1 else None,
                 "l2": "per-step working set (params+grads+activations) >> 126 MB L2; no flush",
             },
             "loss": loss,
@@ -426,7 +449,7 @@ def run_ours(args):
         if coll is not None:
             line["collectives"] = coll
         if world == 1:
-            line["cpu_baseline"] = cpu_reference_sample(cfg)
+            line["cpu_baseline"] = cpu_baseline_sample()
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -441,8 +464,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--eager", action="store_true", help="no CUDA-graph capture of the step")
-    ap.add_argument("--collectives", choices=["peer", "nccl"], default="peer",
-                    help="DP-group AG-v / RS-v: NVLink peer memory (fused RS+AdamW) or NCCL")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -46,26 +46,39 @@ int zb_device_sync(void);
 int zb_gemm_bf16(const void* A, const void* B, void* C, const void* bias, const void* R,
                  void* aux, int M, int N, int K, int lda, int ldb, int ldc, int ldr, int ldaux,
                  int a_mn_major, int b_mn_major, int epilogue, float beta, zb_stream_t stream);
+/* The tile zb_gemm_bf16 picks: the committed B200 tile table (gemm_tune_cache.txt
+ * beside the library, read once, never written by the library), else the wave-
+ * quantisation cost model.  pair: 0 1-CTA 128xBN, 1 CTA pair 256xBN, 2 two pairs
+ * multicasting A; bn 128/192/256; splits = K splits (fp32 beta=1 accumulation only). */
+int zb_gemm_choice(int M, int N, int K, int a_mn_major, int b_mn_major, int epilogue,
+                   float beta, int ldc, int* pair, int* bn, int* splits, int* from_table);
+/* zb_gemm_bf16 with an explicit tile (tests, benchmarks, tuning); a negative pair /
+ * raster or a zero bn / splits keeps the default for that field.  raster: 0 M-fastest,
+ * 1 N-fastest tile order.  tma_epi = 0 forces the direct-store epilogue. */
+int zb_gemm_bf16_tile(const void* A, const void* B, void* C, const void* bias, const void* R,
+                      void* aux, int M, int N, int K, int lda, int ldb, int ldc, int ldr,
+                      int ldaux, int a_mn_major, int b_mn_major, int epilogue, float beta,
+                      int pair, int bn, int splits, int raster, int tma_epi, zb_stream_t stream);
+/* Times the cost model's tile and its neighbours on scratch outputs (inputs only read)
+ * and returns the fastest.  Synchronises `stream`; rejected during graph capture.
+ * Offline tuning only (scripts/tune_gemm.py writes the tile table). */
+int zb_gemm_tune(const void* A, const void* B, const void* bias, const void* R, void* aux,
+                 int M, int N, int K, int lda, int ldb, int ldc, int ldr, int ldaux,
+                 int a_mn_major, int b_mn_major, int epilogue, float beta, int* pair, int* bn,
+                 int* splits, zb_stream_t stream);
 
 /* ---------------------------------------------------------------- attention
  * Causal attention over the fused QKV rows ([q|k|v] per token, pitch ld),
- * n_seq sequences of S tokens, H heads of dim D (64 or 128).
+ * n_seq sequences of S tokens (S % 128 == 0), H heads of dim D (64 or 128), on
+ * 5th-gen tensor cores: S and O accumulate in TMEM, Q/K/V tiles streamed by TMA.
  * out [n_seq*S, H*D] bf16; lse [n_seq, H, S] fp32.  Same tasks as above. */
 int zb_attn_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int D, int ld,
                 float scale, zb_stream_t stream);
-/* Same contract on 5th-gen tensor cores: S and O accumulate in TMEM, K/V streamed
- * by TMA, one softmax thread per query row.  S % 128 == 0. */
-int zb_attn_fwd_tc(const void* qkv, void* out, void* lse, int n_seq, int S, int H, int D, int ld,
-                   float scale, zb_stream_t stream);
-/* Backward on 5th-gen tensor cores; contract as zb_attn_bwd, dout pitch H*D, 16-byte
- * aligned, S % 128 == 0.  With dq_accum (fp32 [n_seq*S][H*D] workspace) and D == 64:
- * one fused pass (dQ partials reduce-added into dq_accum, then scaled into dqkv);
- * otherwise two passes (dK/dV, then dQ) without atomics. */
-int zb_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const void* lse, void* dqkv,
-                   void* dq_accum, void* delta, int n_seq, int S, int H, int D, int ld,
-                   float scale, zb_stream_t stream);
-/* Writes dQ, dK, dV into the matching columns of dqkv (pitch ld).
- * delta: fp32 scratch [n_seq, H, S].  dq_accum: reserved (may be NULL). */
+/* Writes dQ, dK, dV into the matching columns of dqkv (pitch ld); dout pitch H*D,
+ * 16-byte aligned.  delta: fp32 scratch [n_seq, H, S].  With dq_accum (fp32
+ * [n_seq*S][H*D] workspace) and D == 64: one fused pass (dQ partials reduce-added into
+ * dq_accum, then scaled into dqkv); otherwise two passes (dK/dV, then dQ) without
+ * atomics. */
 int zb_attn_bwd(const void* qkv, const void* out, const void* dout, const void* lse, void* dqkv,
                 void* dq_accum, void* delta, int n_seq, int S, int H, int D, int ld, float scale,
                 zb_stream_t stream);

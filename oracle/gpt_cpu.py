@@ -14,21 +14,121 @@ parameters it reads, the math equals this full-batch step.
 from __future__ import annotations
 
 import math
-from typing import Dict
+from dataclasses import dataclass
+from typing import Dict, List, Tuple
 
 import torch
 import torch.nn.functional as F
 
-from paper_2507_10392_b200.plan.emulated import ModelConfig
-from paper_2507_10392_b200.runtime.model import (embed_layout, head_layout, init_flat,
-                                                 layer_layout)
+# This module is self-contained: it imports nothing from the product package (so
+# the CPU baseline / reference arm never loads the product's CUDA library).  The
+# flat parameter layouts and the init rule below are the executor's documented
+# contract, restated here independently; tests/test_parity_units.py
+# pins the product's initial parameters bit-exactly against init_params().
 
 
-def init_params(cfg: ModelConfig, seed: int) -> Dict[object, torch.Tensor]:
-    """fp32 flat buffers {layer index | 'embed' | 'head'} with the product's init."""
-    p = {i: init_flat(layer_layout(cfg), "layer", i, cfg, seed) for i in range(cfg.n_layer)}
-    p["embed"] = init_flat(embed_layout(cfg), "embed", 0, cfg, seed)
-    p["head"] = init_flat(head_layout(cfg), "head", 0, cfg, seed)
+@dataclass(frozen=True)
+class OracleConfig:
+    """Transformer shape (field meaning as the product's ModelConfig; any object
+    with these attributes is accepted by the functions below)."""
+
+    name: str
+    family: str
+    n_layer: int
+    d_model: int
+    n_head: int
+    vocab: int
+    seq_len: int
+    d_ff: int = 0
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_head
+
+    @property
+    def ffn(self) -> int:
+        return self.d_ff or 4 * self.d_model
+
+
+GPT2_SMALL = OracleConfig("gpt2-small-124m", "gpt", 12, 768, 12, 50304, 1024)
+
+
+def _ffn(cfg) -> int:
+    return cfg.d_ff or 4 * cfg.d_model
+
+
+def layer_entries(cfg) -> List[Tuple[str, Tuple[int, ...]]]:
+    """Named tensors of one layer's flat buffer, in flat order."""
+    d, f = cfg.d_model, _ffn(cfg)
+    if cfg.family == "llama":
+        return [("attn_norm", (d,)), ("qkv_w", (3 * d, d)), ("o_w", (d, d)),
+                ("mlp_norm", (d,)), ("gu_w", (2 * f, d)), ("down_w", (d, f))]
+    return [("ln1_w", (d,)), ("ln1_b", (d,)), ("qkv_w", (3 * d, d)), ("qkv_b", (3 * d,)),
+            ("proj_w", (d, d)), ("proj_b", (d,)), ("ln2_w", (d,)), ("ln2_b", (d,)),
+            ("fc1_w", (f, d)), ("fc1_b", (f,)), ("fc2_w", (d, f)), ("fc2_b", (d,))]
+
+
+def embed_entries(cfg):
+    if cfg.family == "llama":
+        return [("wte", (cfg.vocab, cfg.d_model))]
+    return [("wte", (cfg.vocab, cfg.d_model)), ("wpe", (cfg.seq_len, cfg.d_model))]
+
+
+def head_entries(cfg):
+    d = cfg.d_model
+    if cfg.family == "llama":
+        return [("norm_w", (d,)), ("head_w", (cfg.vocab, d))]
+    return [("lnf_w", (d,)), ("lnf_b", (d,)), ("head_w", (cfg.vocab, d))]
+
+
+def unit_entries(cfg, unit):
+    """Entries of a unit: a layer index, "embed" or "head"."""
+    if isinstance(unit, int):
+        return layer_entries(cfg)
+    return embed_entries(cfg) if unit == "embed" else head_entries(cfg)
+
+
+def spans(entries):
+    """[(name, lo, hi, shape)] flat element ranges."""
+    out, off = [], 0
+    for name, shape in entries:
+        n = math.prod(shape)
+        out.append((name, off, off + n, shape))
+        off += n
+    return out
+
+
+def views(entries, flat: torch.Tensor) -> Dict[str, torch.Tensor]:
+    return {name: flat[lo:hi].view(*shape) for name, lo, hi, shape in spans(entries)}
+
+
+def _init_unit(cfg, entries, kind: str, index: int, seed: int) -> torch.Tensor:
+    """GPT-2 init: N(0, 0.02) weights, residual projections (proj_w, fc2_w) N(0,
+    0.02/sqrt(2L)), norm weights 1, biases 0; tensor t of a unit draws from its own
+    CPU generator seeded seed*1000003 + kind*100003 + index*101 + t (kind: layer 0,
+    embed 1, head 2)."""
+    n = sum(math.prod(s) for _, s in entries)
+    flat = torch.empty(n, dtype=torch.float32)
+    resid_std = 0.02 / math.sqrt(2 * cfg.n_layer)
+    kcode = {"layer": 0, "embed": 1, "head": 2}[kind]
+    for t, (name, lo, hi, shape) in enumerate(spans(entries)):
+        v = flat[lo:hi]
+        if name.endswith("_b"):
+            v.zero_()
+        elif name.startswith("ln") or name.endswith("norm") or name == "norm_w":
+            v.fill_(1.0)
+        else:
+            g = torch.Generator()
+            g.manual_seed(seed * 1_000_003 + kcode * 100_003 + index * 101 + t)
+            v.normal_(0.0, resid_std if name in ("proj_w", "fc2_w") else 0.02, generator=g)
+    return flat
+
+
+def init_params(cfg, seed: int) -> Dict[object, torch.Tensor]:
+    """fp32 flat buffers {layer index | 'embed' | 'head'}."""
+    p = {i: _init_unit(cfg, layer_entries(cfg), "layer", i, seed) for i in range(cfg.n_layer)}
+    p["embed"] = _init_unit(cfg, embed_entries(cfg), "embed", 0, seed)
+    p["head"] = _init_unit(cfg, head_entries(cfg), "head", 0, seed)
     return p
 
 
@@ -58,7 +158,7 @@ def _rmsnorm(x, w, eps=1e-5):
 
 
 def _llama_block(cfg: ModelConfig, w, x, n_seq):
-    S, H, D, f = cfg.seq_len, cfg.n_head, cfg.head_dim, cfg.ffn
+    S, H, D, f = cfg.seq_len, cfg.n_head, cfg.d_model // cfg.n_head, _ffn(cfg)
     h = _rmsnorm(x, w["attn_norm"])
     q, k, v = (h @ w["qkv_w"].t()).view(n_seq, S, 3, H, D).unbind(2)
     q, k, v = (t.transpose(1, 2) for t in (q, k, v))
@@ -71,7 +171,7 @@ def _llama_block(cfg: ModelConfig, w, x, n_seq):
 def _block(cfg: ModelConfig, w, x, n_seq):
     if cfg.family == "llama":
         return _llama_block(cfg, w, x, n_seq)
-    S, H, D, d = cfg.seq_len, cfg.n_head, cfg.head_dim, cfg.d_model
+    S, H, D, d = cfg.seq_len, cfg.n_head, cfg.d_model // cfg.n_head, cfg.d_model
     h = F.layer_norm(x, (d,), w["ln1_w"], w["ln1_b"], 1e-5)
     qkv = h @ w["qkv_w"].t() + w["qkv_b"]
     q, k, v = qkv.view(n_seq, S, 3, H, D).unbind(2)
@@ -90,18 +190,16 @@ def loss_and_grads(cfg: ModelConfig, params: Dict[object, torch.Tensor], batch: 
     B = batch.shape[0]
     S = cfg.seq_len
     leaves = {k: v.detach().clone().requires_grad_() for k, v in params.items()}
-    views = {k: (layer_layout(cfg) if isinstance(k, int) else
-                 embed_layout(cfg) if k == "embed" else head_layout(cfg)).views(v)
-             for k, v in leaves.items()}
+    vw = {k: views(unit_entries(cfg, k), v) for k, v in leaves.items()}
     tok = batch[:, :S].reshape(-1).long()
     lab = batch[:, 1:].reshape(-1).long()
-    e = views["embed"]
+    e = vw["embed"]
     x = e["wte"][tok]
     if "wpe" in e:
         x = x + e["wpe"][torch.arange(B * S) % S]
     for i in range(cfg.n_layer):
-        x = _block(cfg, views[i], x, B)
-    h = views["head"]
+        x = _block(cfg, vw[i], x, B)
+    h = vw["head"]
     if cfg.family == "llama":
         xf = _rmsnorm(x, h["norm_w"])
     else:
@@ -137,6 +235,9 @@ def train_steps(cfg: ModelConfig, batches, seed: int = 1234, **adam_kw):
     return losses, params, grads
 
 
-def synthetic_batch(cfg: ModelConfig, global_batch: int, step: int, base_seed: int = 1234):
-    from paper_2507_10392_b200.runtime.data import synthetic_batch as _sb
-    return _sb(cfg.vocab, cfg.seq_len, global_batch, step, base_seed)
+def synthetic_batch(cfg, global_batch: int, step: int, base_seed: int = 1234):
+    """[global_batch, seq_len+1] int32 tokens ~ Uniform[0, vocab) from a CPU generator
+    seeded base_seed + step (the executor's data contract)."""
+    g = torch.Generator().manual_seed(base_seed + step)
+    return torch.randint(0, cfg.vocab, (global_batch, cfg.seq_len + 1), generator=g,
+                         dtype=torch.int32)

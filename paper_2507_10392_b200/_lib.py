@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("ZB_LIB_PATH") or os.path.join(_HERE, "libzorse_b200.so")
+LIB_PATH = os.path.join(_HERE, "libzorse_b200.so")
 
 P = ctypes.c_void_p
 I = ctypes.c_int
@@ -21,6 +21,9 @@ U64 = ctypes.c_uint64
 # name -> argtypes (all functions return int status, 0 == ok)
 SIGNATURES = {
     "zb_gemm_bf16": [P, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, F, P],
+    "zb_gemm_bf16_tile": [P, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, F, I, I, I, I, I, P],
+    "zb_gemm_choice": [I, I, I, I, I, I, F, I, P, P, P, P],
+    "zb_gemm_tune": [P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, F, P, P, P, P],
     "zb_layernorm_fwd": [P, P, P, P, P, P, P, I, I, F, P],
     "zb_layernorm_bwd": [P, P, P, P, P, P, P, P, P, I, I, P],
     "zb_layernorm_bwd_ex": [P, P, P, P, P, P, P, P, P, P, P, I, I, P],
@@ -30,9 +33,7 @@ SIGNATURES = {
     "zb_xent_fwd_bwd": [P, P, P, P, I, I, I, F, P],
     "zb_bias_grad": [P, P, I, I, I, P],
     "zb_attn_fwd": [P, P, P, I, I, I, I, I, F, P],
-    "zb_attn_fwd_tc": [P, P, P, I, I, I, I, I, F, P],
     "zb_attn_bwd": [P, P, P, P, P, P, P, I, I, I, I, I, F, P],
-    "zb_attn_bwd_tc": [P, P, P, P, P, P, P, I, I, I, I, I, F, P],
     "zb_adamw_shard": [P, P, P, P, P, P, I64, F, F, F, F, F, F, I, P],
     "zb_adamw_shard_dstep": [P, P, P, P, P, P, I64, F, F, F, F, F, F, P, P],
     "zb_step_increment": [P, P],

@@ -894,15 +894,14 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
                void* dq_accum, void* delta, int n_seq, int S, int H, int ld, float scale,
                cudaStream_t s) {
   const int Tn = n_seq * S;
-  static const bool two_pass = getenv("ZB_ATTN_BWD_TWO_PASS") != nullptr;  // A/B
-  const bool fused = D == 64 && dq_accum && !two_pass;
+  const bool fused = D == 64 && dq_accum;
   {
     const int per_cta = 256 / (D / 8);
     cudaError_t e = launch_pdl_k(delta_zero_kernel<D>, dim3((Tn * H + per_cta - 1) / per_cta),
                                  dim3(256), 0, s, (const __nv_bfloat16*)out,
                                  (const __nv_bfloat16*)dout, (float*)delta,
                                  fused ? (float*)dq_accum : (float*)nullptr, Tn, S, H);
-    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: delta");
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd: delta");
   }
   CUtensorMap mq, mo, mdq;
   if (int rc = make_tmap_bf16_2d(&mq, qkv, (uint64_t)3 * H * D, Tn, ld, 64, T)) return rc;
@@ -917,16 +916,11 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     if (e == cudaSuccess && D == 64)
       e = cudaFuncSetAttribute(dkdv_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                DkvSmem<D, true>::TOTAL);
-    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: cudaFuncSetAttribute");
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd: cudaFuncSetAttribute");
     configured = true;
   }
   const dim3 grid(S / T, H, n_seq);
-  static int only = -1;  // debug: ZB_ATTN_BWD_ONLY=dq|dkdv runs one pass
-  if (only < 0) {
-    const char* e = getenv("ZB_ATTN_BWD_ONLY");
-    only = !e ? 0 : (e[0] == 'q' || (e[0] == 'd' && e[1] == 'q')) ? 1 : 2;
-  }
-  if (fused && !only) {
+  if (fused) {
     const int HD = H * D;
     cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)Tn};
     cuuint64_t strides[1] = {(cuuint64_t)HD * 4};
@@ -944,46 +938,37 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = getenv("ZB_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static const bool grid_items = getenv("ZB_ATTN_BWD_GRID") != nullptr;  // A/B: one CTA per item
-    cudaError_t e;
-    if (grid_items) {
-      e = cudaLaunchKernelEx(&cfg, dkdv_kernel<D, true>, mq, mo, mdq, (const float*)lse,
-                             (const float*)delta, (__nv_bfloat16*)dqkv, S, H, ld, scale);
-    } else {
-      static bool cfg_p = false;
-      if (!cfg_p) {
-        e = cudaFuncSetAttribute(dkdvq_persistent_kernel<D>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 DkvSmem<D, true>::TOTAL);
-        if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc: cudaFuncSetAttribute");
-        cfg_p = true;
-      }
-      const int items = (S / T) * H * n_seq;
-      cfg.gridDim = dim3(items < num_sms() ? items : num_sms());
-      e = cudaLaunchKernelEx(&cfg, dkdvq_persistent_kernel<D>, mq, mo, mdq, (const float*)lse,
-                             (const float*)delta, (__nv_bfloat16*)dqkv, S, H, n_seq, ld, scale);
+    static bool cfg_p = false;
+    if (!cfg_p) {
+      cudaError_t e0 = cudaFuncSetAttribute(dkdvq_persistent_kernel<D>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            DkvSmem<D, true>::TOTAL);
+      if (e0 != cudaSuccess) return set_cuda_error(e0, "attn_bwd: cudaFuncSetAttribute");
+      cfg_p = true;
     }
-    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd_tc fused launch");
+    const int items = (S / T) * H * n_seq;
+    cfg.gridDim = dim3(items < num_sms() ? items : num_sms());
+    cudaError_t e = cudaLaunchKernelEx(&cfg, dkdvq_persistent_kernel<D>, mq, mo, mdq, (const float*)lse,
+                                       (const float*)delta, (__nv_bfloat16*)dqkv, S, H, n_seq, ld, scale);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd fused launch");
     const int64_t n8 = (int64_t)Tn * (HD / 8);
     int cg = (int)((n8 + 255) / 256);
     if (cg > num_sms() * 8) cg = num_sms() * 8;
     e = launch_pdl_k(dq_convert_kernel, dim3(cg), dim3(256), 0, s, (const float*)dq_accum,
                      (__nv_bfloat16*)dqkv, Tn, HD, ld, scale);
-    return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_bwd_tc fused launch");
+    return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_bwd fused launch");
   }
-  if (only != 1)
-    dkdv_kernel<D, false><<<grid, kThreads, DkvSmem<D, false>::TOTAL, s>>>(
+  dkdv_kernel<D, false><<<grid, kThreads, DkvSmem<D, false>::TOTAL, s>>>(
         mq, mo, mq /*unused*/, (const float*)lse, (const float*)delta, (__nv_bfloat16*)dqkv, S, H,
         ld, scale);
-  if (only != 2)
-    dq_kernel<D><<<grid, kThreads, DqSmem<D>::TOTAL, s>>>(mq, mo, (const float*)lse,
+  dq_kernel<D><<<grid, kThreads, DqSmem<D>::TOTAL, s>>>(mq, mo, (const float*)lse,
                                                         (const float*)delta, (__nv_bfloat16*)dqkv,
                                                         S, H, ld, scale);
   cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_bwd_tc launch");
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "attn_bwd launch");
 }
 
 }  // namespace fab
@@ -991,18 +976,18 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
 
 using namespace zb;
 
-extern "C" int zb_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const void* lse,
+extern "C" int zb_attn_bwd(const void* qkv, const void* out, const void* dout, const void* lse,
                               void* dqkv, void* dq_accum, void* delta, int n_seq, int S, int H,
                               int D, int ld, float scale, cudaStream_t s) {
-  if (S % 128) return set_error(ZB_ERR_INVALID, "attn_bwd_tc: seq_len must be a multiple of 128");
+  if (S % 128) return set_error(ZB_ERR_INVALID, "attn_bwd: seq_len must be a multiple of 128");
   if (ld % 8 || ((uintptr_t)qkv & 15) || ((uintptr_t)dout & 15))
-    return set_error(ZB_ERR_INVALID, "attn_bwd_tc: bad ld/alignment");
+    return set_error(ZB_ERR_INVALID, "attn_bwd: bad ld/alignment");
   if (n_seq <= 0) return 0;
   if (dq_accum && ((uintptr_t)dq_accum & 15))
-    return set_error(ZB_ERR_INVALID, "attn_bwd_tc: dq_accum must be 16-byte aligned");
+    return set_error(ZB_ERR_INVALID, "attn_bwd: dq_accum must be 16-byte aligned");
   if (D == 64)
     return fab::run<64>(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, S, H, ld, scale, s);
   if (D == 128)
     return fab::run<128>(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, S, H, ld, scale, s);
-  return set_error(ZB_ERR_UNSUPPORTED, "attn_bwd_tc: head_dim %d unsupported (64, 128)", D);
+  return set_error(ZB_ERR_UNSUPPORTED, "attn_bwd: head_dim %d unsupported (64, 128)", D);
 }

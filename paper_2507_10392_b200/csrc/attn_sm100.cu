@@ -700,7 +700,7 @@ static int run(const void* qkv, void* out, void* lse, int n_seq, int S, int H, i
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = getenv("ZB_NO_PDL") ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, fwd_ts_kernel, m128, m64, (__nv_bfloat16*)out,
@@ -1069,7 +1069,7 @@ static int run(const void* qkv, void* out, void* lse, int n_seq, int S, int H, i
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = getenv("ZB_NO_PDL") ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, fwd_pp_kernel<D, HV>, m128, m64, (__nv_bfloat16*)out,
@@ -1106,27 +1106,16 @@ static int run_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int 
 
 using namespace zb;
 
-extern "C" int zb_attn_fwd_tc(const void* qkv, void* out, void* lse, int n_seq, int S, int H,
-                              int D, int ld, float scale, cudaStream_t s) {
-  if (S % 128) return set_error(ZB_ERR_INVALID, "attn_fwd_tc: seq_len must be a multiple of 128");
-  if (ld % 8 || ((uintptr_t)qkv & 15)) return set_error(ZB_ERR_INVALID, "attn_fwd_tc: bad ld/alignment");
+extern "C" int zb_attn_fwd(const void* qkv, void* out, void* lse, int n_seq, int S, int H,
+                           int D, int ld, float scale, cudaStream_t s) {
+  if (S % 128) return set_error(ZB_ERR_INVALID, "attn_fwd: seq_len must be a multiple of 128");
+  if (ld % 8 || ((uintptr_t)qkv & 15)) return set_error(ZB_ERR_INVALID, "attn_fwd: bad ld/alignment");
   if (n_seq <= 0) return 0;
-  // Kernel choice (A/B: ZB_ATTN_FWD=pp|ts|1cta): pairs of query tiles per CTA when
-  // S % 256 == 0, else the two-CTA-per-SM kernel (D = 64) / the single-tile kernel.
-  static const char* pick = getenv("ZB_ATTN_FWD");
-  const bool want_pp = !pick || pick[0] == 'p';
-  if (want_pp && S % 256 == 0 && (D == 64 || D == 128))
-    return D == 64 ? (pick && pick[1] == '1'
-                          ? fa::fa_pp::run<64, 1>(qkv, out, lse, n_seq, S, H, ld, scale, s)
-                          : fa::fa_pp::run<64, 2>(qkv, out, lse, n_seq, S, H, ld, scale, s))
-                   : (pick && pick[1] == '2'
-                          ? fa::fa_pp::run<128, 2>(qkv, out, lse, n_seq, S, H, ld, scale, s)
-                          : fa::fa_pp::run<128, 1>(qkv, out, lse, n_seq, S, H, ld, scale, s));
-  if (D == 64) {
-    const bool one = pick && pick[0] == '1';
-    if (!one) return fa::fa_ts::run(qkv, out, lse, n_seq, S, H, ld, scale, s);
-    return fa::run_fwd<64>(qkv, out, lse, n_seq, S, H, ld, scale, s);
-  }
+  // Pairs of query tiles per CTA when S % 256 == 0; else the two-CTA-per-SM kernel
+  // (D = 64) / the single-tile kernel (D = 128).
+  if (S % 256 == 0 && D == 64) return fa::fa_pp::run<64, 2>(qkv, out, lse, n_seq, S, H, ld, scale, s);
+  if (S % 256 == 0 && D == 128) return fa::fa_pp::run<128, 1>(qkv, out, lse, n_seq, S, H, ld, scale, s);
+  if (D == 64) return fa::fa_ts::run(qkv, out, lse, n_seq, S, H, ld, scale, s);
   if (D == 128) return fa::run_fwd<128>(qkv, out, lse, n_seq, S, H, ld, scale, s);
-  return set_error(ZB_ERR_UNSUPPORTED, "attn_fwd_tc: head_dim %d unsupported (64, 128)", D);
+  return set_error(ZB_ERR_UNSUPPORTED, "attn_fwd: head_dim %d unsupported (64, 128)", D);
 }

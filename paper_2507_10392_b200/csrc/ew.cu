@@ -77,134 +77,7 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
 
 // dx = dres + rstd * (g - mean(g) - xhat * mean(g * xhat)),  g = dy * w
 // dw += sum_rows dy * xhat,  db += sum_rows dy.
-// One warp per row; each lane owns the same MAXV 8-wide column vectors for
-// every row it visits, so dw/db partials stay in registers across rows and
-// the row data is read from HBM exactly once.  Per block: one smem reduction,
-// then one fp32 atomic per column.
-template <int MAXV>
-__global__ void __launch_bounds__(256) layernorm_bwd_kernel(
-    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-    const __nv_bfloat16* __restrict__ w, const float* __restrict__ mean_in,
-    const float* __restrict__ rstd_in, __nv_bfloat16* dx, float* __restrict__ dw,
-    float* __restrict__ db, const __nv_bfloat16* dres, int rows, int d) {
-  pdl_enter();
-  extern __shared__ float sh[];  // [16][warps][32] block-reduction staging
-  const int warps = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int nv = d >> 3;
-  // Small rows (MAXV <= 4, d <= 1024): w stays in registers and the next row's
-  // dy / x loads are in flight while this row computes.  Wider rows would spill,
-  // so they reload w through L1 and do not prefetch.
-  constexpr bool kPipe = MAXV <= 4;
-  uint4 qw[MAXV];
-  const uint4* wr = reinterpret_cast<const uint4*>(w);
-#pragma unroll
-  for (int j = 0; j < MAXV; ++j) {
-    const int v = lane + 32 * j;
-    qw[j] = v < nv ? wr[v] : make_uint4(0, 0, 0, 0);
-  }
-  float adw[MAXV][8], adb[MAXV][8];
-#pragma unroll
-  for (int j = 0; j < MAXV; ++j)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) adw[j][k] = adb[j][k] = 0.f;
-  const int stride = gridDim.x * warps;
-  int row = blockIdx.x * warps + warp;
-  // software pipeline: the next row's dy / x are in flight while this row computes
-  uint4 qd[MAXV], qx[MAXV];
-  auto load = [&](int r, uint4* a, uint4* b) {
-    const uint4* dyr = reinterpret_cast<const uint4*>(dy + (size_t)r * d);
-    const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)r * d);
-#pragma unroll
-    for (int j = 0; j < MAXV; ++j) {
-      const int v = lane + 32 * j;
-      a[j] = v < nv ? dyr[v] : make_uint4(0, 0, 0, 0);
-      b[j] = v < nv ? xr[v] : make_uint4(0, 0, 0, 0);
-    }
-  };
-  if (row < rows) load(row, qd, qx);
-  for (; row < rows; row += stride) {
-    const int next = row + stride;
-    uint4 nd[kPipe ? MAXV : 1], nx[kPipe ? MAXV : 1];
-    if constexpr (kPipe) {
-      if (next < rows) load(next, nd, nx);
-    }
-    const float mean = mean_in[row], rstd = rstd_in[row];
-    float sg = 0.f, sgx = 0.f;
-#pragma unroll
-    for (int j = 0; j < MAXV; ++j) {
-      const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw[j].x;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
-        const float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
-        const float g0 = dv.x * wv.x, g1 = dv.y * wv.y;
-        adw[j][2 * k] += dv.x * h0;
-        adw[j][2 * k + 1] += dv.y * h1;
-        adb[j][2 * k] += dv.x;
-        adb[j][2 * k + 1] += dv.y;
-        sg += g0 + g1;
-        sgx += g0 * h0 + g1 * h1;
-      }
-    }
-    const float mg = warp_sum(sg) / d, mgx = warp_sum(sgx) / d;
-    uint4* dxr = reinterpret_cast<uint4*>(dx + (size_t)row * d);
-    const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + (size_t)row * d) : nullptr;
-#pragma unroll
-    for (int j = 0; j < MAXV; ++j) {
-      const int v = lane + 32 * j;
-      if (v >= nv) continue;
-      const uint4 qr = rr ? rr[v] : make_uint4(0, 0, 0, 0);
-      const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw[j].x, *ri = &qr.x;
-      uint4 o;
-      uint32_t* oi = &o.x;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
-        float2 rv = rr ? unpack_bf16(ri[k]) : make_float2(0.f, 0.f);
-        const float h0 = (xv.x - mean) * rstd, h1 = (xv.y - mean) * rstd;
-        const float o0 = rstd * (dv.x * wv.x - mg - h0 * mgx) + rv.x;
-        const float o1 = rstd * (dv.y * wv.y - mg - h1 * mgx) + rv.y;
-        oi[k] = pack_bf16(o0, o1);
-      }
-      dxr[v] = o;
-    }
-    if constexpr (kPipe) {
-#pragma unroll
-      for (int j = 0; j < MAXV; ++j) {
-        qd[j] = nd[j];
-        qx[j] = nx[j];
-      }
-    } else if (next < rows) {
-      load(next, qd, qx);
-    }
-  }
-  // Block reduction of the per-lane partials without shared-memory atomics:
-  // per column group j, stage [16 values][warp][lane], sum over warps, one
-  // global atomic per column and block.
-#pragma unroll
-  for (int j = 0; j < MAXV; ++j) {
-    if (j) __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      sh[(k * warps + warp) * 32 + lane] = adw[j][k];
-      sh[((8 + k) * warps + warp) * 32 + lane] = adb[j][k];
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < 16 * 32; idx += blockDim.x) {
-      const int k = idx >> 5, ln = idx & 31;
-      const int v = ln + 32 * j;
-      if (v >= nv) continue;
-      float t = 0.f;
-      for (int wi = 0; wi < warps; ++wi) t += sh[(k * warps + wi) * 32 + ln];
-      float* dst = k < 8 ? dw + v * 8 + k : db + v * 8 + (k - 8);
-      atomicAdd(dst, t);
-    }
-  }
-}
-
-// Split backward (default): (1) dx, one warp per row at full occupancy (no
+// Two launches: (1) dx, one warp per row at full occupancy (no
 // cross-row state); (2) dw / db as a column reduction over dy and x, structured
 // like bias_grad (32 column vectors x 8 row lanes per CTA, 4 loads in flight).
 // 75 MB of traffic at HBM speed instead of 50 MB at the fused kernel's
@@ -412,7 +285,10 @@ __global__ void embedding_bwd_kernel(const int* __restrict__ tok,
 
 // ------------------------------------------------------------------ cross-entropy
 // One CTA per row: online (max, sum-exp) pass, then dlogits = (softmax - onehot)*scale
-// written in place (bf16).  loss_sum += (lse - logit[label]).  label < 0: ignored row.
+// written in place (bf16).  loss_sum += (lse - logit[label]).  label < 0: ignored row;
+// label >= V traps (out-of-range class index, as torch's cross_entropy rejects it).
+// The label's logit is read before the first barrier: dlogits may alias logits, and
+// after the block reduction other warps overwrite the row.
 constexpr int XENT_THREADS = 512;
 __global__ void __launch_bounds__(XENT_THREADS) xent_kernel(const __nv_bfloat16* logits,
                                                           const int* __restrict__ labels,
@@ -424,6 +300,8 @@ __global__ void __launch_bounds__(XENT_THREADS) xent_kernel(const __nv_bfloat16*
   const __nv_bfloat16* lr = logits + (size_t)row * ld;
   __nv_bfloat16* gr = dlogits + (size_t)row * ld;
   const int label = labels[row];
+  if (label >= V) __trap();
+  const float label_logit = (threadIdx.x == 0 && label >= 0) ? __bfloat162float(lr[label]) : 0.f;
   const int nv = V >> 3;  // V % 8 == 0 enforced on the host
   float m = -INFINITY, s = 0.f;
   for (int v = threadIdx.x; v < nv; v += XENT_THREADS) {
@@ -471,7 +349,7 @@ __global__ void __launch_bounds__(XENT_THREADS) xent_kernel(const __nv_bfloat16*
   }
   const float lse = s_lse;
   if (threadIdx.x == 0 && label >= 0)
-    atomicAdd(loss_sum, lse - __bfloat162float(lr[label]));
+    atomicAdd(loss_sum, lse - label_logit);
   const float sc = label >= 0 ? scale : 0.f;
   for (int v = threadIdx.x; v < nv; v += XENT_THREADS) {
     uint4 q = reinterpret_cast<const uint4*>(lr)[v];
@@ -618,8 +496,7 @@ static int layernorm_bwd_impl(const void* dy, const void* x, const void* w, cons
   if (rows <= 0) return 0;
   const int threads = 256, per = threads / 32;
   const int vpl = (d / 8 + 31) / 32;  // column vectors per lane
-  static const bool fused = getenv("ZB_LN_BWD_FUSED") != nullptr;  // A/B: single-kernel variant
-  if (!fused || phase != 0) {
+  {
     auto go1 = [&](auto kern) {
       launch_pdl_k(kern, dim3((rows + per - 1) / per), dim3(threads), 0, s,
                    (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w,
@@ -656,27 +533,6 @@ static int layernorm_bwd_impl(const void* dy, const void* x, const void* w, cons
     }
     return launched("layernorm_bwd");
   }
-  // One CTA per SM (measured: more CTAs lose to the per-CTA reduction), each warp
-  // walking rows with the next row's loads in flight.
-  int blocks = (rows + per - 1) / per;
-  if (blocks > num_sms()) blocks = num_sms();
-  const size_t smem = 16 * (size_t)per * 32 * sizeof(float);
-  auto go = [&](auto kern) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl_k(kern, dim3(blocks), dim3(threads), smem, s, (const __nv_bfloat16*)dy,
-                 (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, (const float*)mean,
-                 (const float*)rstd, (__nv_bfloat16*)dx, (float*)dw, (float*)db,
-                 (const __nv_bfloat16*)dres, rows, d);
-  };
-  if (vpl <= 1) go(layernorm_bwd_kernel<1>);
-  else if (vpl <= 2) go(layernorm_bwd_kernel<2>);
-  else if (vpl <= 3) go(layernorm_bwd_kernel<3>);
-  else if (vpl <= 4) go(layernorm_bwd_kernel<4>);
-  else if (vpl <= 7) go(layernorm_bwd_kernel<7>);
-  else if (vpl <= 10) go(layernorm_bwd_kernel<10>);
-  else if (vpl <= 20) go(layernorm_bwd_kernel<20>);
-  return launched("layernorm_bwd");
 }
 
 extern "C" int zb_layernorm_bwd(const void* dy, const void* x, const void* w, const void* mean,
@@ -689,9 +545,6 @@ extern "C" int zb_layernorm_bwd_ex(const void* dy, const void* x, const void* w,
                                    const void* rstd, void* dx, void* dw, void* db,
                                    const void* dres, void* db_res, void* db_out, int rows, int d,
                                    cudaStream_t s) {
-  static const bool fused = getenv("ZB_LN_BWD_FUSED") != nullptr;
-  if (fused && (db_res || db_out))
-    return set_error(ZB_ERR_UNSUPPORTED, "layernorm_bwd_ex: not with ZB_LN_BWD_FUSED");
   return layernorm_bwd_impl(dy, x, w, mean, rstd, dx, dw, db, dres, db_res, db_out, rows, d, s);
 }
 

@@ -918,7 +918,6 @@ static int make_tmap_epi(CUtensorMap* m, const void* ptr, bool f32, uint64_t col
 // the previous kernel's tail; the kernel waits (griddep_wait) before any global access.
 template <typename Kern, typename... Args>
 static cudaError_t launch_pdl(Kern kern, dim3 grid, int smem, cudaStream_t stream, Args... args) {
-  static const bool off = getenv("ZB_NO_PDL") != nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
@@ -926,7 +925,7 @@ static cudaError_t launch_pdl(Kern kern, dim3 grid, int smem, cudaStream_t strea
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);
@@ -936,7 +935,6 @@ static cudaError_t launch_pdl(Kern kern, dim3 grid, int smem, cudaStream_t strea
 template <typename Kern, typename... Args>
 static cudaError_t launch_pdl_cluster(Kern kern, dim3 grid, int smem, cudaStream_t stream,
                                       int cluster_x, Args... args) {
-  static const bool off = getenv("ZB_NO_PDL") != nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
@@ -944,7 +942,7 @@ static cudaError_t launch_pdl_cluster(Kern kern, dim3 grid, int smem, cudaStream
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   attr[1].id = cudaLaunchAttributeClusterDimension;
   attr[1].val.clusterDim.x = cluster_x;
   attr[1].val.clusterDim.y = 1;
@@ -1141,12 +1139,14 @@ struct GemmKey {
 static std::mutex g_tune_mu;
 static std::map<GemmKey, GemmChoice> g_tuned;
 
-// Persistent tuning cache (one line per shape: M N K a_mn b_mn epi beta1 ldc pair bn
-// splits).  Path: $ZB_GEMM_TUNE_CACHE, else gemm_tune_cache.txt beside this library.
-// Loaded once; new measurements are appended, so a tuned run (or the committed file)
-// makes later runs start without tuning launches.
+// Tile table measured on B200 (scripts/tune_gemm.py): gemm_tune_cache.txt beside this
+// library, one line per shape "g1 M N K a_mn b_mn epi beta1 ldc pair bn splits".  The
+// library only READS it (once, on the first call); entries whose tag is not the
+// current kernel generation kTileTableTag are ignored, so tilings measured on older
+// kernels never outlive a kernel change.  Shapes not in the table use the cost model.
+static const char* kTileTableTag = "g1";
+
 static std::string tune_cache_path() {
-  if (const char* e = getenv("ZB_GEMM_TUNE_CACHE")) return e;
   Dl_info info;
   if (dladdr((void*)&tune_cache_path, &info) && info.dli_fname) {
     std::string so = info.dli_fname;
@@ -1162,20 +1162,17 @@ static void tune_cache_load() {
   loaded = true;
   FILE* f = fopen(tune_cache_path().c_str(), "r");
   if (!f) return;
-  GemmKey k;
-  GemmChoice c;
-  while (fscanf(f, "%d %d %d %d %d %d %d %d %d %d %d", &k.M, &k.N, &k.K, &k.a_mn, &k.b_mn, &k.epi,
-                &k.beta1, &k.ldc, &c.pair, &c.bn, &c.splits) == 11)
+  char line[256], tag[16];
+  while (fgets(line, sizeof(line), f)) {
+    GemmKey k;
+    GemmChoice c;
+    if (sscanf(line, "%15s %d %d %d %d %d %d %d %d %d %d %d", tag, &k.M, &k.N, &k.K, &k.a_mn,
+               &k.b_mn, &k.epi, &k.beta1, &k.ldc, &c.pair, &c.bn, &c.splits) != 12)
+      continue;
+    if (strcmp(tag, kTileTableTag) != 0) continue;
     if ((c.bn == 128 || c.bn == 192 || c.bn == 256) && c.splits >= 1 && (c.pair >= 0 && c.pair <= 2))
       g_tuned[k] = c;
-  fclose(f);
-}
-
-static void tune_cache_append(const GemmKey& k, const GemmChoice& c) {
-  FILE* f = fopen(tune_cache_path().c_str(), "a");
-  if (!f) return;
-  fprintf(f, "%d %d %d %d %d %d %d %d %d %d %d\n", k.M, k.N, k.K, k.a_mn, k.b_mn, k.epi, k.beta1,
-          k.ldc, c.pair, c.bn, c.splits);
+  }
   fclose(f);
 }
 
@@ -1185,8 +1182,10 @@ struct GemmCall {
   float beta;
 };
 
+// raster: -1 = by operand size, 0 = M-fastest, 1 = N-fastest; allow_tma_epi: 0 forces
+// the direct-store epilogue (tests / experiments only).
 static int launch_choice(const GemmCall& g, const GemmChoice& ch, void* C, void* aux,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, int raster = -1, int allow_tma_epi = 1) {
   const int BN = ch.bn, pair = ch.pair;
   CUtensorMap ta, tb;
   int rc;
@@ -1213,8 +1212,6 @@ static int launch_choice(const GemmCall& g, const GemmChoice& ch, void* C, void*
   args.splits = ch.splits;
   {
     const uint64_t a_bytes = (uint64_t)g.M * g.K * 2, b_bytes = (uint64_t)g.N * g.K * 2;
-    const char* re = getenv("ZB_GEMM_RASTER");  // 0|1 pins the raster (benchmarking)
-    const int raster = re ? atoi(re) : -1;
     args.n_fastest = raster >= 0 ? raster : (a_bytes > b_bytes && a_bytes > (64ull << 20));
   }
   const int epilogue = g.epilogue;
@@ -1240,7 +1237,7 @@ static int launch_choice(const GemmCall& g, const GemmChoice& ch, void* C, void*
     if (g.R) ok = ok && ((uintptr_t)g.R & 15) == 0 && (g.ldr % 8) == 0;
     if (epilogue == EPI_BIAS_GELU || epilogue == EPI_GELU_BWD) ok = ok && aux;
     if (epilogue == EPI_BIAS_RESID || epilogue == EPI_RESID) ok = ok && g.R;
-    if (ok && getenv("ZB_GEMM_NO_TMA_EPI")) ok = false;
+    if (!allow_tma_epi) ok = false;
     if (ok) {
       int rc2 = make_tmap_epi(&et.c, C, f32, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldc);
       if (!rc2 && aux)
@@ -1308,10 +1305,9 @@ static int launch_choice(const GemmCall& g, const GemmChoice& ch, void* C, void*
   return set_error(ZB_ERR_INVALID, "gemm: unsupported layout (A MN-major with B K-major)");
 }
 
-// Measured choice: time the model's pick and its neighbours once per shape on
-// scratch outputs (inputs are only read), keep the fastest.  Runs only outside
-// CUDA-graph capture (the first eager step warms every shape); ZB_GEMM_TUNE=0
-// keeps the model's choice.
+// Measured choice (zb_gemm_tune, called by scripts/tune_gemm.py only): time the
+// model's pick and its neighbours on scratch outputs (inputs are only read), keep
+// the fastest.  Synchronises the stream; never called by zb_gemm_bf16.
 static GemmChoice tune_choice(const GemmCall& g, const GemmChoice& model, void* aux_ro,
                               cudaStream_t stream) {
   std::vector<GemmChoice> cands{model};
@@ -1373,13 +1369,8 @@ static GemmChoice tune_choice(const GemmCall& g, const GemmChoice& model, void* 
   return best;
 }
 
-}  // namespace zb
-using namespace zb;
-
-extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* bias,
-                            const void* R, void* aux, int M, int N, int K, int lda, int ldb,
-                            int ldc, int ldr, int ldaux, int a_mn_major, int b_mn_major,
-                            int epilogue, float beta, cudaStream_t stream) {
+static int gemm_validate(const void* A, const void* B, const void* bias, const void* R,
+                         const void* aux, int M, int N, int K, int lda, int ldb, int epilogue) {
   if (M <= 0 || N <= 0 || K <= 0) return set_error(ZB_ERR_INVALID, "gemm: bad shape %d %d %d", M, N, K);
   if ((lda % 8) || (ldb % 8))
     return set_error(ZB_ERR_INVALID, "gemm: lda/ldb must be multiples of 8 elements");
@@ -1394,44 +1385,86 @@ extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* b
     return set_error(ZB_ERR_INVALID, "gemm: epilogue %d needs aux", epilogue);
   if ((epilogue == EPI_BIAS_RESID || epilogue == EPI_RESID) && !R)
     return set_error(ZB_ERR_INVALID, "gemm: epilogue %d needs a residual", epilogue);
-  const char* fenv = getenv("ZB_GEMM_CTAS");  // 1|2 pins 1-CTA / 2-CTA tiles (benchmarking)
-  const int force = fenv ? atoi(fenv) : 0;
-  const char* e1 = getenv("ZB_GEMM_BN");      // benchmarking overrides
-  const char* e2 = getenv("ZB_GEMM_SPLITS");
-  const char* e3 = getenv("ZB_GEMM_DEBUG");
-  const char* e4 = getenv("ZB_GEMM_TUNE");
-  const int fbn = e1 ? atoi(e1) : 0, fsp = e2 ? atoi(e2) : 0, dbg = e3 ? atoi(e3) : 0;
-  const bool tune = !(e4 && atoi(e4) == 0) && !force && !fbn && !fsp;
+  return 0;
+}
+
+// The tile zb_gemm_bf16 uses: the measured table entry, else the cost model.
+static GemmChoice default_choice(int M, int N, int K, int a_mn, int b_mn, int epilogue, float beta,
+                                 int ldc, int* from_table) {
+  const GemmKey key{M, N, K, a_mn, b_mn, epilogue, beta == 1.f ? 1 : 0, ldc};
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  tune_cache_load();
+  auto it = g_tuned.find(key);
+  if (from_table) *from_table = it != g_tuned.end();
+  if (it != g_tuned.end()) return it->second;
+  return model_choice(M, N, K, a_mn, b_mn, epilogue, beta, 0);
+}
+
+}  // namespace zb
+using namespace zb;
+
+extern "C" int zb_gemm_bf16(const void* A, const void* B, void* C, const void* bias,
+                            const void* R, void* aux, int M, int N, int K, int lda, int ldb,
+                            int ldc, int ldr, int ldaux, int a_mn_major, int b_mn_major,
+                            int epilogue, float beta, cudaStream_t stream) {
+  if (int rc = gemm_validate(A, B, bias, R, aux, M, N, K, lda, ldb, epilogue)) return rc;
+  GemmCall g{A, B, bias, R, M, N, K, lda, ldb, ldc, ldr, ldaux, a_mn_major, b_mn_major,
+             epilogue, beta};
+  const GemmChoice ch = default_choice(M, N, K, a_mn_major, b_mn_major, epilogue, beta, ldc, nullptr);
+  return launch_choice(g, ch, C, aux, stream);
+}
+
+extern "C" int zb_gemm_bf16_tile(const void* A, const void* B, void* C, const void* bias,
+                                 const void* R, void* aux, int M, int N, int K, int lda, int ldb,
+                                 int ldc, int ldr, int ldaux, int a_mn_major, int b_mn_major,
+                                 int epilogue, float beta, int pair, int bn, int splits,
+                                 int raster, int tma_epi, cudaStream_t stream) {
+  if (int rc = gemm_validate(A, B, bias, R, aux, M, N, K, lda, ldb, epilogue)) return rc;
   GemmCall g{A, B, bias, R, M, N, K, lda, ldb, ldc, ldr, ldaux, a_mn_major, b_mn_major,
              epilogue, beta};
   GemmChoice ch = model_choice(M, N, K, a_mn_major, b_mn_major, epilogue, beta,
-                               force == 4 ? 2 : force);
-  if (force == 4) ch.pair = 2;  // ZB_GEMM_CTAS=4: two CTA pairs sharing A (multicast)
-  if (fbn == 128 || fbn == 256 || (fbn == 192 && !(ch.pair && b_mn_major))) ch.bn = fbn;
-  if (fsp > 0 && epilogue == EPI_F32 && beta == 1.f) ch.splits = fsp;
-  const char* how = "model";
-  if (tune) {
-    const GemmKey key{M, N, K, a_mn_major, b_mn_major, epilogue, beta == 1.f ? 1 : 0, ldc};
-    std::lock_guard<std::mutex> lk(g_tune_mu);
-    tune_cache_load();
-    auto it = g_tuned.find(key);
-    if (it != g_tuned.end()) {
-      ch = it->second;
-      how = "tuned";
-    } else {
-      cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(stream, &st);
-      if (st == cudaStreamCaptureStatusNone) {
-        ch = tune_choice(g, ch, aux, stream);
-        g_tuned[key] = ch;
-        tune_cache_append(key, ch);
-        how = "tuned";
-      }
-    }
+                               pair == 0 ? 1 : (pair > 0 ? 2 : 0));
+  if (pair >= 0) ch.pair = pair;
+  if (bn > 0) {
+    if (bn != 128 && bn != 192 && bn != 256) return set_error(ZB_ERR_INVALID, "gemm: bn %d", bn);
+    ch.bn = bn;
   }
-  if (dbg)
-    fprintf(stderr, "zb_gemm M=%d N=%d K=%d a_mn=%d b_mn=%d epi=%d -> %s BN=%d splits=%d (%s)\n",
-            M, N, K, a_mn_major, b_mn_major, epilogue, ch.pair == 2 ? "2x2cta" : ch.pair ? "2cta" : "1cta", ch.bn,
-            ch.splits, how);
-  return launch_choice(g, ch, C, aux, stream);
+  if (splits > 0) {
+    if (splits > 1 && !(epilogue == EPI_F32 && beta == 1.f))
+      return set_error(ZB_ERR_INVALID, "gemm: K splits need fp32 accumulation (beta = 1)");
+    ch.splits = splits;
+  }
+  if (ch.pair && M < 256) return set_error(ZB_ERR_INVALID, "gemm: CTA-pair tiles need M >= 256");
+  return launch_choice(g, ch, C, aux, stream, raster, tma_epi != 0);
+}
+
+extern "C" int zb_gemm_choice(int M, int N, int K, int a_mn_major, int b_mn_major, int epilogue,
+                              float beta, int ldc, int* pair, int* bn, int* splits,
+                              int* from_table) {
+  if (!pair || !bn || !splits) return set_error(ZB_ERR_INVALID, "gemm_choice: NULL output");
+  const GemmChoice ch = default_choice(M, N, K, a_mn_major, b_mn_major, epilogue, beta, ldc, from_table);
+  *pair = ch.pair;
+  *bn = ch.bn;
+  *splits = ch.splits;
+  return 0;
+}
+
+extern "C" int zb_gemm_tune(const void* A, const void* B, const void* bias, const void* R,
+                            void* aux, int M, int N, int K, int lda, int ldb, int ldc, int ldr,
+                            int ldaux, int a_mn_major, int b_mn_major, int epilogue, float beta,
+                            int* pair, int* bn, int* splits, cudaStream_t stream) {
+  if (int rc = gemm_validate(A, B, bias, R, aux, M, N, K, lda, ldb, epilogue)) return rc;
+  if (!pair || !bn || !splits) return set_error(ZB_ERR_INVALID, "gemm_tune: NULL output");
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &st);
+  if (st != cudaStreamCaptureStatusNone)
+    return set_error(ZB_ERR_INVALID, "gemm_tune: not allowed during graph capture");
+  GemmCall g{A, B, bias, R, M, N, K, lda, ldb, ldc, ldr, ldaux, a_mn_major, b_mn_major,
+             epilogue, beta};
+  const GemmChoice model = model_choice(M, N, K, a_mn_major, b_mn_major, epilogue, beta, 0);
+  const GemmChoice ch = tune_choice(g, model, aux, stream);
+  *pair = ch.pair;
+  *bn = ch.bn;
+  *splits = ch.splits;
+  return 0;
 }

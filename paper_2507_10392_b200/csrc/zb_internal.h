@@ -24,14 +24,10 @@ int tensor_map_encode(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, v
 // 2-D bf16 tensor map, 128-byte swizzle, box {box_inner, box_outer}.
 int make_tmap_bf16_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
                       uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer);
-// delta[b,h,q] = sum_d dO*O (attention backward preprocessing, attn.cu).
-int launch_attn_delta(const void* o, const void* dout, void* delta, int T, int S, int H, int D,
-                      cudaStream_t s);
 
 // Programmatic dependent launch (PDL) on `stream`: the kernel may be scheduled while
 // its predecessor drains (once every predecessor CTA executed griddep_launch()), and
 // must call griddep_wait() (common.cuh pdl_enter) before touching global memory.
-// ZB_NO_PDL=1 turns the attribute off (plain stream order) for A/B runs.
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

@@ -12,7 +12,7 @@ import torch
 from ._lib import call as _call
 
 # Device kernel launches issued per C-ABI entry point (for the bench's gpu_launches).
-_LAUNCHES_PER_CALL = {"zb_attn_bwd": 3, "zb_attn_bwd_tc": 3, "zb_layernorm_bwd": 2,
+_LAUNCHES_PER_CALL = {"zb_attn_bwd": 3, "zb_layernorm_bwd": 2,
                       "zb_layernorm_bwd_ex": 2, "zb_rmsnorm_bwd": 2}
 _launches = [0]
 
@@ -54,13 +54,7 @@ def _need_cuda(*ts):
             raise ValueError("libzorse_b200 kernels take CUDA tensors only (no CPU fallback)")
 
 
-def gemm(a, b, out, *, a_t=False, b_t=False, epilogue=EPI_BF16, bias=None, resid=None,
-         aux=None, beta=0.0, M=None, N=None, K=None):
-    """out[M,N] = op(a) @ op(b)^T with tcgen05.
-
-    a: [M,K] (a_t=False) or [K,M] (a_t=True);  b: [N,K] (b_t=False) or [K,N] (b_t=True).
-    All 2-D, row-major with unit inner stride; leading dims taken from stride(0).
-    """
+def _gemm_args(a, b, out, a_t, b_t, bias, resid, aux, M, N, K):
     _need_cuda(a, b, out, bias, resid, aux)
     if a_t:
         K_, M_ = a.shape
@@ -78,12 +72,58 @@ def gemm(a, b, out, *, a_t=False, b_t=False, epilogue=EPI_BF16, bias=None, resid
     for t in (a, b, out):
         if t.stride(-1) != 1:
             raise ValueError("gemm operands need unit inner stride")
+    return (M, N, K, a.stride(0), b.stride(0), out.stride(0),
+            resid.stride(0) if resid is not None else 0, aux.stride(0) if aux is not None else 0,
+            int(a_t), int(b_t))
+
+
+def gemm(a, b, out, *, a_t=False, b_t=False, epilogue=EPI_BF16, bias=None, resid=None,
+         aux=None, beta=0.0, M=None, N=None, K=None):
+    """out[M,N] = op(a) @ op(b)^T with tcgen05.
+
+    a: [M,K] (a_t=False) or [K,M] (a_t=True);  b: [N,K] (b_t=False) or [K,N] (b_t=True).
+    All 2-D, row-major with unit inner stride; leading dims taken from stride(0).
+    The tile comes from the committed B200 tile table, else the cost model.
+    """
+    dims = _gemm_args(a, b, out, a_t, b_t, bias, resid, aux, M, N, K)
     call("zb_gemm_bf16", _ptr(a), _ptr(b), _ptr(out), _ptr(bias), _ptr(resid), _ptr(aux),
-         M, N, K, a.stride(0), b.stride(0), out.stride(0),
-         resid.stride(0) if resid is not None else 0,
-         aux.stride(0) if aux is not None else 0,
-         int(a_t), int(b_t), epilogue, float(beta), _stream())
+         *dims, epilogue, float(beta), _stream())
     return out
+
+
+def gemm_tile(a, b, out, *, pair=-1, bn=0, splits=0, raster=-1, tma_epi=True, a_t=False,
+              b_t=False, epilogue=EPI_BF16, bias=None, resid=None, aux=None, beta=0.0):
+    """``gemm`` with an explicit tile (tests / tuning / benchmarks): pair 0 = 1-CTA,
+    1 = CTA pair, 2 = multicast pairs; bn 128/192/256; K splits (fp32 beta=1 only);
+    raster 0 = M-fastest, 1 = N-fastest; tma_epi False = direct-store epilogue.
+    Negative / zero values keep the cost model's pick for that field."""
+    dims = _gemm_args(a, b, out, a_t, b_t, bias, resid, aux, None, None, None)
+    call("zb_gemm_bf16_tile", _ptr(a), _ptr(b), _ptr(out), _ptr(bias), _ptr(resid), _ptr(aux),
+         *dims, epilogue, float(beta), int(pair), int(bn), int(splits), int(raster),
+         int(bool(tma_epi)), _stream())
+    return out
+
+
+def gemm_choice(M, N, K, *, a_t=False, b_t=False, epilogue=EPI_BF16, beta=0.0, ldc=None):
+    """(pair, bn, splits, from_table) that ``gemm`` uses for this shape."""
+    import ctypes
+    outs = [ctypes.c_int() for _ in range(4)]
+    call("zb_gemm_choice", M, N, K, int(a_t), int(b_t), epilogue, float(beta),
+         N if ldc is None else ldc, *[ctypes.byref(o) for o in outs])
+    return tuple(o.value for o in outs[:3]) + (bool(outs[3].value),)
+
+
+def gemm_tune(a, b, out, *, a_t=False, b_t=False, epilogue=EPI_BF16, bias=None, resid=None,
+              aux=None, beta=0.0):
+    """Measure the candidate tiles for this call's shape (synchronises; never inside
+    graph capture) and return the fastest (pair, bn, splits).  scripts/tune_gemm.py
+    writes the results into the committed tile table."""
+    import ctypes
+    dims = _gemm_args(a, b, out, a_t, b_t, bias, resid, aux, None, None, None)
+    outs = [ctypes.c_int() for _ in range(3)]
+    call("zb_gemm_tune", _ptr(a), _ptr(b), _ptr(bias), _ptr(resid), _ptr(aux), *dims, epilogue,
+         float(beta), *[ctypes.byref(o) for o in outs], _stream())
+    return tuple(o.value for o in outs)
 
 
 def layernorm_fwd(x, w, b, y, mean, rstd, eps=1e-5):
@@ -136,29 +176,24 @@ def xent_fwd_bwd(logits, labels, loss_sum, dlogits, scale):
          logits.stride(0), float(scale), _stream())
 
 
-def bias_grad(dy, db, beta=1.0):
-    """db (fp32) = beta*db + column sums of dy [rows, n] (bf16)."""
+def bias_grad(dy, db):
+    """db (fp32) += column sums of dy [rows, n] (bf16)."""
     _need_cuda(dy, db)
     rows, n = dy.shape
     call("zb_bias_grad", _ptr(dy), _ptr(db), rows, n, dy.stride(0), _stream())
 
 
-def attn_fwd(qkv, out, lse, n_seq, seq_len, n_head, head_dim, scale, impl="tc"):
-    """impl "tc": tcgen05/TMEM kernel (default); "mma": legacy mma.sync kernel."""
+def attn_fwd(qkv, out, lse, n_seq, seq_len, n_head, head_dim, scale):
+    """Causal attention forward on tcgen05/TMEM (csrc/attn_sm100.cu)."""
     _need_cuda(qkv, out, lse)
-    call("zb_attn_fwd_tc" if impl == "tc" else "zb_attn_fwd", _ptr(qkv), _ptr(out), _ptr(lse), n_seq, seq_len, n_head, head_dim,
+    call("zb_attn_fwd", _ptr(qkv), _ptr(out), _ptr(lse), n_seq, seq_len, n_head, head_dim,
          qkv.stride(0), float(scale), _stream())
 
 
 def attn_bwd(qkv, out, dout, lse, dqkv, dq_accum, delta, n_seq, seq_len, n_head, head_dim,
-             scale, impl="tc"):
-    """impl "tc": tcgen05/TMEM kernels (default); "mma": legacy mma.sync kernels."""
+             scale):
+    """Causal attention backward on tcgen05/TMEM (csrc/attn_bwd_sm100.cu)."""
     _need_cuda(qkv, out, dout, lse, dqkv, dq_accum, delta)
-    if impl == "tc":
-        call("zb_attn_bwd_tc", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), _ptr(dqkv),
-             _ptr(dq_accum), _ptr(delta), n_seq, seq_len, n_head, head_dim, qkv.stride(0),
-             float(scale), _stream())
-        return
     call("zb_attn_bwd", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), _ptr(dqkv), _ptr(dq_accum),
          _ptr(delta), n_seq, seq_len, n_head, head_dim, qkv.stride(0), float(scale), _stream())
 

@@ -10,7 +10,6 @@ the reference's (ties broken toward the smallest lexicographic vertex id).
 from __future__ import annotations
 
 import ctypes
-import os
 from typing import Dict, List, Tuple
 
 import numpy as np
@@ -18,24 +17,28 @@ import numpy as np
 from .graph import ClusterGraph, Partition, PartitionError, make_partition
 
 
-def _native_kernel():
+_UNRESOLVED = object()
+_native = _UNRESOLVED
+
+
+def native_kernel():
     """``zb_min_cut`` from the C-ABI library (csrc/mincut.cpp), or None when the library
     is not built — the reference likewise prefers its compiled kernel and falls back to
-    the numpy twin (partition.py:26-38)."""
-    try:
-        from .._lib import lib
-        return lib().zb_min_cut
-    except Exception:  # noqa: BLE001 - library absent: use the restatement below
-        return None
-
-
-_NATIVE = _native_kernel() if not os.environ.get("ZB_PURE_PYTHON_MINCUT") else None
-MINCUT_BACKEND = "native" if _NATIVE is not None else "python"
+    the numpy twin (partition.py:26-38).  Resolved on the first min-cut, not at import,
+    so importing the planner never loads the library."""
+    global _native
+    if _native is _UNRESOLVED:
+        try:
+            from .._lib import lib
+            _native = lib().zb_min_cut
+        except Exception:  # noqa: BLE001 - library absent: use the restatement below
+            _native = None
+    return _native
 
 
 def min_cut_kernel(weights: np.ndarray, lexrank: np.ndarray) -> Tuple[float, List[int]]:
     """Global minimum 2-cut of a dense symmetric graph: (weight, sorted side)."""
-    if _NATIVE is not None:
+    if native_kernel() is not None:
         return min_cut_native(weights, lexrank)
     return min_cut_python(weights, lexrank)
 
@@ -49,7 +52,7 @@ def min_cut_native(weights: np.ndarray, lexrank: np.ndarray) -> Tuple[float, Lis
     cut = ctypes.c_double()
     side = np.zeros(n, dtype=np.int64)
     ln = ctypes.c_int64()
-    rc = _NATIVE(w.ctypes.data, n, rank.ctypes.data, ctypes.byref(cut), side.ctypes.data,
+    rc = native_kernel()(w.ctypes.data, n, rank.ctypes.data, ctypes.byref(cut), side.ctypes.data,
                  ctypes.byref(ln))
     if rc:
         from .._lib import lib

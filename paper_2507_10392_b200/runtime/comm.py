@@ -10,7 +10,6 @@ The NCCL unique ids are exchanged with ``torch.distributed`` (plumbing only).
 from __future__ import annotations
 
 import ctypes
-import os
 from typing import List, Sequence, Tuple
 
 import torch
@@ -89,25 +88,20 @@ class NcclComm:
             self.handle = None
 
 
-def build_comms(dist, world_rank: int, world_size: int, groups_ranks: List[List[int]],
-                group_comms: bool = True):
-    """Create the world communicator and this rank's group communicator.
+def build_comms(dist, world_rank: int, world_size: int, groups_ranks: List[List[int]]):
+    """Create the world NCCL communicator (stage-boundary P2P, loss all-reduce).
 
-    ``groups_ranks[gi]`` lists the world ranks of DP group gi in shard order.
-    Returns (world_comm, group_comm_or_None).
+    DP-group collectives run over NVLink peer memory (``PeerGroup``), so no group
+    communicator is created.  Returns (world_comm, None).
     """
     ids = None
     if world_rank == 0:
-        ids = [NcclComm.new_unique_id()] + [NcclComm.new_unique_id() for _ in groups_ranks]
+        ids = [NcclComm.new_unique_id()]
     box = [ids]
     dist.broadcast_object_list(box, src=0)
     ids = box[0]
     world = NcclComm(ids[0], world_size, world_rank)
-    group = None
-    for gi, ranks in enumerate(groups_ranks):
-        if group_comms and world_rank in ranks and len(ranks) > 1:
-            group = NcclComm(ids[1 + gi], len(ranks), ranks.index(world_rank))
-    return world, group
+    return world, None
 
 
 class PeerGroup:
@@ -159,7 +153,6 @@ class PeerGroup:
         dist.all_gather_object(allh, mine)
         for ranks in groups_ranks:
             if world_rank in ranks and len(ranks) > 1:
-                mode = {"ce": 0, "sm": 1}.get(os.environ.get("ZB_PEER_AG", ""), mode)
                 return PeerGroup(arena, ranks, world_rank, allh, mode)
         return None
 

@@ -43,6 +43,7 @@ from ..plan.costs import CostContext
 from ..plan.emulated import ModelConfig
 from ..plan.schedule import Event, build_schedule
 from ..plan.shard import ShardSpec, split_flat
+from .transfers import boundary_transfers, sample_ranges
 from .model import (FlatLayout, make_model_ops, alloc_acts, alloc_bwd_scratch, embed_layout,
                     head_layout, init_flat, layer_layout)
 
@@ -258,67 +259,13 @@ class StageExecutor:
         self.gsumsq = torch.zeros(1, device=device, dtype=torch.float32)
 
         # ---------------- sample ranges and boundary transfer lists ----------
-        self._sample_ranges = self._compute_sample_ranges()
-        self.transfers = self._compute_transfers()
+        self._sample_ranges = sample_ranges(plan)
+        self.transfers = boundary_transfers(plan, self._sample_ranges, dev_id, rank_of, S)
 
     # ------------------------------------------------------------ geometry
-    def _compute_sample_ranges(self):
-        """ranges[gi][m][dev] = (lo, hi) sample offsets inside microbatch m."""
-        out = []
-        for gi, g in enumerate(self.plan.groups):
-            per_m = []
-            for m in range(self.M):
-                off, r = 0, {}
-                for dev, cnt in self.plan.routing[gi][m]:
-                    r[dev] = (off, off + cnt)
-                    off += cnt
-                if off != self.mbs:
-                    raise ValueError(f"routing of group {gi} microbatch {m} covers {off} samples")
-                for dev in g.device_ids:
-                    r.setdefault(dev, (0, 0))
-                per_m.append(r)
-            out.append(per_m)
-        return out
-
     def my_samples(self, m: int) -> Tuple[int, int]:
         lo, hi = self._sample_ranges[self.gi][m][self.dev_id]
         return m * self.mbs + lo, m * self.mbs + hi
-
-    def _pairs(self, g_from: int, g_to: int, m: int):
-        """(src dev, dst dev, sample lo, sample hi) intersections for microbatch m."""
-        src, dst = self._sample_ranges[g_from][m], self._sample_ranges[g_to][m]
-        out = []
-        for a in self.plan.groups[g_from].device_ids:
-            alo, ahi = src[a]
-            for b in self.plan.groups[g_to].device_ids:
-                blo, bhi = dst[b]
-                lo, hi = max(alo, blo), min(ahi, bhi)
-                if lo < hi:
-                    out.append((a, b, lo, hi))
-        return out
-
-    def _compute_transfers(self):
-        """Per (direction, boundary s, m): list of (peer rank, row lo, row hi, is_send)
-        where rows index this rank's [n_tok, d] buffer."""
-        S = self.cfg.seq_len
-        me = self.dev_id
-        out = {}
-        for s in range(self.n_stages - 1):
-            ga, gb = self.order[s][0], self.order[s + 1][0]
-            if ga == gb:
-                continue
-            for m in range(self.M):
-                for direction, (g_from, g_to) in (("f", (ga, gb)), ("b", (gb, ga))):
-                    lst = []
-                    for a, b, lo, hi in self._pairs(g_from, g_to, m):
-                        if a == me:
-                            base = self._sample_ranges[g_from][m][me][0]
-                            lst.append((self.rank_of[b], (lo - base) * S, (hi - base) * S, True))
-                        if b == me:
-                            base = self._sample_ranges[g_to][m][me][0]
-                            lst.append((self.rank_of[a], (lo - base) * S, (hi - base) * S, False))
-                    out[(direction, s, m)] = lst
-        return out
 
     # ------------------------------------------------------------ data
     def load_batch(self, batch: torch.Tensor) -> int:

@@ -23,7 +23,6 @@ Activation layout: token-major [tokens, d] bf16; a microbatch slice of
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Tuple
 
@@ -198,12 +197,13 @@ class WgradLane:
     (wave tails, small HBM-bound kernels).  ``join`` at the end of the block makes
     the compute stream wait for every forked GEMM before the block's buffers are
     reused (the next block's recompute overwrites them).  CPU tensors (tests' torch
-    twin) and ZB_WGRAD_LANE=0 run everything inline."""
+    twin) run everything inline; ``enabled = False`` serialises the lane (the bench's
+    per-launch GEMM timing)."""
 
     def __init__(self):
         self.stream = None
         self.pending = False
-        self.enabled = os.environ.get("ZB_WGRAD_LANE", "1") != "0"
+        self.enabled = True
 
     def fork(self, t: torch.Tensor):
         """Context for one wgrad launch, ordered after the compute stream's work so far."""

@@ -26,10 +26,8 @@ class ZorseTrainer:
     def __init__(self, plan: TrainingPlan, ctx: CostContext, cfg: ModelConfig, *,
                  world_rank: int = 0, world_size: int = 1, seed: int = 1234,
                  adam: AdamConfig = AdamConfig(), init_device: str = "cpu",
-                 schedule: str = "gpipe", streams: bool = True, collectives: str = "peer",
-                 offload_acts: bool = False, _ops=None, _comms=None, _device=None):
-        if collectives not in ("peer", "nccl"):
-            raise ValueError(f"collectives must be 'peer' or 'nccl', not {collectives!r}")
+                 schedule: str = "gpipe", streams: bool = True, offload_acts: bool = False,
+                 _ops=None, _comms=None, _device=None):
         devices = list(ctx.graph.vertices)
         if len(devices) != world_size:
             raise ValueError(f"cluster profile has {len(devices)} devices but world size is "
@@ -39,7 +37,8 @@ class ZorseTrainer:
         self.world_rank, self.world_size = world_rank, world_size
         groups_ranks = [[self.rank_of[d] for d in g.device_ids] for g in plan.groups]
         if _ops is None:
-            # Product path: B200 kernels + NCCL.  No CPU fallback.
+            # Product path: B200 kernels; DP-group collectives over NVLink peer memory,
+            # stage-boundary P2P and the loss all-reduce over NCCL.  No CPU fallback.
             if not torch.cuda.is_available():
                 raise RuntimeError("ZorseTrainer needs a CUDA (B200) device; there is no CPU path")
             from .. import kernels as ops
@@ -47,8 +46,7 @@ class ZorseTrainer:
             if world_size > 1:
                 import torch.distributed as dist
                 from .comm import build_comms
-                world, group = build_comms(dist, world_rank, world_size, groups_ranks,
-                                           group_comms=(collectives == "nccl"))
+                world, group = build_comms(dist, world_rank, world_size, groups_ranks)
             else:
                 world, group = None, None
         else:  # test harness injection (tests/cpu_ops.py)
@@ -61,8 +59,7 @@ class ZorseTrainer:
         self.exec = StageExecutor(plan, ctx, cfg, self.dev_id, self.rank_of, world, group, ops,
                                   device, seed=seed, adam=adam, init_device=init_device,
                                   schedule=schedule, streams=streams, offload_acts=offload_acts)
-        self.collectives = collectives if world_size > 1 else None
-        if _ops is None and world_size > 1 and collectives == "peer":
+        if _ops is None and world_size > 1:
             # AG-v / fused RS-v+AdamW over NVLink peer memory (csrc/peer.cu)
             from .comm import PeerGroup
             peer = PeerGroup.build(dist, self.exec.arena, world_rank, groups_ranks)

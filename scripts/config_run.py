@@ -66,10 +66,8 @@ def main():
     if plan.routing is None:
         P.attach_routing(plan, rt, "transformer")
     t0 = time.time()
-    coll = os.environ.get("ZB_COLLECTIVES", "peer")
     tr = ZorseTrainer(plan, ctx, cfg, world_rank=rank, world_size=world, schedule=r["schedule"],
-                      init_device="cuda", collectives=coll,
-                      offload_acts=os.environ.get("ZB_OFFLOAD", "0") == "1")
+                      init_device="cuda", offload_acts="--offload" in sys.argv)
     init_s = time.time() - t0
     batch = synthetic_batch(cfg.vocab, cfg.seq_len, r["gb"], 1, pin=True)
     losses = [tr.step(batch)]  # warm-up
@@ -90,7 +88,7 @@ def main():
     dist.all_reduce(gmem, op=dist.ReduceOp.MAX)
     if rank == 0:
         tok = r["gb"] * cfg.seq_len
-        print(json.dumps({"collectives": coll, "offload_acts": tr.exec.offload,
+        print(json.dumps({"offload_acts": tr.exec.offload,
             "run": name, "model": cfg.name, "n_gpus": world, "schedule": r["schedule"],
             "strategy": r["strategy"], "groups": [[g.device_ids, g.layers_assigned, g.shares]
                                                   for g in plan.groups],

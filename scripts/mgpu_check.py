@@ -1,7 +1,8 @@
 """Multi-GPU parity run (torchrun, one process per GPU): executes a small GPT
-through the product path (NCCL AG-v/RS-v, many-to-many P2P) for LAYOUT and
-checks every rank's loss, reduced gradient shards and updated master shards
-against the CPU fp32 oracle.  Prints one JSON line per rank; exits 1 on failure.
+through the product path (NVLink peer AG-v / fused RS-v+AdamW, many-to-many P2P
+over NCCL) for LAYOUT, gathers every rank's gradient / update / Adam-moment shards
+to rank 0, assembles the units and compares them tensor by tensor with the CPU
+fp32 oracle (oracle/parity.py).  Rank 0 prints one JSON line; exits 1 on failure.
 
   torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/mgpu_check.py LAYOUT
 """
@@ -15,7 +16,7 @@ sys.path.insert(0, ROOT)
 import torch
 import torch.distributed as dist
 
-from oracle import gpt_cpu
+from oracle import parity
 from paper_2507_10392_b200 import plan as P
 from paper_2507_10392_b200.plan import emulated as E
 from paper_2507_10392_b200.runtime.data import synthetic_batch
@@ -24,7 +25,7 @@ from paper_2507_10392_b200.runtime.trainer import ZorseTrainer
 CFG = E.ModelConfig("mgpu-gpt", "gpt", n_layer=4, d_model=256, n_head=4, vocab=2048, seq_len=128)
 LLAMA = E.ModelConfig("mgpu-llama", "llama", n_layer=4, d_model=512, n_head=4, vocab=4096,
                       seq_len=256, d_ff=1376)
-XLW = E.ModelConfig("mgpu-xl-width", "gpt", n_layer=4, d_model=1600, n_head=25, vocab=4096,
+XLW = E.ModelConfig("mgpu-xl-width", "gpt", n_layer=2, d_model=1600, n_head=25, vocab=4096,
                     seq_len=256)
 LAYOUTS = {
     # name: (nodes, groups, n_microbatches, ministage counts, strategy, global batch)
@@ -63,44 +64,37 @@ def main():
     plan = P.build_plan(ctx, prof, P.make_partition(ctx.graph, groups), M, counts,
                         P.Strategy(strategy), P.cluster_fingerprint(prof), "transformer")
     P.attach_routing(plan, rt, "transformer")
-    coll = os.environ.get("ZB_COLLECTIVES", "peer")
-    graph = os.environ.get("ZB_GRAPH", "1") == "1"
+    graph = os.environ.get("ZB_GRAPH", "1") == "1"   # script option: step 2 replays a graph
     tr = ZorseTrainer(plan, ctx, CFG, world_rank=rank, world_size=world,
-                      schedule=SCHED.get(name, "gpipe"), collectives=coll)
+                      schedule=SCHED.get(name, "gpipe"))
     tr.exec.capture_grads = True
-    params = gpt_cpu.init_params(CFG, 1234)
-    state = {}
-    ok = True
-    worst = {"loss": 0.0, "grad": 0.0, "cos": 1.0, "param": 0.0, "worst_unit": None}
+    orc = parity.OracleRun(CFG) if rank == 0 else None
+    records, losses = [], []
     for step in (1, 2):
         batch = synthetic_batch(CFG.vocab, CFG.seq_len, gb, step)
         if step == 2 and graph:
             tr.capture()      # step 2 replays a CUDA graph of the whole step
+        before = parity.snapshot(tr.exec)
         loss = tr.step(batch.pin_memory())
-        ref_loss, grads = gpt_cpu.loss_and_grads(CFG, params, batch)
-        gpt_cpu.adamw(params, grads, state, step)
-        worst["loss"] = max(worst["loss"], abs(loss - ref_loss) / ref_loss)
-        for u, g in tr.exec.captured.items():
-            pu = tr.exec.units[u]
-            ref = grads[u][pu.lo:pu.hi]
-            rel = ((g.cpu() - ref).norm() / (ref.norm() + 1e-12)).item()
-            cos = torch.nn.functional.cosine_similarity(g.cpu().double(), ref.double(), dim=0).item()
-            if rel > worst["grad"]:
-                worst["grad"], worst["worst_unit"] = rel, str(u)
-            worst["cos"] = min(worst["cos"], cos)
-    for u, pu in tr.exec.units.items():
-        err = (pu.master.cpu() - params[u][pu.lo:pu.hi]).abs().max().item()
-        worst["param"] = max(worst["param"], err)
-    # bf16 storage / fp32 accumulate vs the fp32 oracle; small uneven shards of
-    # norm weights accumulate the most rounding (DESIGN.md §3 tolerances)
-    ok = (worst["loss"] < 1e-2 and worst["grad"] < 5e-2 and worst["cos"] > 0.998
-          and worst["param"] < 5e-3)
-    print(json.dumps({"layout": name, "collectives": coll, "graph": graph, "rank": rank, "dev": tr.dev_id, "group": tr.exec.gi,
-                      "share": tr.exec.share, "units": len(tr.exec.units), "ok": ok, **worst}),
-          flush=True)
+        rec = parity.executor_step_record(tr.exec, loss, before)
+        allrec = [None] * world if rank == 0 else None
+        dist.gather_object(rec, allrec, dst=0)
+        if rank == 0:
+            pairs, recs = parity.check_step(CFG, orc, batch, step, allrec)
+            losses += [(step, a, b) for a, b in pairs]
+            records += recs
+    ok = True
+    if rank == 0:
+        ok = all(parity.loss_ok(a, b, st) for st, a, b in losses) and not parity.failures(records)
+        print(json.dumps({"layout": name, "graph": graph, "world": world, "ok": ok,
+                          "loss_rel": max(abs(a - b) / abs(b) for _, a, b in losses),
+                          **parity.worst(records),
+                          "failures": parity.failures(records)[:4]}, default=str), flush=True)
+    flag = [ok]
+    dist.broadcast_object_list(flag, src=0)
     dist.barrier()
     dist.destroy_process_group()
-    sys.exit(0 if ok else 1)
+    sys.exit(0 if flag[0] else 1)
 
 
 if __name__ == "__main__":

@@ -104,7 +104,7 @@ def xent_fwd_bwd(logits, labels, loss_sum, dlogits, scale):
     dlogits.copy_(p * scale * ok[:, None])
 
 
-def bias_grad(dy, db, beta=1.0):
+def bias_grad(dy, db):
     db += dy.float().sum(0)
 
 

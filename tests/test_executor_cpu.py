@@ -17,7 +17,7 @@ import torch.multiprocessing as mp
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import cpu_ops  # noqa: E402
 
-from oracle import gpt_cpu  # noqa: E402
+from oracle import parity  # noqa: E402
 from paper_2507_10392_b200 import plan as P  # noqa: E402
 from paper_2507_10392_b200.plan import emulated as E  # noqa: E402
 from paper_2507_10392_b200.runtime.data import synthetic_batch  # noqa: E402
@@ -42,49 +42,33 @@ def _setup(nodes, groups, n_mb, counts, strategy, cfg=None):
     return plan, ctx
 
 
-def _oracle(steps, cfg=None):
-    cfg = cfg or CFG
-    batches = [synthetic_batch(cfg.vocab, cfg.seq_len, GB, s) for s in range(1, steps + 1)]
-    params = gpt_cpu.init_params(cfg, 1234)
-    state, losses, grads = {}, [], None
-    for step, b in enumerate(batches, start=1):
-        loss, grads = gpt_cpu.loss_and_grads(cfg, params, b)
-        losses.append(loss)
-        gpt_cpu.adamw(params, grads, state, step)
-    return losses, params, grads
-
-
-def _rel(a, b):
-    return ((a - b).norm() / (b.norm() + 1e-12)).item()
-
-
 def _run_rank(trainer, steps):
-    trainer.exec.capture_grads = True
-    cfg = trainer.exec.cfg
-    losses = []
-    for s in range(1, steps + 1):
-        losses.append(trainer.step(synthetic_batch(cfg.vocab, cfg.seq_len, GB, s)))
+    """Per step, this rank's record for oracle/parity.check_step."""
     ex = trainer.exec
-    return {"losses": losses,
-            "shards": {u: (pu.lo, pu.hi, pu.master.clone(), ex.captured[u].clone())
-                       for u, pu in ex.units.items()}}
+    ex.capture_grads = True
+    cfg = ex.cfg
+    out = []
+    for s in range(1, steps + 1):
+        before = parity.snapshot(ex)
+        loss = trainer.step(synthetic_batch(cfg.vocab, cfg.seq_len, GB, s))
+        out.append(parity.executor_step_record(ex, loss, before))
+    return out
 
 
 def _check(results, steps, cfg=None):
-    ref_losses, ref_params, ref_grads = _oracle(steps, cfg)
-    for r in results:
-        for got, want in zip(r["losses"], ref_losses):
-            assert abs(got - want) / abs(want) < 1e-2, (got, want)
-    covered = {}
-    for r in results:
-        for u, (lo, hi, master, grad) in r["shards"].items():
-            covered.setdefault(u, []).append((lo, hi))
-            assert _rel(grad, ref_grads[u][lo:hi]) < 3e-2, f"grad {u}[{lo}:{hi}]"
-            assert (master - ref_params[u][lo:hi]).abs().max().item() < 2.5e-3 * steps, f"param {u}"
-    for u, spans in covered.items():  # shards tile every flat buffer exactly once
-        spans.sort()
-        assert spans[0][0] == 0 and all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
-        assert spans[-1][1] == ref_params[u].numel()
+    """Assemble every unit from the ranks' shards (they must tile it exactly once)
+    and compare tensor by tensor with the oracle (oracle/parity.py tolerances)."""
+    cfg = cfg or CFG
+    orc = parity.OracleRun(cfg)
+    records = []
+    for step in range(1, steps + 1):
+        b = synthetic_batch(cfg.vocab, cfg.seq_len, GB, step)
+        losses, recs = parity.check_step(cfg, orc, b, step, [r[step - 1] for r in results])
+        for got, ref in losses:
+            assert parity.loss_ok(got, ref, step), (step, got, ref)
+        records += recs
+    bad = parity.failures(records)
+    assert not bad, parity.describe(records)
 
 
 @pytest.mark.parametrize("n_mb,counts,strategy", [(1, [1], "zorse"), (2, [4], "zorse"),
@@ -139,10 +123,8 @@ def _worker(rank, world, port, spec, q, cfg=None, schedule="gpipe", fused=False)
             return world_c, group
         tr = ZorseTrainer(plan, ctx, cfg or CFG, world_rank=rank, world_size=world, _ops=cpu_ops,
                           _comms=comms, schedule=schedule)
-        res = _run_rank(tr, 2)
-        # ship plain numpy (tensors in a Queue are shared by fd and die with the worker)
-        res["shards"] = {u: (lo, hi, m.numpy(), g.numpy()) for u, (lo, hi, m, g) in res["shards"].items()}
-        q.put((rank, res))
+        # plain numpy (tensors in a Queue are shared by fd and die with the worker)
+        q.put((rank, _run_rank(tr, 2)))
     except Exception as exc:  # surface worker failures to the parent
         import traceback
         q.put((rank, traceback.format_exc()))
@@ -178,9 +160,6 @@ def _run_gloo(spec, world, cfg=None, schedule="gpipe", fused=False):
         p.join(timeout=60)
     errs = [r for r in results.values() if isinstance(r, str)]
     assert not errs, errs[0]
-    for r in results.values():
-        r["shards"] = {u: (lo, hi, torch.from_numpy(m), torch.from_numpy(g))
-                       for u, (lo, hi, m, g) in r["shards"].items()}
     _check(list(results.values()), 2, cfg)
 
 
@@ -224,3 +203,45 @@ def test_1f1b_schedule_shape():
         counts = sched.collective_counts()[gi]
         assert counts == {"allgather": 2 * plan.groups[gi].layers_assigned * 4,
                           "reduce_scatter": plan.groups[gi].layers_assigned}
+
+
+def _faulty(name, wrap):
+    """A copy of the CPU twin with one op wrapped (mutation test of the checker)."""
+    import types
+    m = types.ModuleType("cpu_ops_faulty")
+    m.__dict__.update(cpu_ops.__dict__)
+    setattr(m, name, wrap(getattr(cpu_ops, name)))
+    return m
+
+
+def _ln_weight_grad_scaled(f):   # LayerNorm dw 3% low: hid inside a unit's norm before
+    def g(dy, x, w, mean, rstd, dx, dw, db, *a, **kw):
+        before = dw.clone()
+        f(dy, x, w, mean, rstd, dx, dw, db, *a, **kw)
+        dw.copy_(before + 0.97 * (dw - before))
+    return g
+
+
+def _bias_grad_dropped(f):       # fc1 / qkv bias gradient lost
+    return lambda dy, db: None
+
+
+def _adam_no_bias_correction(f):  # bias-corrected first moment replaced by the raw one
+    def g(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, lr, b1, b2, eps, wd, scale, step):
+        f(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, lr * (1 - b1), b1, b2, eps,
+          wd / (1 - b1), scale, step)
+    return g
+
+
+@pytest.mark.parametrize("name,wrap", [("layernorm_bwd", _ln_weight_grad_scaled),
+                                       ("bias_grad", _bias_grad_dropped),
+                                       ("adamw_shard", _adam_no_bias_correction)],
+                         ids=["ln-dw-3pct", "bias-grad-dropped", "adam-bias-correction"])
+def test_parity_checker_catches_faults(name, wrap):
+    """The per-tensor checks (oracle/parity.py) reject faults that the round-1 per-unit
+    gradient bound let through: a 3% error in LayerNorm weight gradients, a dropped
+    bias gradient, a wrong Adam step size."""
+    plan, ctx = _setup([("n0", ["b200"])], [["n0-0"]], 1, [1], "zorse")
+    tr = ZorseTrainer(plan, ctx, CFG, _ops=_faulty(name, wrap))
+    with pytest.raises(AssertionError):
+        _check([_run_rank(tr, 2)], 2)

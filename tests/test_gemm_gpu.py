@@ -72,13 +72,12 @@ def test_gemm_wgrad_layout_f32_accumulate(cuda, M, N, Kd):
 
 
 @pytest.fixture(params=["tma", "direct"])
-def epi_path(request, monkeypatch):
-    """Run with the TMA-store epilogue (default) and with the direct-store fallback."""
+def epi_path(request):
+    """GEMM entry for the TMA-store epilogue (default path) and for the direct-store
+    epilogue (explicit tile request)."""
     if request.param == "direct":
-        monkeypatch.setenv("ZB_GEMM_NO_TMA_EPI", "1")
-    else:
-        monkeypatch.delenv("ZB_GEMM_NO_TMA_EPI", raising=False)
-    return request.param
+        return lambda *a, **kw: K.gemm_tile(*a, tma_epi=False, **kw)
+    return K.gemm
 
 
 @pytest.mark.parametrize("M,N,Kd", [(512, 1536, 384), (200, 136, 72), (130, 328, 96),
@@ -90,18 +89,18 @@ def test_gemm_epilogues(cuda, epi_path, M, N, Kd):
     bias = _rand(N)
     acc = a.float() @ b.float().t()
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    K.gemm(a, b, out, epilogue=K.EPI_BIAS, bias=bias)
+    epi_path(a, b, out, epilogue=K.EPI_BIAS, bias=bias)
     _close(out, acc + bias.float())
     aux = torch.empty_like(out)
-    K.gemm(a, b, out, epilogue=K.EPI_BIAS_GELU, bias=bias, aux=aux)
+    epi_path(a, b, out, epilogue=K.EPI_BIAS_GELU, bias=bias, aux=aux)
     _close(aux, acc + bias.float())
     _close(out, _gelu(aux.float()))
     r = _rand(M, N)
-    K.gemm(a, b, out, epilogue=K.EPI_BIAS_RESID, bias=bias, resid=r)
+    epi_path(a, b, out, epilogue=K.EPI_BIAS_RESID, bias=bias, resid=r)
     _close(out, acc + bias.float() + r.float())
-    K.gemm(a, b, out, epilogue=K.EPI_GELU_BWD, aux=aux)
+    epi_path(a, b, out, epilogue=K.EPI_GELU_BWD, aux=aux)
     _close(out, acc * _gelu_grad(aux.float()))
-    K.gemm(a, b, out, epilogue=K.EPI_BIAS_GELU_NA, bias=bias)
+    epi_path(a, b, out, epilogue=K.EPI_BIAS_GELU_NA, bias=bias)
     _close(out, _gelu((acc + bias.float()).bfloat16().float()))
     torch.cuda.synchronize()
 
@@ -114,12 +113,12 @@ def test_gemm_f32_store_and_accumulate(cuda, epi_path, M, N, Kd):
     x = _rand(Kd, N)
     prod = dy.float().t() @ x.float()
     c = torch.full((M, N), 7.0, device="cuda")
-    K.gemm(dy, x, c, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=0.0)
+    epi_path(dy, x, c, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=0.0)
     torch.cuda.synchronize()
     _close(c, prod, tol=1e-3)
     c2 = torch.randn(M, N, device="cuda")
     ref = c2 + prod
-    K.gemm(dy, x, c2, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=1.0)
+    epi_path(dy, x, c2, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=1.0)
     torch.cuda.synchronize()
     _close(c2, ref, tol=1e-3)
 
@@ -128,26 +127,25 @@ def test_gemm_f32_store_and_accumulate(cuda, epi_path, M, N, Kd):
 @pytest.mark.parametrize("ctas", ["1", "2"])
 @pytest.mark.parametrize("M,N,Kd,lay", [(1000, 392, 4096, "dgrad"), (640, 264, 2048, "tn"),
                                         (2944, 384, 1024, "wgrad")])
-def test_gemm_tile_rasters(cuda, monkeypatch, raster, ctas, M, N, Kd, lay):
+def test_gemm_tile_rasters(cuda, raster, ctas, M, N, Kd, lay):
     """Both tile rasters (M-fastest; N-fastest, used when A outgrows L2) and both CTA
-    modes, on ragged shapes, against torch fp32 (ZB_GEMM_RASTER / ZB_GEMM_CTAS pin them)."""
-    monkeypatch.setenv("ZB_GEMM_RASTER", raster)
-    monkeypatch.setenv("ZB_GEMM_CTAS", ctas)
+    modes, on ragged shapes, against torch fp32 (pinned through zb_gemm_bf16_tile)."""
+    tile = dict(raster=int(raster), pair=int(ctas) - 1)
     torch.manual_seed(5)
     if lay == "tn":
         a, b = _rand(M, Kd), _rand(N, Kd)
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        K.gemm(a, b, out)
+        K.gemm_tile(a, b, out, **tile)
         ref = a.float() @ b.float().t()
     elif lay == "dgrad":
         a, b = _rand(M, Kd), _rand(Kd, N)
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        K.gemm(a, b, out, b_t=True)
+        K.gemm_tile(a, b, out, **tile, b_t=True)
         ref = a.float() @ b.float()
     else:
         a, b = _rand(Kd, M), _rand(Kd, N)
         out = torch.full((M, N), 0.5, device="cuda")
-        K.gemm(a, b, out, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=1.0)
+        K.gemm_tile(a, b, out, **tile, a_t=True, b_t=True, epilogue=K.EPI_F32, beta=1.0)
         ref = 0.5 + a.float().t() @ b.float()
     torch.cuda.synchronize()
     _close(out, ref, tol=1e-3 if lay == "wgrad" else 2e-2)
@@ -157,14 +155,13 @@ def test_gemm_tile_rasters(cuda, monkeypatch, raster, ctas, M, N, Kd, lay):
 @pytest.mark.parametrize("M,N,Kd,lay,epi", [(512, 512, 256, "tn", 0), (1000, 768, 3072, "tn", 3),
                                             (8192, 3072, 768, "tn", 7), (1024, 1024, 2048, "dgrad", 0),
                                             (2304, 1024, 4096, "wgrad", 5), (768, 1536, 768, "tn", 2)])
-def test_gemm_multicast_pairs(cuda, monkeypatch, bn, M, N, Kd, lay, epi):
+def test_gemm_multicast_pairs(cuda, bn, M, N, Kd, lay, epi):
     """Two CTA pairs per cluster sharing the A tile through TMA multicast
-    (ZB_GEMM_CTAS=4), every layout and the epilogue families, vs torch fp32."""
+    (pair=2), every layout and the epilogue families, vs torch fp32."""
     n_tiles = (N + int(bn) - 1) // int(bn)
     if n_tiles % 2 or (lay != "tn" and bn == "192"):
         pytest.skip("multicast pairs need an even n-tile count (MN-major B: BN 256)")
-    monkeypatch.setenv("ZB_GEMM_CTAS", "4")
-    monkeypatch.setenv("ZB_GEMM_BN", bn)
+    tile = dict(pair=2, bn=int(bn))
     torch.manual_seed(7)
     bias = _rand(N, scale=0.5)
     if lay == "tn":
@@ -181,24 +178,24 @@ def test_gemm_multicast_pairs(cuda, monkeypatch, bn, M, N, Kd, lay, epi):
         kw = {"a_t": True, "b_t": True}
     if epi == 5:
         out = torch.full((M, N), 0.25, device="cuda")
-        K.gemm(a, b, out, epilogue=5, beta=1.0, **kw)
+        K.gemm_tile(a, b, out, **tile, epilogue=5, beta=1.0, **kw)
         torch.cuda.synchronize()
         _close(out, ref + 0.25, tol=1e-3)
         return
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     if epi == 0:
-        K.gemm(a, b, out, **kw)
+        K.gemm_tile(a, b, out, **tile, **kw)
         exp = ref
     elif epi == 3:
         r = _rand(M, N)
-        K.gemm(a, b, out, epilogue=3, bias=bias, resid=r, **kw)
+        K.gemm_tile(a, b, out, **tile, epilogue=3, bias=bias, resid=r, **kw)
         exp = ref + bias.float() + r.float()
     elif epi == 7:
-        K.gemm(a, b, out, epilogue=7, bias=bias, **kw)
+        K.gemm_tile(a, b, out, **tile, epilogue=7, bias=bias, **kw)
         exp = _gelu(ref + bias.float())
     else:  # 2: pre-activation to aux, GELU to out
         aux = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        K.gemm(a, b, out, epilogue=2, bias=bias, aux=aux, **kw)
+        K.gemm_tile(a, b, out, **tile, epilogue=2, bias=bias, aux=aux, **kw)
         torch.cuda.synchronize()
         _close(aux, ref + bias.float())
         exp = _gelu(ref + bias.float())

@@ -124,19 +124,21 @@ def _attn_ref(qkv, n_seq, S, H, D):
     return o.transpose(1, 2).reshape(n_seq * S, H * D), lse
 
 
-@pytest.mark.parametrize("impl", ["tc", "tc-fused-dq", "mma"])
+@pytest.mark.parametrize("bwd", ["two-pass", "fused-dq"])
 @pytest.mark.parametrize("n_seq,S,H,D", [(2, 128, 4, 64), (1, 1024, 3, 64), (2, 256, 2, 128),
-                                         (1, 2048, 2, 128), (3, 512, 12, 64)])
-def test_attention_fwd_bwd(cuda, n_seq, S, H, D, impl):
-    fused = impl == "tc-fused-dq"
-    impl = "tc" if fused else impl
+                                         (1, 2048, 2, 128), (3, 512, 12, 64), (1, 384, 2, 128)])
+def test_attention_fwd_bwd(cuda, n_seq, S, H, D, bwd):
+    """tcgen05 attention vs torch fp32: forward kernels by S % 256 (query-tile pairs,
+    else the 2-CTA/SM (D 64) or single-tile (D 128) kernel); backward fused (dQ
+    reduce-added, D = 64) or two passes."""
+    fused = bwd == "fused-dq"
     torch.manual_seed(4)
     T = n_seq * S
     qkv = torch.randn(T, 3 * H * D, device="cuda").bfloat16()
     out = torch.empty(T, H * D, device="cuda", dtype=torch.bfloat16)
     lse = torch.empty(n_seq, H, S, device="cuda")
     scale = 1.0 / math.sqrt(D)
-    K.attn_fwd(qkv, out, lse, n_seq, S, H, D, scale, impl=impl)
+    K.attn_fwd(qkv, out, lse, n_seq, S, H, D, scale)
     qf = qkv.float().requires_grad_()
     ro, rlse = _attn_ref(qf, n_seq, S, H, D)
     torch.cuda.synchronize()
@@ -146,9 +148,8 @@ def test_attention_fwd_bwd(cuda, n_seq, S, H, D, impl):
     ro.backward(dout.float())
     dqkv = torch.empty_like(qkv)
     delta = torch.empty(n_seq, H, S, device="cuda")
-    # tc + dq_accum: single fused pass at D = 64 (dQ by fp32 reduce-add)
     dq_acc = torch.empty(T, H * D, device="cuda") if fused else None
-    K.attn_bwd(qkv, out, dout, lse, dqkv, dq_acc, delta, n_seq, S, H, D, scale, impl=impl)
+    K.attn_bwd(qkv, out, dout, lse, dqkv, dq_acc, delta, n_seq, S, H, D, scale)
     torch.cuda.synchronize()
     g = qf.grad.view(T, 3, H * D)
     d = dqkv.view(T, 3, H * D)

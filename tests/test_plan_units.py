@@ -166,7 +166,7 @@ def test_native_min_cut_matches_numpy_twin():
     min_cut_kernel) is bit-identical to the numpy restatement, ties included."""
     import numpy as np
     from paper_2507_10392_b200.plan import mincut as MC
-    if MC._NATIVE is None:
+    if MC.native_kernel() is None:
         pytest.skip("library not built")
     rng = np.random.default_rng(7)
     for trial in range(200):

@@ -1,12 +1,14 @@
 """End-to-end training steps on one B200 through the product path (C-ABI
-kernels), against the CPU fp32 oracle.  Tolerances (bf16 storage, fp32
-accumulate): loss rel <= 1e-2; per-unit gradient rel-L2 <= 3e-2; master params
-after 2 AdamW steps within 2*2.5e-3 absolute (lr 1e-3 => <= ~1.25 lr per step)."""
+kernels), against the CPU fp32 oracle, tensor by tensor (oracle/parity.py):
+step-1 loss rel <= 2e-3 (later steps 1e-2); every named tensor's reduced gradient
+rel-L2 <= 2e-2 with cosine >= 0.999; >= 99% of the above-noise-floor elements of
+every tensor's fp32 master update within 0.05*lr of the oracle's update; exp_avg
+rel-L2 <= 2e-2."""
 
 import pytest
 import torch
 
-from oracle import gpt_cpu
+from oracle import parity
 from paper_2507_10392_b200 import plan as P
 from paper_2507_10392_b200.plan import emulated as E
 from paper_2507_10392_b200.runtime.data import synthetic_batch
@@ -26,8 +28,21 @@ def _setup(cfg, gb, n_mb, counts, strategy):
     return plan, ctx
 
 
-def _rel(a, b):
-    return ((a - b).norm() / (b.norm() + 1e-12)).item()
+def run_and_compare(tr, cfg, batches, lr=1e-3):
+    """Steps the trainer and the oracle side by side (oracle synced to the product's
+    state before each step); returns (loss triples, per-tensor records)."""
+    ex = tr.exec
+    ex.capture_grads = True
+    orc = parity.OracleRun(cfg)
+    losses, records = [], []
+    for step, b in enumerate(batches, start=1):
+        before = parity.snapshot(ex)
+        loss = tr.step(b.pin_memory())
+        pairs, recs = parity.check_step(cfg, orc, b, step,
+                                        [parity.executor_step_record(ex, loss, before)], lr)
+        losses += [(step, got, ref) for got, ref in pairs]
+        records += recs
+    return losses, records
 
 
 @pytest.mark.parametrize("cfg,gb,n_mb,counts,strategy,offload", [
@@ -49,24 +64,9 @@ def test_training_steps_match_oracle(cuda, cfg, gb, n_mb, counts, strategy, offl
     plan, ctx = _setup(cfg, gb, n_mb, counts, strategy)
     tr = ZorseTrainer(plan, ctx, cfg, offload_acts=offload)
     assert tr.exec.offload == offload
-    tr.exec.capture_grads = True
     batches = [synthetic_batch(cfg.vocab, cfg.seq_len, gb, s) for s in (1, 2)]
-    params = gpt_cpu.init_params(cfg, 1234)
-    state = {}
-    for step, b in enumerate(batches, start=1):
-        loss = tr.step(b.pin_memory())
-        ref_loss, ref_grads = gpt_cpu.loss_and_grads(cfg, params, b)
-        gpt_cpu.adamw(params, ref_grads, state, step)
-        assert abs(loss - ref_loss) / ref_loss < 1e-2, (step, loss, ref_loss)
-        wide = cfg.d_model >= 4096
-        for u, g in tr.exec.captured.items():
-            r = _rel(g.cpu(), ref_grads[u])
-            if wide and step > 1:
-                cos = torch.nn.functional.cosine_similarity(g.cpu().flatten(),
-                                                            ref_grads[u].flatten(), dim=0).item()
-                assert r < 5e-2 and cos >= 0.998, (step, u, r, cos)
-            else:
-                assert r < 3e-2, (step, u, r)
-    for u, pu in tr.exec.units.items():
-        err = (pu.master.cpu() - params[u]).abs().max().item()
-        assert err < 5e-3, (u, err)
+    losses, records = run_and_compare(tr, cfg, batches)
+    for step, loss, ref in losses:
+        assert parity.loss_ok(loss, ref, step), (step, loss, ref)
+    bad = parity.failures(records)
+    assert not bad, parity.describe(records)
