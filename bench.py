@@ -235,18 +235,22 @@ def measure_collectives(trainer, dist, iters=20):
     import types
     ex = trainer.exec
     comm = ex.group_comm
-    if comm is None or not getattr(comm, "fused_optimizer", False):
+    if comm is None:
         return None
-    key = max(ex.units, key=lambda k: ex.units[k].layout.numel)
+    key = max(ex.units, key=lambda k: ex.units[k].numel)
     pu = ex.units[key]
     g = len(pu.counts)
-    P = pu.layout.numel
+    P = pu.numel
     shard = pu.hi - pu.lo
-    scratch = types.SimpleNamespace(
-        grad_off=pu.grad_off, flag_off=pu.flag_off, lo=pu.lo, hi=pu.hi, grad=pu.grad,
-        master=pu.master.clone(), exp_avg=pu.exp_avg.clone(), exp_avg_sq=pu.exp_avg_sq.clone(),
-        full=torch.empty_like(pu.full))
-    sumsq = torch.zeros(1, device=pu.grad.device)
+    stage = next(s for s, units in ex.chunks.items() if key in units)
+    goff = ex.grad_lo + ex.win.grad_slot[stage] * ex.grad_slot_bytes + ex._grad_unit_off[key]
+    full = torch.empty(P, device=pu.master.device, dtype=torch.bfloat16)   # window slot stand-in
+    scratch = types.SimpleNamespace(   # the unit's gradient slot (same offset on every rank)
+        grad_off=goff, flag_off=pu.flag_off, lo=pu.lo, hi=pu.hi,
+        grad=ex.arena.view(goff, P, torch.float32), master=pu.master.clone(),
+        exp_avg=pu.exp_avg.clone(), exp_avg_sq=pu.exp_avg_sq.clone(),
+        shard=torch.empty_like(pu.shard))
+    sumsq = torch.zeros(1, device=pu.master.device)
 
     def timeit(fn):
         for _ in range(3):
@@ -268,7 +272,7 @@ def measure_collectives(trainer, dist, iters=20):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
-    ag_ms = timeit(lambda: comm.allgather_unit(pu))
+    ag_ms = timeit(lambda: comm.gather(pu, full, ex.step_dev))
     rs_ms = timeit(lambda: comm.reduce_scatter_adamw(scratch, ex.adam, sumsq, ex.step_dev))
     ag_bytes = maxed((P - shard) * 2)                 # bf16 received from peers
     rs_bytes = maxed((g - 1) * shard * 4)             # fp32 peer slices read

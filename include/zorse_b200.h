@@ -173,22 +173,31 @@ int zb_p2p_group(void* comm, int n, const int* peers, void* const* bufs, const i
 int zb_allreduce_sum(void* comm, void* buf, int64_t count, int dtype, zb_stream_t stream);
 
 /* ---- NVLink peer-memory collectives of one DP group (csrc/peer.cu) ------------------
- * Each rank's arena (per parameter unit: bf16 full, fp32 grad, 16-B flag record
- * {param_ready, grad_ready, done, pad}) is exported once with a CUDA IPC handle;
- * `bases[p]` is rank p's arena base as mapped in this process (bases[me] local).
- * Offsets are byte offsets inside the arena, identical on every rank. */
+ * Each rank exports one arena with a CUDA IPC handle: per parameter unit a 16-byte
+ * flag record {param_ready, grad_ready, done, pad} (same offset on every rank), the
+ * fp32 gradient window slots (same offsets on every rank) and the rank's persistent
+ * bf16 parameter shard (rank-specific offset).  `bases[p]` is rank p's arena base
+ * as mapped in this process (bases[me] local).  Offsets are byte offsets. */
 int zb_ipc_handle_size(void);
 int zb_ipc_get_handle(const void* ptr, void* handle_out, uint64_t* offset_out);
 int zb_ipc_open(const void* handle, void** base_out);
 int zb_ipc_close(void* base);
 /* *flag = *epoch_dev + delta with system-scope release (after a system fence). */
 int zb_peer_signal(void* flag, const void* epoch_dev, int delta, zb_stream_t stream);
+/* Bound of every flag spin (seconds; 0 = unbounded; default 120).  A spin that
+ * exceeds it prints the flag it waited for and traps. */
+int zb_peer_set_timeout(double seconds);
+/* One-CTA kernel: wait until every peer's flag at flag_off >= *epoch_dev + delta
+ * (e.g. param_ready of a unit: the peers finished reading its gradient slot). */
+int zb_peer_wait(void* const* bases, int nranks, int me, uint64_t flag_off,
+                 const void* epoch_dev, int epoch_delta, zb_stream_t stream);
 /* AllGather-v before a layer (replaces the AllGather task, simulate.py:292-328 and
  * :408-446; costs.py:138-149): wait for every peer's param_ready >= *epoch_dev +
- * epoch_delta, then copy peer p's [displs[p], displs[p]+counts[p]) elements into the
- * local buffer at buf_off.  mode 0: copy engines; mode 1: SM pull kernel. */
-int zb_peer_allgather_v(void* const* bases, int nranks, int me, uint64_t buf_off,
-                        int elem_bytes, const int64_t* counts, const int64_t* displs,
+ * epoch_delta, then copy rank p's shard (counts[p] elements at bases[p] +
+ * shard_offs[p]) to dst + displs[p] (local full buffer) for every p.  mode 0: copy
+ * engines; mode 1: SM pull kernel. */
+int zb_peer_allgather_v(void* const* bases, int nranks, int me, const uint64_t* shard_offs,
+                        void* dst, int elem_bytes, const int64_t* counts, const int64_t* displs,
                         uint64_t flag_off, const void* epoch_dev, int epoch_delta, int mode,
                         zb_stream_t stream);
 /* ReduceScatter-v + grad scale + AdamW + bf16 cast in one kernel (replaces the

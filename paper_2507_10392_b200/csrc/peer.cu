@@ -1,10 +1,12 @@
 // Collectives of one uneven ZeRO-3 DP group over NVLink peer memory.
 //
-// Every rank of a group holds the same "arena" layout: per parameter unit (a
-// layer, the embedding, the head) a bf16 `full` buffer, an fp32 `grad` buffer
-// and a 16-byte flag record {param_ready, grad_ready, done_counter, pad}.  The
-// arenas are exchanged once with CUDA IPC handles, so every rank can address
-// every peer's buffers directly through NVSwitch.
+// Every rank of a group exports one "arena" (CUDA IPC handle, mapped once by the
+// other ranks, so every rank addresses every peer's buffers through NVSwitch):
+// per parameter unit (a layer, the embedding, the head) a 16-byte flag record
+// {param_ready, grad_ready, done_counter, pad} and the rank's persistent bf16
+// parameter SHARD; plus the fp32 gradient window slots (full units, assigned
+// identically on every rank of the group).  Gathered full parameters live in
+// local window slots that peers never read.
 //
 // The two per-layer collectives the reference models (hetplan simulate.py:
 // AllGather tasks :292-328 / :408-446, ReduceScatter :523-534, OptimStep
@@ -12,7 +14,7 @@
 //
 //  * AllGather-v (zb_peer_allgather_v): wait until every peer published the
 //    parameter shard of the previous step (param_ready >= epoch - 1), then pull
-//    each peer's shard [displ_p, displ_p + count_p) into the local full buffer
+//    each rank's shard into [displ_p, displ_p + count_p) of a local full buffer
 //    — with the copy engines (mode 0, no SMs taken from the concurrent GEMMs) or
 //    with an SM kernel (mode 1, 16-byte loads, many requests in flight).
 //  * ReduceScatter-v + scale + AdamW + bf16 cast, ONE kernel
@@ -23,17 +25,16 @@
 //    place; the last CTA to finish publishes param_ready = epoch.  The reduced
 //    gradient never round-trips through HBM.
 //
-// Ordering argument (why no "done reading" handshake is needed): a rank
-// overwrites its grad buffer only in the next step's backward of that layer,
-// which follows its next AllGather of the layer, which waits for every peer's
-// param_ready of this step, which each peer publishes only after its fused
-// kernel finished reading.  A rank overwrites its parameter shard only in its
-// fused kernel, which waits for every peer's grad_ready, published only after
-// that peer's backward — hence after its last AllGather of the layer in the
-// step.  Epochs are the device-resident step counter (CUDA-graph safe); flags
-// are monotonic.
+// Ordering: a gradient window slot is handed to another unit only after
+// zb_peer_wait saw every peer's param_ready of the slot's previous unit, which
+// each peer publishes only after its fused kernel finished reading the slot.  A
+// rank overwrites its parameter shard only in its fused kernel, which waits for
+// every peer's grad_ready, published only after that peer's backward — hence
+// after its last AllGather of the layer in the step.  Epochs are the
+// device-resident step counter (CUDA-graph safe); flags are monotonic.
 //
-// All spins are bounded (30 s of %globaltimer) and trap instead of hanging.
+// All spins are bounded (default 120 s of %globaltimer, zb_peer_set_timeout; 0 =
+// unbounded) and trap with a message instead of hanging.
 #include "adam.cuh"
 #include "zb_internal.h"
 
@@ -66,14 +67,16 @@ ZB_DEVICE void st_release_sys(uint32_t* p, uint32_t v) {
 
 ZB_DEVICE void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
+static uint64_t g_timeout_ns = 120ull * 1000000000ull;
+
 // Spin until (int)(*flag - target) >= 0.
 ZB_DEVICE void wait_flag(const uint32_t* flag, uint32_t target, int who, int me,
-                         uint64_t flag_off) {
+                         uint64_t flag_off, uint64_t timeout_ns) {
   if ((int)(ld_acquire_sys(flag) - target) >= 0) return;
   const uint64_t t0 = global_ns();
   while ((int)(ld_acquire_sys(flag) - target) < 0) {
     __nanosleep(64);
-    if (global_ns() - t0 > 30ull * 1000000000ull) {
+    if (timeout_ns && global_ns() - t0 > timeout_ns) {
       printf("zorse peer: rank %d timeout waiting for peer %d flag@%llu >= %u (have %u)\n", me,
              who, (unsigned long long)flag_off, target, ld_acquire_sys(flag));
       __trap();
@@ -83,10 +86,11 @@ ZB_DEVICE void wait_flag(const uint32_t* flag, uint32_t target, int who, int me,
 
 // Threads 0..g-1 of the block wait for peer t's flag; then the whole block proceeds.
 ZB_DEVICE void block_wait_peers(const PeerBases& pb, int g, int me, uint64_t flag_off,
-                                uint32_t target) {
+                                uint32_t target, uint64_t timeout_ns) {
   const int t = threadIdx.x;
   if (t < g && t != me)
-    wait_flag(reinterpret_cast<const uint32_t*>(pb.base[t] + flag_off), target, t, me, flag_off);
+    wait_flag(reinterpret_cast<const uint32_t*>(pb.base[t] + flag_off), target, t, me, flag_off,
+              timeout_ns);
   if (t < g) fence_sys();
   __syncthreads();
 }
@@ -96,13 +100,13 @@ ZB_DEVICE void block_wait_peers(const PeerBases& pb, int g, int me, uint64_t fla
 // both collectives live in this single-CTA kernel, so a rank that runs ahead
 // spins on one SM and never starves its own compute stream.
 __global__ void peer_wait_kernel(PeerBases pb, int g, int me, uint64_t flag_off,
-                                 const int* epoch, int delta, int publish) {
+                                 const int* epoch, int delta, int publish, uint64_t timeout_ns) {
   const uint32_t e = (uint32_t)*epoch;
   if (publish && threadIdx.x == 0) {
     fence_sys();
     st_release_sys(reinterpret_cast<uint32_t*>(pb.base[me] + flag_off), e);
   }
-  block_wait_peers(pb, g, me, flag_off, e + delta);
+  block_wait_peers(pb, g, me, flag_off, e + delta, timeout_ns);
 }
 
 __global__ void peer_signal_kernel(uint32_t* flag, const int* epoch, int delta) {
@@ -111,24 +115,23 @@ __global__ void peer_signal_kernel(uint32_t* flag, const int* epoch, int delta) 
 }
 
 struct Segs {
-  int64_t off[kMaxPeers];  // element offsets
+  uint64_t src[kMaxPeers];  // byte offset of peer p's shard in its arena
+  int64_t off[kMaxPeers];   // element offset of peer p's shard in the full buffer
   int64_t cnt[kMaxPeers];
 };
 
-// SM pull: every peer's segment copied with 16-byte vectors (all segments are
-// 128-B aligned by the shard rule; the tail of the last one is done bytewise).
-__global__ void __launch_bounds__(512) peer_pull_kernel(PeerBases pb, int g, int me,
-                                                         uint64_t buf_off, int elem_bytes,
-                                                         Segs segs, uint64_t flag_off,
-                                                         const int* epoch, int delta) {
-  char* dst_base = pb.base[me] + buf_off;
+// SM pull: every peer's shard copied into the local full buffer with 16-byte
+// vectors (shards are 128-B aligned by the shard rule; the tail of the last one is
+// done bytewise).
+__global__ void __launch_bounds__(512) peer_pull_kernel(PeerBases pb, int g, int me, char* dst_base,
+                                                         int elem_bytes, Segs segs) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   for (int p = 0; p < g; ++p) {
-    if (p == me) continue;
     const int64_t bytes = segs.cnt[p] * elem_bytes;
-    const char* src = pb.base[p] + buf_off + segs.off[p] * elem_bytes;
+    const char* src = pb.base[p] + segs.src[p];
     char* dst = dst_base + segs.off[p] * elem_bytes;
+    if (src == dst) continue;
     const int64_t n16 = bytes >> 4;
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
     uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -271,6 +274,12 @@ typedef CUresult (*GetAddressRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 using namespace zb;
 
+extern "C" int zb_peer_set_timeout(double seconds) {
+  if (!(seconds >= 0.0)) return set_error(ZB_ERR_INVALID, "peer timeout must be >= 0");
+  g_timeout_ns = (uint64_t)(seconds * 1e9);
+  return 0;
+}
+
 extern "C" int zb_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
 
 extern "C" int zb_ipc_get_handle(const void* ptr, void* handle_out, uint64_t* offset_out) {
@@ -313,43 +322,58 @@ extern "C" int zb_peer_signal(void* flag, const void* epoch_dev, int delta, cuda
   return e == cudaSuccess ? 0 : set_cuda_error(e, "peer_signal");
 }
 
-extern "C" int zb_peer_allgather_v(void* const* bases, int g, int me, uint64_t buf_off,
-                                   int elem_bytes, const int64_t* counts, const int64_t* displs,
-                                   uint64_t flag_off, const void* epoch_dev, int epoch_delta,
-                                   int mode, cudaStream_t s) {
+extern "C" int zb_peer_wait(void* const* bases, int g, int me, uint64_t flag_off,
+                            const void* epoch_dev, int epoch_delta, cudaStream_t s) {
   PeerBases pb;
   if (int rc = load_bases(&pb, bases, g, me)) return rc;
+  if (!epoch_dev) return set_error(ZB_ERR_INVALID, "peer wait: NULL epoch");
   if (g == 1) return 0;
+  peer_wait_kernel<<<1, 32, 0, s>>>(pb, g, me, flag_off, (const int*)epoch_dev, epoch_delta, 0,
+                                       g_timeout_ns);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "peer_wait");
+}
+
+extern "C" int zb_peer_allgather_v(void* const* bases, int g, int me, const uint64_t* shard_offs,
+                                   void* dst, int elem_bytes, const int64_t* counts,
+                                   const int64_t* displs, uint64_t flag_off,
+                                   const void* epoch_dev, int epoch_delta, int mode,
+                                   cudaStream_t s) {
+  PeerBases pb;
+  if (int rc = load_bases(&pb, bases, g, me)) return rc;
+  if (!dst || !shard_offs || !counts || !displs || !epoch_dev)
+    return set_error(ZB_ERR_INVALID, "peer allgather: NULL argument");
   Segs segs;
   std::memset(&segs, 0, sizeof(segs));
   for (int p = 0; p < g; ++p) {
+    segs.src[p] = shard_offs[p];
     segs.off[p] = displs[p];
     segs.cnt[p] = counts[p];
-    if (((displs[p] * elem_bytes) & 15) || ((buf_off) & 15))
+    if (((displs[p] * elem_bytes) & 15) || (shard_offs[p] & 15) || ((uintptr_t)dst & 15))
       return set_error(ZB_ERR_INVALID, "peer allgather: segment %d not 16-byte aligned", p);
   }
   cudaError_t e;
-  if (mode == 0) {  // copy engines
-    peer_wait_kernel<<<1, 32, 0, s>>>(pb, g, me, flag_off, (const int*)epoch_dev, epoch_delta, 0);
+  if (g > 1) {
+    peer_wait_kernel<<<1, 32, 0, s>>>(pb, g, me, flag_off, (const int*)epoch_dev, epoch_delta, 0,
+                                       g_timeout_ns);
     if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "peer_wait");
+  }
+  char* d = static_cast<char*>(dst);
+  if (mode == 0) {  // copy engines
     for (int p = 0; p < g; ++p) {
-      if (p == me || counts[p] == 0) continue;
-      const size_t off = buf_off + (size_t)displs[p] * elem_bytes;
-      e = cudaMemcpyAsync(pb.base[me] + off, pb.base[p] + off, (size_t)counts[p] * elem_bytes,
-                          cudaMemcpyDeviceToDevice, s);
+      const char* src = pb.base[p] + shard_offs[p];
+      char* to = d + (size_t)displs[p] * elem_bytes;
+      if (counts[p] == 0 || src == to) continue;
+      e = cudaMemcpyAsync(to, src, (size_t)counts[p] * elem_bytes, cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) return set_cuda_error(e, "peer allgather copy");
     }
     return 0;
   }
-  peer_wait_kernel<<<1, 32, 0, s>>>(pb, g, me, flag_off, (const int*)epoch_dev, epoch_delta, 0);
-  if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "peer_wait");
   int64_t total = 0;
-  for (int p = 0; p < g; ++p)
-    if (p != me) total += counts[p] * elem_bytes;
+  for (int p = 0; p < g; ++p) total += counts[p] * elem_bytes;
   int64_t want = (total / 16 + 2047) / 2048;
   int grid = (int)(want < 1 ? 1 : (want > 64 ? 64 : want));
-  peer_pull_kernel<<<grid, 512, 0, s>>>(pb, g, me, buf_off, elem_bytes, segs, flag_off,
-                                        (const int*)epoch_dev, epoch_delta);
+  peer_pull_kernel<<<grid, 512, 0, s>>>(pb, g, me, d, elem_bytes, segs);
   e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_cuda_error(e, "peer_pull");
 }
@@ -377,7 +401,7 @@ extern "C" int zb_peer_rs_adamw(void* const* bases, int g, int me, uint64_t grad
   __nv_bfloat16* pp = (__nv_bfloat16*)param_bf16;
   float *go = (float*)grad_out, *ss = (float*)sumsq;
   if (g > 1) {  // publish grad_ready = epoch, wait for every peer's
-    peer_wait_kernel<<<1, 32, 0, s>>>(pb, g, me, flag_off + 4, ep, 0, 1);
+    peer_wait_kernel<<<1, 32, 0, s>>>(pb, g, me, flag_off + 4, ep, 0, 1, g_timeout_ns);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "peer_wait");
   }

@@ -107,15 +107,16 @@ def build_comms(dist, world_rank: int, world_size: int, groups_ranks: List[List[
 class PeerGroup:
     """Collectives of one DP group over NVLink peer memory (csrc/peer.cu).
 
-    Every rank's ``Arena`` is exported once with a CUDA IPC handle and mapped by
-    the other ranks of its group.  ``allgather_unit`` is the AllGather-v before a
-    layer (copy engines by default); ``reduce_scatter_adamw`` is ReduceScatter-v +
-    scale + AdamW + bf16 cast in ONE kernel, so the executor skips the separate
-    OptimStep launch for this group (``fused_optimizer``).  Cross-rank ordering
-    uses per-unit flags stamped with the device-resident step counter.
+    Every rank's ``Arena`` (flags, gradient window slots, its bf16 parameter shards)
+    is exported once with a CUDA IPC handle and mapped by the other ranks of its
+    group.  ``gather`` is the AllGather-v of a unit into a local window slot (copy
+    engines by default); ``reduce_scatter_adamw`` is ReduceScatter-v + scale + AdamW +
+    bf16 cast in ONE kernel; ``wait_consumed`` holds a gradient slot until every peer
+    has read it.  Cross-rank ordering uses per-unit flags stamped with the
+    device-resident step counter.
     """
 
-    fused_optimizer = True
+    one_sided = True   # gathers pull peers' shards; a rank that needs nothing skips them
 
     def __init__(self, arena, ranks: List[int], world_rank: int, handles, mode: int = 0):
         self.ranks = list(ranks)
@@ -136,7 +137,6 @@ class PeerGroup:
             self._opened.append(base.value)
             bases.append(base.value + off)
         self.bases = (ctypes.c_void_p * self.nranks)(*bases)
-        self.epoch = None   # device int32 step counter (set by the executor)
 
     @staticmethod
     def build(dist, arena, world_rank: int, groups_ranks: List[List[int]], mode: int = 0):
@@ -162,21 +162,31 @@ class PeerGroup:
     def _unit_arrays(self, pu):
         if pu.peer_cache is None:
             pu.peer_cache = ((ctypes.c_int64 * self.nranks)(*pu.counts),
-                             (ctypes.c_int64 * self.nranks)(*pu.displs))
+                             (ctypes.c_int64 * self.nranks)(*pu.displs),
+                             (ctypes.c_uint64 * self.nranks)(*pu.shard_offs))
         return pu.peer_cache
 
-    def allgather_unit(self, pu) -> None:
-        counts, displs = self._unit_arrays(pu)
+    def gather(self, pu, dst, step_dev) -> None:
+        """AllGather-v of ``pu`` into ``dst`` (full [P] bf16): wait for every peer's
+        parameter shard of the previous step, then copy every rank's shard."""
+        counts, displs, offs = self._unit_arrays(pu)
         _count_launch(1 if self.mode == 0 else 2)   # wait kernel (+ SM pull)
-        call("zb_peer_allgather_v", self.bases, self.nranks, self.rank, pu.full_off, 2, counts,
-             displs, pu.flag_off, self.epoch.data_ptr(), -1, self.mode, self._stream())
+        call("zb_peer_allgather_v", self.bases, self.nranks, self.rank, offs, dst.data_ptr(), 2,
+             counts, displs, pu.flag_off, step_dev.data_ptr(), -1, self.mode, self._stream())
+
+    def wait_consumed(self, pu, delta: int, step_dev) -> None:
+        """Every peer finished reading this rank's gradient slot of ``pu`` (its
+        param_ready >= step + delta)."""
+        _count_launch(1)
+        call("zb_peer_wait", self.bases, self.nranks, self.rank, pu.flag_off,
+             step_dev.data_ptr(), delta, self._stream())
 
     def reduce_scatter_adamw(self, pu, adam, sumsq, step_dev, write_grad: bool = False) -> None:
         grad_out = pu.grad[pu.lo:pu.hi].data_ptr() if write_grad else None
         _count_launch(2)                            # publish+wait kernel, fused kernel
         call("zb_peer_rs_adamw", self.bases, self.nranks, self.rank, pu.grad_off, pu.lo,
-             pu.hi - pu.lo, pu.flag_off, self.epoch.data_ptr(), pu.master.data_ptr(),
-             pu.exp_avg.data_ptr(), pu.exp_avg_sq.data_ptr(), pu.full[pu.lo:pu.hi].data_ptr(),
+             pu.hi - pu.lo, pu.flag_off, step_dev.data_ptr(), pu.master.data_ptr(),
+             pu.exp_avg.data_ptr(), pu.exp_avg_sq.data_ptr(), pu.shard.data_ptr(),
              grad_out, sumsq.data_ptr() if sumsq is not None else None, adam.lr, adam.beta1,
              adam.beta2, adam.eps, adam.weight_decay, 1.0, step_dev.data_ptr(), self._stream())
 

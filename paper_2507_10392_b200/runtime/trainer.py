@@ -26,7 +26,8 @@ class ZorseTrainer:
     def __init__(self, plan: TrainingPlan, ctx: CostContext, cfg: ModelConfig, *,
                  world_rank: int = 0, world_size: int = 1, seed: int = 1234,
                  adam: AdamConfig = AdamConfig(), init_device: str = "cpu",
-                 schedule: str = "gpipe", streams: bool = True, offload_acts: bool = False,
+                 schedule: str = "gpipe", streams: bool = True,
+                 offload_acts: Optional[bool] = None,
                  _ops=None, _comms=None, _device=None):
         devices = list(ctx.graph.vertices)
         if len(devices) != world_size:
@@ -64,7 +65,6 @@ class ZorseTrainer:
             from .comm import PeerGroup
             peer = PeerGroup.build(dist, self.exec.arena, world_rank, groups_ranks)
             if peer is not None:
-                peer.epoch = self.exec.step_dev
                 self.exec.group_comm = peer
         self.loss_buf = torch.zeros(1, device=device, dtype=torch.float32)
 

@@ -197,20 +197,22 @@ class GlooComm:
         self.dist.all_reduce(buf, group=self.pg)
 
 
-class GlooFusedComm(GlooComm):
-    """TEST-ONLY twin of runtime.comm.PeerGroup's interface (fused RS-v + AdamW at the
-    ReduceScatter event, OptimStep skipped), to exercise that executor path on CPU."""
+class GlooGroupComm(GlooComm):
+    """TEST-ONLY twin of runtime.comm.PeerGroup's interface over gloo: gather into a
+    window slot, RS-v + AdamW on this rank's shard at the ReduceScatter event."""
 
-    fused_optimizer = True
+    def gather(self, pu, dst, step_dev):
+        dst[pu.lo:pu.hi].copy_(pu.shard)
+        self.allgather_v(dst, pu.counts, pu.displs)
 
-    def allgather_unit(self, pu):
-        self.allgather_v(pu.full, pu.counts, pu.displs)
+    def wait_consumed(self, pu, delta, step_dev):
+        return None   # gloo collectives are synchronous
 
     def reduce_scatter_adamw(self, pu, adam, sumsq, step_dev, write_grad=False):
         self.reduce_scatter_v(pu.grad, pu.counts, pu.displs)
-        adamw_shard(pu.master, pu.exp_avg, pu.exp_avg_sq, pu.grad[pu.lo:pu.hi],
-                    pu.full[pu.lo:pu.hi], sumsq, adam.lr, adam.beta1, adam.beta2, adam.eps,
-                    adam.weight_decay, 1.0, step_dev)
+        adamw_shard(pu.master, pu.exp_avg, pu.exp_avg_sq, pu.grad[pu.lo:pu.hi], pu.shard,
+                    sumsq, adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay, 1.0,
+                    step_dev)
 
 
 def step_increment(step_dev):

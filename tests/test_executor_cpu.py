@@ -105,7 +105,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, spec, q, cfg=None, schedule="gpipe", fused=False):
+def _worker(rank, world, port, spec, q, cfg=None, schedule="gpipe"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -115,9 +115,8 @@ def _worker(rank, world, port, spec, q, cfg=None, schedule="gpipe", fused=False)
         def comms(groups_ranks):
             world_c = cpu_ops.GlooComm(list(range(world)), rank)
             group = None
-            kind = cpu_ops.GlooFusedComm if fused else cpu_ops.GlooComm
             for ranks in groups_ranks:  # every rank must create every subgroup
-                c = kind(ranks, rank)
+                c = cpu_ops.GlooGroupComm(ranks, rank)
                 if rank in ranks and len(ranks) > 1:
                     group = c
             return world_c, group
@@ -144,11 +143,11 @@ def test_three_ranks_gloo_matches_oracle(spec):
     _run_gloo(spec, 3)
 
 
-def _run_gloo(spec, world, cfg=None, schedule="gpipe", fused=False):
+def _run_gloo(spec, world, cfg=None, schedule="gpipe"):
     ctx_mp = mp.get_context("spawn")
     q = ctx_mp.Queue()
     port = _free_port()
-    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, spec, q, cfg, schedule, fused))
+    procs = [ctx_mp.Process(target=_worker, args=(r, world, port, spec, q, cfg, schedule))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -169,11 +168,11 @@ def _run_gloo(spec, world, cfg=None, schedule="gpipe", fused=False):
     (([("n0", ["b200", "b200", "b200h"])], [["n0-0", "n0-1", "n0-2"]], 2, [1], "pp-zero3"),
      "1f1b"),
 ], ids=["interleaved", "dp3-1f1b"])
-def test_fused_optimizer_path_gloo(spec, schedule):
-    """The executor path of the NVLink peer collectives (RS-v + AdamW fused at the
-    ReduceScatter event, grads cleared after each unit's first gather, OptimStep
-    empty) against the oracle, with a gloo twin of the communicator."""
-    _run_gloo(spec, 3, CFG, schedule, fused=True)
+def test_windows_gloo(spec, schedule):
+    """Parameter / gradient window slots reused across ministages (interleaved
+    stages alternating groups) and the PP_ZERO3 two-layer window under 1F1B,
+    against the oracle, with a gloo twin of the peer communicator."""
+    _run_gloo(spec, 3, CFG, schedule)
 
 
 def test_1f1b_three_stages_llama_gloo():

@@ -83,3 +83,52 @@ def test_boundary_transfers_match_brute_force(case):
                 assert dict(sends) == dict(want)
                 assert dict(recvs) == dict(want)
                 assert sum(want.values()) == plan.microbatch_size * S
+
+
+def _windows(case):
+    from paper_2507_10392_b200.runtime.executor import WindowPlan
+    plan, devices = _plan(case)
+    prof = P.load_cluster_profile(os.path.join(GOLD, case["cluster"]))
+    model, workload = P.load_model_workload(os.path.join(GOLD, case["model"]))
+    ctx = P.CostContext(graph=P.build_cluster_graph(prof), runtime=P.fit_runtime_model(prof),
+                        model=model, workload=workload)
+    sched = P.build_schedule(ctx, plan)
+    order, ranges = plan.global_order(), plan.stage_layer_ranges()
+    for gi, g in enumerate(plan.groups):
+        mine = [s for s in range(len(order)) if order[s][0] == gi]
+        chunks = {s: list(range(*ranges[s])) for s in mine}
+        head = len(order) - 1 if order[-1][0] == gi else None
+        plans = [WindowPlan(sched.stream_for(d), chunks, head, len(g.device_ids) > 1,
+                            plan.strategy.gathers_per_microbatch) for d in g.device_ids]
+        yield plan, gi, sched.stream_for(g.device_ids[0]), plans
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: c["name"])
+def test_window_slots(case):
+    """Window-slot plans (runtime/executor.WindowPlan) for every golden plan: identical
+    on every rank of a group (peers address each other's gradient slots by offset);
+    INTERLEAVED materialises at most two ministages (simulate.py FREEf/FREEb ring,
+    costs.py:566-571); at most two gradient slots; every slot handed over only after
+    its previous holder's release event was issued earlier in the stream."""
+    for plan, gi, events, plans in _windows(case):
+        w = plans[0]
+        for other in plans[1:]:
+            assert (other.grad_slot, other.grad_prev, other.param_slot, other.param_prev) == \
+                (w.grad_slot, w.grad_prev, w.param_slot, w.param_prev)
+        assert w.n_grad_slots <= 2
+        if plan.strategy.offloads and len(plan.groups[gi].device_ids) > 1:
+            assert w.n_param_slots <= 2
+        idx = {e.key: i for i, e in enumerate(events)}
+        for s, (prev, same_step) in w.grad_prev.items():
+            if prev is not None and same_step:
+                head = s == len(plan.global_order()) - 1
+                first = min(i for i, e in enumerate(events) if e.stage == s and
+                            (e.kind == "Bwd" or (e.kind == "Fwd" and head)))
+                last_rs = max(i for i, e in enumerate(events)
+                              if e.kind == "ReduceScatter" and e.stage == prev)
+                assert last_rs < first
+        for key, prev in w.param_prev.items():
+            if prev is not None:
+                free = idx[("FREE" + prev[0], prev[1])]
+                ag = idx[("AG" + key[0], key[1], 0)]
+                assert free < ag
