@@ -75,6 +75,14 @@ def _rnd(x: int) -> int:
     return (x + ALIGN - 1) // ALIGN * ALIGN
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 @dataclass
 class AdamConfig:
     lr: float = 1e-3
@@ -291,6 +299,7 @@ class StageExecutor:
                                  "p2p": torch.cuda.Stream(device=device),
                                  "host": torch.cuda.Stream(device=device)}
             self.gather_stream = torch.cuda.Stream(device=device)
+            self.prep_stream = torch.cuda.Stream(device=device)   # gradient-slot handover
         self.record_timeline = False  # measured Gantt (see measured_timeline)
         self._marks = []
         self.capture_grads = False   # tests: keep each reduced grad shard before Adam
@@ -315,33 +324,35 @@ class StageExecutor:
         if self.has_head:
             specs.append(("head", head_layout(cfg), "head", 0))
             self.chunks[self.n_stages - 1].append("head")
+        # Units are initialised one at a time (the full fp32 init of a unit is a
+        # transient of one unit, never of the stage): shard bounds first, then the
+        # window plan and the arena, then per unit master / shard from its init.
         self.units: Dict[object, ParamUnit] = {}
-        inits = {}
-        for key, layout, kind, idx in specs:
-            inits[key] = init_flat(layout, kind, idx, cfg, seed, device=init_device)
-            name = f"layer{key}" if kind == "layer" else kind
-            self.units[key] = ParamUnit(name, layout, split_flat(layout.numel, shares).bounds,
-                                        self.pos, inits[key], device)
+        bounds = {key: split_flat(layout.numel, shares).bounds for key, layout, _, _ in specs}
         self.win = WindowPlan(self.events, self.chunks,
                               self.n_stages - 1 if self.has_head else None, self.g_size > 1,
                               self.per_layer)
         unit_keys = [k for k, *_ in specs]
-        shard_counts = {k: self.units[k].counts for k in unit_keys}
-        self.grad_slot_bytes = max(sum(_rnd(4 * self.units[u].numel) for u in units)
+        shard_counts = {k: [hi - lo for lo, hi in bounds[k]] for k in unit_keys}
+        numel = {key: layout.numel for key, layout, _, _ in specs}
+        self.grad_slot_bytes = max(sum(_rnd(4 * numel[u]) for u in units)
                                    for units in self.chunks.values())
         self.arena_layouts = [Arena.layout(unit_keys, shard_counts, self.win.n_grad_slots,
                                            self.grad_slot_bytes, r) for r in range(self.g_size)]
         flags, self.grad_lo, shard_off, nbytes = self.arena_layouts[self.pos]
         self.arena = Arena(nbytes, device)
-        for k in unit_keys:
-            pu = self.units[k]
-            pu.flag_off = flags[k]
-            pu.shard_offs = [self.arena_layouts[r][2][k] for r in range(self.g_size)]
-            pu.shard = self.arena.view(shard_off[k], pu.shard_numel, torch.bfloat16)
-            pu.shard.copy_(inits[k][pu.lo:pu.hi].to(device=device, dtype=torch.bfloat16))
+        for key, layout, kind, idx in specs:
+            init = init_flat(layout, kind, idx, cfg, seed, device=init_device)
+            name = f"layer{key}" if kind == "layer" else kind
+            pu = ParamUnit(name, layout, bounds[key], self.pos, init, device)
+            self.units[key] = pu
+            pu.flag_off = flags[key]
+            pu.shard_offs = [self.arena_layouts[r][2][key] for r in range(self.g_size)]
+            pu.shard = self.arena.view(shard_off[key], pu.shard_numel, torch.bfloat16)
+            pu.shard.copy_(init[pu.lo:pu.hi].to(device=device, dtype=torch.bfloat16))
+            del init
             if self.g_size == 1:
                 pu.bind_full(pu.shard)    # single-rank group: the shard is the unit
-        del inits
         self._grad_unit_off: Dict[object, int] = {}    # byte offset inside the chunk's slot
         self._param_unit_off: Dict[object, int] = {}   # element offset inside a param slot
         for s, units in self.chunks.items():
@@ -493,7 +504,7 @@ class StageExecutor:
         start.record(main)
         self._marks = [("start", start)] if timed else []
         streams = {"compute": main, **self.lane_streams}
-        for st in list(self.lane_streams.values()) + [self.gather_stream]:
+        for st in list(self.lane_streams.values()) + [self.gather_stream, self.prep_stream]:
             st.wait_event(start)                     # fork (also joins a graph capture)
         done = self._done                            # task key -> [(stream, event)]
         last = {}
@@ -524,18 +535,19 @@ class StageExecutor:
                 self._marks.append((ev, b0, e))
             done[ev.key] = [(st, e)]
             last[lane] = e
-        gs = torch.cuda.Event()
-        gs.record(self.gather_stream)
-        main.wait_event(gs)
+        for st in (self.gather_stream, self.prep_stream):
+            j = torch.cuda.Event()
+            j.record(st)
+            main.wait_event(j)
         for lane, e in last.items():                 # join
             if lane != "compute":
                 main.wait_event(e)
 
-    def _wait_done(self, keys) -> None:
-        """Make the current stream wait for the completion of task keys."""
+    def _wait_done(self, keys, stream=None) -> None:
+        """Make the current (or the given) stream wait for the completion of task keys."""
         if not self.multistream:
             return
-        st = torch.cuda.current_stream(self.device)
+        st = stream or torch.cuda.current_stream(self.device)
         for k in keys:
             for src, e in self._done.get(k, ()):
                 if src is not st:
@@ -553,23 +565,31 @@ class StageExecutor:
 
     def _acquire_grads(self, s: int) -> None:
         """Bind the chunk's units to their gradient slot and clear it, once the slot's
-        previous holder was reduce-scattered here and read by every peer."""
+        previous holder was reduce-scattered here and read by every peer.  The
+        handover (peer waits + clearing) runs on its own stream, which depends only
+        on the previous holder's ReduceScatter, so it is off the compute path."""
         units = self.chunks[s]
         if self.units[units[0]].grad is not None:
             return
-        prev, same_step = self.win.grad_prev[s]
-        if prev is not None:
-            if same_step:
-                n_rs = self.ranges[prev][1] - self.ranges[prev][0]
-                self._wait_done([("RS", prev, i) for i in range(n_rs)])
-            if self.group_comm is not None:
-                for u in self.chunks[prev]:
-                    self.group_comm.wait_consumed(self.units[u], 0 if same_step else -1,
-                                                  self.step_dev)
         base = self.grad_lo + self.win.grad_slot[s] * self.grad_slot_bytes
         region = self.arena.view(base, self.grad_slot_bytes // 4, torch.float32)
         last = units[-1]
-        region[:self._grad_unit_off[last] // 4 + self.units[last].numel].zero_()
+        used = self._grad_unit_off[last] // 4 + self.units[last].numel
+        prev, same_step = self.win.grad_prev[s]
+        ps = self.prep_stream if self.multistream else None
+        if prev is not None and same_step:
+            n_rs = self.ranges[prev][1] - self.ranges[prev][0]
+            self._wait_done([("RS", prev, i) for i in range(n_rs)], ps)
+        with torch.cuda.stream(ps) if ps is not None else _nullctx():
+            if prev is not None and self.group_comm is not None:
+                for u in self.chunks[prev]:
+                    self.group_comm.wait_consumed(self.units[u], 0 if same_step else -1,
+                                                  self.step_dev)
+            region[:used].zero_()
+        if ps is not None:
+            e = torch.cuda.Event()
+            e.record(ps)
+            torch.cuda.current_stream(self.device).wait_event(e)
         for u in units:
             pu = self.units[u]
             off = self._grad_unit_off[u]

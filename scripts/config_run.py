@@ -67,8 +67,11 @@ def main():
         P.attach_routing(plan, rt, "transformer")
     t0 = time.time()
     tr = ZorseTrainer(plan, ctx, cfg, world_rank=rank, world_size=world, schedule=r["schedule"],
-                      init_device="cuda", offload_acts="--offload" in sys.argv)
+                      init_device="cuda",
+                      offload_acts=False if "--no-offload" in sys.argv else None)
     init_s = time.time() - t0
+    init_peak = torch.cuda.max_memory_allocated() / 2**30
+    torch.cuda.reset_peak_memory_stats()   # the steps' peak, without the one-off init
     batch = synthetic_batch(cfg.vocab, cfg.seq_len, r["gb"], 1, pin=True)
     losses = [tr.step(batch)]  # warm-up
     torch.cuda.synchronize()
@@ -86,6 +89,17 @@ def main():
     mem = torch.cuda.max_memory_allocated() / 2**30
     gmem = torch.tensor([mem], device="cuda")
     dist.all_reduce(gmem, op=dist.ReduceOp.MAX)
+    # per-rank peak vs the plan's Eq.2 estimate (costs.py:538-607, restated bit-exact)
+    est = P.memory_estimate(ctx, plan, tr.exec.gi, tr.dev_id)
+    mine = {"dev": tr.dev_id, "share": tr.exec.share, "max_alloc_gib": mem,
+            "init_peak_gib": init_peak,
+            "executor": {k: (v / 2**30 if isinstance(v, int) and v > 1024 else v)
+                         for k, v in tr.exec.memory_report().items()},
+            "estimate_gib": {"params": est.m_params / 2**30, "grads": est.m_grads / 2**30,
+                             "optim": est.m_optim / 2**30, "activations": est.m_activations / 2**30,
+                             "total": est.m_total / 2**30}}
+    per_rank = [None] * world
+    dist.all_gather_object(per_rank, mine)
     if rank == 0:
         tok = r["gb"] * cfg.seq_len
         print(json.dumps({"offload_acts": tr.exec.offload,
@@ -95,7 +109,8 @@ def main():
             "n_microbatches": plan.n_microbatches, "global_batch": r["gb"], "seq_len": cfg.seq_len,
             "ms_per_step": ms.item(), "tokens_per_s": tok / (ms.item() * 1e-3),
             "model_tflops_per_gpu": cfg.flops_per_token() * tok / (ms.item() * 1e-3) / 1e12 / world,
-            "loss_first_last": losses, "max_mem_gib": gmem.item(), "init_s": init_s}), flush=True)
+            "loss_first_last": losses, "max_mem_gib": gmem.item(), "init_s": init_s,
+            "memory_per_rank": per_rank}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
