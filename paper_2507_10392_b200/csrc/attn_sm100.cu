@@ -840,53 +840,62 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(BQ, BKV, 0, 0);
       constexpr uint32_t idesc_o = umma_idesc_bf16(BQ, D, 0, 1);
-      const uint32_t q_base[2] = {smem_u32(sm + L::OFF_QA), smem_u32(sm + L::OFF_QB)};
+      const uint32_t q_base0 = smem_u32(sm + L::OFF_QA), q_base1 = smem_u32(sm + L::OFF_QB);
+      const uint32_t ts0 = tmem, ts1 = tmem + 128, to0 = tmem + 256, to1 = tmem + 256 + D;
       int g = 0, lt = 0;
-      int ns[2] = {0, 0};  // S blocks issued per tile (parity of p_full waits)
+      int ns0 = 0, ns1 = 0;  // S blocks issued per tile (parity of p_full waits)
+      // (tile index x is a compile-time constant in every call below: no
+      // dynamically indexed local arrays on the issue path)
       for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
         int pr, h, b;
         decode(t, pr, h, b);
         const int qa = 2 * pr, qb = qa + 1;
-        const int last[2] = {qa, qb};
         mbar_wait(q_full, lt & 1);
-        auto issue_s = [&](int x, int j) {  // S_x(j) = Q_x K_j^T
+        auto issue_s = [&](auto xc, int j) {  // S_x(j) = Q_x K_j^T
+          constexpr int x = decltype(xc)::value;
           const int st = (g + j) % NST;
           mbar_wait(&kv_full[st], ((g + j) / NST) & 1);
           tc_fence_after();
           const uint32_t k_base = smem_u32(sm + L::OFF_K + st * L::KV_BYTES);
+          const uint32_t qb_ = x ? q_base1 : q_base0;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
-            mma_bf16_ss(t_s[x], desc_kmajor(q_base[x], kk, BQ), desc_kmajor(k_base, kk, BKV),
+            mma_bf16_ss(x ? ts1 : ts0, desc_kmajor(qb_, kk, BQ), desc_kmajor(k_base, kk, BKV),
                         idesc_s, kk > 0 ? 1u : 0u);
           mma_commit(&s_full[x]);
         };
-        auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P_x from TMEM
+        auto issue_pv = [&](auto xc, int j) {  // O_x += P_x(j) V_j, P_x from TMEM
+          constexpr int x = decltype(xc)::value;
           const int st = (g + j) % NST;
-          mbar_wait(&p_full[x], ns[x] & 1);
-          ++ns[x];
+          int& ns = x ? ns1 : ns0;
+          mbar_wait(&p_full[x], ns & 1);
+          ++ns;
           if (j == 0) mbar_wait(&o_empty[x], (lt & 1) ^ 1);
           tc_fence_after();
           const uint32_t v_base = smem_u32(sm + L::OFF_V + st * L::KV_BYTES);
+          const uint32_t tsx = x ? ts1 : ts0, tox = x ? to1 : to0;
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk) {
             const uint64_t bdesc = umma_desc_sw128(
                 v_base + (kk >> 2) * (D / 64) * 8192 + (kk & 3) * 2048, 8192, 1024);
             // P keys [64h, 64h+64) sit in the S columns of half h (see the softmax)
-            const uint32_t a_tm = HV == 2 ? t_s[x] + (kk >> 2) * 64 + (kk & 3) * 8 : t_s[x] + kk * 8;
-            mma_bf16_ts(t_o[x], a_tm, bdesc, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+            const uint32_t a_tm = HV == 2 ? tsx + (kk >> 2) * 64 + (kk & 3) * 8 : tsx + kk * 8;
+            mma_bf16_ts(tox, a_tm, bdesc, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           }
-          if (j == last[x]) mma_commit(&o_done[x]);
+          if (j == (x ? qb : qa)) mma_commit(&o_done[x]);
         };
-        issue_s(0, 0);
-        issue_s(1, 0);
+        using X0 = std::integral_constant<int, 0>;
+        using X1 = std::integral_constant<int, 1>;
+        issue_s(X0{}, 0);
+        issue_s(X1{}, 0);
         for (int j = 0; j <= qb; ++j) {
           if (j <= qa) {
-            issue_pv(0, j);
-            if (j + 1 <= qa) issue_s(0, j + 1);
+            issue_pv(X0{}, j);
+            if (j + 1 <= qa) issue_s(X0{}, j + 1);
           }
-          issue_pv(1, j);
+          issue_pv(X1{}, j);
           mma_commit(&kv_empty[(g + j) % NST]);  // K_j, V_j no longer read
-          if (j + 1 <= qb) issue_s(1, j + 1);
+          if (j + 1 <= qb) issue_s(X1{}, j + 1);
         }
         mma_commit(q_empty);
         g += qb + 1;
@@ -907,7 +916,7 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
     const float sl2 = scale * LOG2E;
     constexpr float RESCALE_T = 8.f;
     constexpr int NCH = (BKV / 32) / HV;  // 32-column S chunks per warp
-    const uint32_t ts = t_s[x], to = t_o[x];
+    const uint32_t ts = x ? t_s[1] : t_s[0], to = x ? t_o[1] : t_o[0];
     float* xch = reinterpret_cast<float*>(sm + L::OFF_X) + x * 2 * BQ;
     auto pair_sync = [&]() {
       if constexpr (HV == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + x * 4 + wq) : "memory");

@@ -23,6 +23,8 @@ from typing import Dict, List, Optional, Sequence, Tuple
 from .configure import TrainingPlan
 from .costs import CostContext, Strategy, allgather_time, best_cross_link, reduce_scatter_time
 
+CATEGORIES = ("params", "grads", "optim", "activations")   # simulate.py:60
+
 # Tie-break rank of each event kind (simulate.py:47-59).
 KIND_RANK = {
     "AllGather": 0, "P2PRecv": 1, "LoadAct": 2, "Fwd": 3, "Recompute": 4, "Bwd": 5,
@@ -48,6 +50,7 @@ class Task:
     lanes: Tuple[Tuple[str, str], ...]
     deps: Tuple[tuple, ...]
     prio: tuple
+    effects: Tuple[Tuple[str, str, float, str], ...] = ()   # (device, category, delta, at)
 
 
 @dataclass(frozen=True)
@@ -65,6 +68,7 @@ class Event:
     device_ids: Tuple[str, ...]
     lane: str
     deps: Tuple[tuple, ...] = ()
+    effects: Tuple[Tuple[str, str, float, str], ...] = ()
 
 
 class TaskGraph:
@@ -132,8 +136,19 @@ class TaskGraph:
         gi = self.group_of(s)
         return reduce_scatter_time(self.ctx, self.layer_bytes(layer), self.ids(gi))
 
+    def chunk_bytes(self, s: int):
+        return sum(self.layer_bytes(layer) for layer in self.layers(s))
+
+    def z3_window_bytes(self, s: int) -> float:
+        """Materialised-parameter window: the chunk's two largest layers minus the
+        resident shard slice (simulate.py:223-229)."""
+        d_dp = len(self.ids(self.group_of(s)))
+        sizes = sorted((self.layer_bytes(layer) for layer in self.layers(s)), reverse=True)
+        return sum(sizes[:2]) * (1.0 - 1.0 / d_dp)
+
     # ------------------------------------------------------------ emission
-    def add(self, key, kind, stage, microbatch=-1, layer=-1, *, duration, lanes, deps) -> None:
+    def add(self, key, kind, stage, microbatch=-1, layer=-1, *, duration, lanes, deps,
+            effects=()) -> None:
         if key in self.by_key:
             raise SimulationError(f"duplicate task key {key}")
         forward = key[0].endswith("f") or key[0] in _FORWARD_KEYS
@@ -144,7 +159,8 @@ class TaskGraph:
         t = Task(seq=len(self.tasks), key=key, kind=kind,
                  group=self.group_of(stage) if stage >= 0 else -1, stage=stage,
                  microbatch=microbatch, layer=layer, duration=duration, lanes=tuple(lanes),
-                 deps=tuple(deps), prio=(pos, microbatch, KIND_RANK[kind], layer, len(self.tasks)))
+                 deps=tuple(deps), prio=(pos, microbatch, KIND_RANK[kind], layer, len(self.tasks)),
+                 effects=tuple(effects))
         self.by_key[key] = t
         self.tasks.append(t)
 
@@ -153,6 +169,7 @@ class TaskGraph:
         M = plan.n_microbatches
         offload = plan.strategy.offloads
         per_mb = plan.strategy.gathers_per_microbatch
+        k_act = ctx.k_act
         link: Dict[Tuple[int, str], Tuple[str, str, float]] = {}
         for b in range(self.n - 1):
             lo, hi = self.group_of(b), self.group_of(b + 1)
@@ -183,15 +200,20 @@ class TaskGraph:
                             deps = [("F", mine[q - 1], M - 1)]
                         else:
                             deps = []
+                        eff = [(d, "params", self.z3_window_bytes(s), "start")
+                               for d in self.ids(gi)] if i == 0 else []
                         self.add(("AGf", s, i, m), "AllGather", s, m, layer,
-                                 duration=self.ag_time(s, layer), lanes=coll, deps=deps)
+                                 duration=self.ag_time(s, layer), lanes=coll, deps=deps,
+                                 effects=eff)
             else:
                 for i, layer in enumerate(lays):
                     deps = [("AGf", s, i - 1)] if i > 0 else []
                     if offload and q >= 2:
                         deps.append(("FREEf", mine[q - 2]))
+                    eff = [(d, "params", self.layer_bytes(layer), "start")
+                           for d in self.ids(gi)] if offload else []
                     self.add(("AGf", s, i), "AllGather", s, -1, layer,
-                             duration=self.ag_time(s, layer), lanes=coll, deps=deps)
+                             duration=self.ag_time(s, layer), lanes=coll, deps=deps, effects=eff)
             fwd_t = self.compute_time(s, "fwd")
             for m in range(M):
                 deps = ([("AGf", s, i, m) for i in range(len(lays))] if per_mb
@@ -204,11 +226,26 @@ class TaskGraph:
                     p = fwd_slots[gi].index((s, m))
                     if p >= 2:
                         deps.append(("OA",) + fwd_slots[gi][p - 2])
+                eff = []
+                for d in self.ids(gi):
+                    # the materialised window closes on every member, zero-share included
+                    if per_mb:
+                        eff.append((d, "params", -self.z3_window_bytes(s), "end"))
+                    u = self.act_unit(gi, d)
+                    if u == 0:
+                        continue
+                    if offload:
+                        eff.append((d, "activations", (1 + k_act) * u, "start"))
+                    else:
+                        eff.append((d, "activations", (len(lays) + k_act) * u, "start"))
+                    eff.append((d, "activations", -k_act * u, "end"))
                 self.add(("F", s, m), "Fwd", s, m, duration=fwd_t,
-                         lanes=self.lanes(gi, "compute"), deps=deps)
+                         lanes=self.lanes(gi, "compute"), deps=deps, effects=eff)
                 if offload:
                     self.add(("OA", s, m), "OffloadAct", s, m, duration=self.act_transfer_time(gi),
-                             lanes=self.lanes(gi, "host"), deps=[("F", s, m)])
+                             lanes=self.lanes(gi, "host"), deps=[("F", s, m)],
+                             effects=[(d, "activations", -self.act_unit(gi, d), "end")
+                                      for d in self.ids(gi) if self.act_unit(gi, d) > 0])
                 if s + 1 < self.n and self.group_of(s + 1) != gi:
                     src, dst, bw = link[(s, "f")]
                     self.add(("PSf", s, m), "P2PSend", s, m, duration=boundary_bytes / bw,
@@ -217,7 +254,8 @@ class TaskGraph:
                              lanes=((dst, "p2p"),), deps=[("PSf", s, m)])
             if offload:
                 self.add(("FREEf", s), "FreeParams", s, duration=0.0, lanes=(),
-                         deps=[("F", s, M - 1)])
+                         deps=[("F", s, M - 1)],
+                         effects=[(d, "params", -self.chunk_bytes(s), "end") for d in self.ids(gi)])
 
         # ---------------- backward: gathers, reload, recompute, Bwd, RS -----
         for s in reversed(range(self.n)):
@@ -237,8 +275,11 @@ class TaskGraph:
                                 deps.append(("B", s, m - 1))
                             elif r >= 1:
                                 deps.append(("B", chunks[r - 1], M - 1))
+                        eff = [(d, "params", self.z3_window_bytes(s), "start")
+                               for d in self.ids(gi)] if i == 0 else []
                         self.add(("AGb", s, i, m), "AllGather", s, m, layer,
-                                 duration=self.ag_time(s, layer), lanes=coll, deps=deps)
+                                 duration=self.ag_time(s, layer), lanes=coll, deps=deps,
+                                 effects=eff)
             else:
                 for i, layer in enumerate(lays):
                     if i > 0:
@@ -249,16 +290,21 @@ class TaskGraph:
                             deps.append(("FREEb", chunks[r - 2]))
                     else:
                         deps = [("F", s, M - 1)]
+                    eff = [(d, "params", self.layer_bytes(layer), "start")
+                           for d in self.ids(gi)] if offload else []
                     self.add(("AGb", s, i), "AllGather", s, -1, layer,
-                             duration=self.ag_time(s, layer), lanes=coll, deps=deps)
+                             duration=self.ag_time(s, layer), lanes=coll, deps=deps, effects=eff)
             rc_t = self.compute_time(s, "fwd")
             bwd_t = self.compute_time(s, "bwd")
+            grad_bytes = self.chunk_bytes(s) / (len(self.ids(gi)) if per_mb else 1)
             for m in range(M):
                 if offload:
                     p = bwd_slots[gi].index((s, m))
                     deps = [("OA", s, m), ("RC",) + bwd_slots[gi][p - 1] if p >= 1 else ("F", s, M - 1)]
                     self.add(("LA", s, m), "LoadAct", s, m, duration=self.act_transfer_time(gi),
-                             lanes=self.lanes(gi, "host"), deps=deps)
+                             lanes=self.lanes(gi, "host"), deps=deps,
+                             effects=[(d, "activations", self.act_unit(gi, d), "end")
+                                      for d in self.ids(gi) if self.act_unit(gi, d) > 0])
                 deps = [("F", s, m)]
                 if m > 0:
                     deps.append(("B", s, m - 1))
@@ -270,12 +316,20 @@ class TaskGraph:
                     prev = chunks[r - 1]
                     deps.append(("RS", prev, len(self.layers(prev)) - 1))
                 self.add(("RC", s, m), "Recompute", s, m, duration=rc_t,
-                         lanes=self.lanes(gi, "compute"), deps=deps)
+                         lanes=self.lanes(gi, "compute"), deps=deps,
+                         effects=[(d, "activations", k_act * self.act_unit(gi, d), "start")
+                                  for d in self.ids(gi) if self.act_unit(gi, d) > 0])
                 deps = [("RC", s, m)]
                 if s + 1 < self.n:
                     deps.append(("B", s + 1, m) if self.group_of(s + 1) == gi else ("PRb", s, m))
+                eff = [(d, "grads", grad_bytes, "start") for d in self.ids(gi)] if m == 0 else []
+                drop = 1 + k_act if offload else len(lays) + k_act
+                eff += [(d, "activations", -drop * self.act_unit(gi, d), "end")
+                        for d in self.ids(gi) if self.act_unit(gi, d) > 0]
+                if per_mb:
+                    eff += [(d, "params", -self.z3_window_bytes(s), "end") for d in self.ids(gi)]
                 self.add(("B", s, m), "Bwd", s, m, duration=bwd_t,
-                         lanes=self.lanes(gi, "compute"), deps=deps)
+                         lanes=self.lanes(gi, "compute"), deps=deps, effects=eff)
                 if s > 0 and self.group_of(s - 1) != gi:
                     src, dst, bw = link[(s - 1, "b")]
                     self.add(("PSb", s - 1, m), "P2PSend", s, m, duration=boundary_bytes / bw,
@@ -284,11 +338,14 @@ class TaskGraph:
                              lanes=((dst, "p2p"),), deps=[("PSb", s - 1, m)])
             if offload:
                 self.add(("FREEb", s), "FreeParams", s, duration=0.0, lanes=(),
-                         deps=[("B", s, M - 1)])
+                         deps=[("B", s, M - 1)],
+                         effects=[(d, "params", -self.chunk_bytes(s), "end") for d in self.ids(gi)])
             for i, layer in enumerate(lays):
                 deps = [("B", s, M - 1)] + ([("RS", s, i - 1)] if i > 0 else [])
+                eff = [(d, "grads", -grad_bytes, "end") for d in self.ids(gi)] \
+                    if i == len(lays) - 1 else []
                 self.add(("RS", s, i), "ReduceScatter", s, -1, layer,
-                         duration=self.rs_time(s, layer), lanes=coll, deps=deps)
+                         duration=self.rs_time(s, layer), lanes=coll, deps=deps, effects=eff)
 
         # ---------------- per-ministage optimizer -------------------------
         for s in range(self.n):
@@ -430,7 +487,8 @@ def list_schedule(tasks: Sequence[Task], plan: TrainingPlan) -> List[Event]:
         out.append(Event(key=pick.key, kind=pick.kind, group=pick.group, stage=pick.stage,
                          microbatch=pick.microbatch, layer=pick.layer, start=start, end=end,
                          device_ids=tuple(d for d, _ in pick.lanes) or plan.groups[pick.group].device_ids,
-                         lane=pick.lanes[0][1] if pick.lanes else "none", deps=pick.deps))
+                         lane=pick.lanes[0][1] if pick.lanes else "none", deps=pick.deps,
+                         effects=pick.effects))
         for child in children[pick.key]:
             waiting[child.key] -= 1
             if end > earliest[child.key]:
@@ -465,6 +523,14 @@ class Schedule:
                 counts[e.group]["reduce_scatter"] += 1
         return counts
 
+    def memory(self, ctx: CostContext):
+        """(peaks, traces) of the simulator's memory accounting for this schedule."""
+        return memory_replay(ctx, self.plan, self.events)
+
+    def gantt_rows(self):
+        return [(e.start, e.end, e.kind, e.group, e.stage, e.microbatch, e.layer, e.lane,
+                 e.device_ids) for e in self.events]
+
     def group_of_device(self, dev_id: str) -> int:
         for gi, g in enumerate(self.plan.groups):
             if dev_id in g.device_ids:
@@ -496,6 +562,93 @@ class Schedule:
                 if order[peer_stage][0] == gi:
                     out.append(e)  # receiving side of the transfer
         return out
+
+
+def initial_memory(ctx: CostContext, plan: TrainingPlan) -> Dict[str, Dict[str, float]]:
+    """Resident-from-t=0 bytes per device and category (simulate.py:565-588):
+    optimizer shard, persistent gradient buffer, strategy-dependent parameters."""
+    base: Dict[str, Dict[str, float]] = {}
+    elem = ctx.model.bytes_per_element
+    ranges = plan.stage_layer_ranges()
+    order = plan.global_order()
+    for gi, group in enumerate(plan.groups):
+        layers = [layer for idx, (g, _) in enumerate(order) if g == gi
+                  for layer in range(*ranges[idx])]
+        param_count = sum(ctx.model.params_of(layer) for layer in layers)
+        param_bytes = param_count * elem
+        d_dp = group.d_dp
+        for dev in group.devices:
+            state = {c: 0.0 for c in CATEGORIES}
+            state["optim"] = param_count * ctx.workload.optimizer_bytes_per_param / d_dp
+            state["grads"] = param_bytes / d_dp
+            if plan.strategy is Strategy.PP_ZERO2:
+                state["params"] = param_bytes
+            elif plan.strategy is Strategy.PP_ZERO3:
+                state["params"] = param_bytes / d_dp
+            base[dev.id] = state
+    return base
+
+
+def memory_replay(ctx: CostContext, plan: TrainingPlan, events: Sequence[Event]):
+    """The simulator's memory accounting (simulate.py:660-696): apply every event's
+    effects in time order — end-effects before start-effects at equal timestamps —
+    on top of the initial residency.  Returns (peaks {device: {category|total}},
+    traces {device: [(time, params, grads, optim, activations, total)]})."""
+    deltas: Dict[str, List[tuple]] = defaultdict(list)
+    for idx, e in enumerate(events):
+        for dev, cat, delta, at in e.effects:
+            time = e.start if at == "start" else e.end
+            phase = 1 if at == "start" else 0
+            deltas[dev].append((time, phase, idx, cat, delta))
+    base = initial_memory(ctx, plan)
+    peaks: Dict[str, Dict[str, float]] = {}
+    traces: Dict[str, List[tuple]] = {}
+    for group in plan.groups:
+        for dev in group.devices:
+            state = dict(base[dev.id])
+            trace = [(0.0, state["params"], state["grads"], state["optim"],
+                      state["activations"], sum(state.values()))]
+            peak = dict(state)
+            peak["total"] = sum(state.values())
+            for time, _, _, cat, delta in sorted(deltas.get(dev.id, [])):
+                state[cat] += delta
+                total = sum(state.values())
+                trace.append((time, state["params"], state["grads"], state["optim"],
+                              state["activations"], total))
+                for c in CATEGORIES:
+                    peak[c] = max(peak[c], state[c])
+                peak["total"] = max(peak["total"], total)
+            for cat, value in state.items():
+                if value < -1e-6 or (cat in ("params", "activations")
+                                     and abs(value - base[dev.id][cat]) > 1e-6):
+                    raise SimulationError(f"memory accounting leak on {dev.id}/{cat}: "
+                                          f"end state {value}, expected {base[dev.id][cat]}")
+            peaks[dev.id] = peak
+            traces[dev.id] = trace
+    return peaks, traces
+
+
+def write_gantt_csv(path: str, rows) -> None:
+    """Gantt CSV in the reference's columns (simulate.py:115-126); rows are
+    (start, end, kind, group, stage, microbatch, layer, lane, devices)."""
+    import csv
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["start", "end", "kind", "group", "stage", "microbatch", "layer", "lane",
+                    "devices"])
+        for r in rows:
+            w.writerow([repr(r[0]), repr(r[1])] + list(r[2:8]) + [" ".join(r[8])])
+
+
+def write_memory_csv(path: str, traces) -> None:
+    """Memory CSV in the reference's columns (simulate.py:128-137)."""
+    import csv
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["device", "time", "params", "grads", "optim", "activations", "total"])
+        for dev in sorted(traces):
+            for row in traces[dev]:
+                w.writerow([dev] + [repr(v) for v in row])
 
 
 def build_schedule(ctx: CostContext, plan: TrainingPlan, kind: str = "gpipe") -> Schedule:

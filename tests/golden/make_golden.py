@@ -111,8 +111,9 @@ def fixed_layout_case(name, nodes, model_cfg, global_batch, groups, n_mb, counts
     }
 
 
-def planner_case(name, nodes, model_cfg, global_batch, k_max=None, strategies=("zorse",)):
-    prof_json = E.profile_json(nodes)
+def planner_case(name, nodes, model_cfg, global_batch, k_max=None, strategies=("zorse",),
+                 prof_json=None):
+    prof_json = prof_json if prof_json is not None else E.profile_json(nodes)
     _dump(prof_json, f"cluster_{name}.json")
     _dump(model_cfg.model_json(global_batch), f"model_{name}.json")
     profile = load_cluster_profile(os.path.join(HERE, f"cluster_{name}.json"))
@@ -131,6 +132,15 @@ def planner_case(name, nodes, model_cfg, global_batch, k_max=None, strategies=("
         "collective_counts": {str(k): v for k, v in tl.collective_counts.items()},
         "shards": _ref_shards(plan, model.params_of),
     }
+
+
+def measured_profile_case(name, profile_path, model_cfg, global_batch, k_max=None):
+    """plan_training on a cluster profile whose runtime samples were MEASURED on B200
+    (scripts/profile_layers.py; the planner loop closed on real layer timings)."""
+    with open(os.path.join(ROOT, profile_path)) as fh:
+        raw = json.load(fh)
+    return planner_case(name, None, model_cfg, global_batch, k_max=k_max,
+                        prof_json=raw.get("cluster_profile", raw))
 
 
 def reference_fixture_case(name, profile, model, workload, **kw):
@@ -188,6 +198,8 @@ def main():
         planner_case("tiny_search", E.CONFIG_NODES["tiny-2stage"], E.TINY_GPT, 8, k_max=2),
         planner_case("gpt2s_search", E.dp_group_nodes(8), E.GPT2_SMALL, 64, k_max=1),
         planner_case("llama13b_search", E.CONFIG_NODES["llama13b-8"], E.LLAMA_13B, 256),
+        measured_profile_case("gpt2s_measured8", "profiles/r01_measured_b200_profile_gpt2s.json",
+                              E.GPT2_SMALL, 64, k_max=1),
         # the reference README's planner benchmark: 128 GPUs, ~1,600 candidates (README:139-140)
         reference_fixture_case("ref_128gpu", rf.large_two_region_cluster(), rf.transformer_model(),
                                rf.default_workload()),

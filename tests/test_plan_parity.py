@@ -137,3 +137,26 @@ def test_plan_training_bit_exact(case):
                                     k_max=case["k_max"])
     assert len(records) == case["n_candidates"]
     assert plan.dumps() == case["plan_json"]
+
+
+MEMORY = _load("memory.json")
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["name"] in MEMORY], ids=lambda c: c["name"])
+def test_memory_replay_bit_exact(case, tmp_path):
+    """The simulator's memory accounting (task effects, simulate.py:284-550; replay
+    :660-696; initial residency :565-588) and its Gantt / memory CSV exports
+    (:115-137), restated, reproduce the reference's peaks and file bytes."""
+    import hashlib
+    prof, ctx = _ctx(case)
+    plan = P.TrainingPlan.from_json_dict(json.loads(case["plan_json"]), prof)
+    sched = P.build_schedule(ctx, plan)
+    peaks, traces = sched.memory(ctx)
+    want = MEMORY[case["name"]]
+    assert {d: {c: repr(v) for c, v in p.items()} for d, p in peaks.items()} == want["peaks"]
+    from paper_2507_10392_b200.plan.schedule import write_gantt_csv, write_memory_csv
+    write_gantt_csv(str(tmp_path / "g.csv"), sched.gantt_rows())
+    write_memory_csv(str(tmp_path / "m.csv"), traces)
+    sha = lambda p: hashlib.sha256(p.read_bytes()).hexdigest()  # noqa: E731
+    assert sha(tmp_path / "g.csv") == want["gantt_sha256"]
+    assert sha(tmp_path / "m.csv") == want["memory_sha256"]
