@@ -1,7 +1,7 @@
 """`hetplan report` for a plan EXECUTED on B200 (cli.py:234-285).
 
 For one workload — the bench layout (default) or a BASELINE config layout from
-scripts/config_run.py (``--run NAME``) — prints and writes (profiles/ or --out):
+scripts/config_run.py (``--config NAME``) — prints and writes (profiles/ or --out):
 
   latency: the plan's Eq.1 estimate (costs.py total_iteration_latency), the
            simulated iteration (simulate.py list schedule) and the MEASURED
@@ -13,7 +13,7 @@ scripts/config_run.py (``--run NAME``) — prints and writes (profiles/ or --out
            start / end, same columns, simulate.py:115-126) and
            <tag>_memory_simulated.csv (simulate.py:128-137).
 
-  torchrun --nproc-per-node N scripts/report.py [--run NAME] [--profile measured.json]
+  torchrun --nproc-per-node N scripts/report.py [--config NAME] [--profile measured.json]
            [--tag TAG] [--out DIR]
 
 ``--profile`` plans on a measured cluster profile (scripts/profile_layers.py output,
@@ -77,7 +77,7 @@ def build(args, world):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--run", default=None)
+    ap.add_argument("--config", dest="run", default=None)
     ap.add_argument("--profile", default=None)
     ap.add_argument("--model", default="gpt2-small-124m")
     ap.add_argument("--global-batch", type=int, default=0)
