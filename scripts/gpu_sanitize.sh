@@ -1,9 +1,7 @@
 #!/bin/bash
-# compute-sanitizer over one call of every kernel family (scripts/sanitize_kernels.py).
+# One call of every kernel family + a smoke step (scripts/sanitize_kernels.py).
+# compute-sanitizer itself is closed on the GPU pool (profiles/r02_compute_sanitizer_pool_closed.txt),
+# so this runs plain; bounds are asserted on the host side of every C-ABI entry point.
 mkdir -p gpurun_out
 python scripts/sanitize_kernels.py > gpurun_out/sanitize_plain.log 2>&1; echo "plain rc=$?" >> gpurun_out/sanitize_plain.log
-for tool in memcheck synccheck racecheck; do
-  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_kernels.py > gpurun_out/sanitize_$tool.log 2>&1
-  echo "$tool rc=$?" >> gpurun_out/sanitize_$tool.log
-done
-tail -n 4 gpurun_out/sanitize_*.log
+tail -n 3 gpurun_out/sanitize_plain.log
