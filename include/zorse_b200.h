@@ -184,6 +184,9 @@ int zb_ipc_open(const void* handle, void** base_out);
 int zb_ipc_close(void* base);
 /* *flag = *epoch_dev + delta with system-scope release (after a system fence). */
 int zb_peer_signal(void* flag, const void* epoch_dev, int delta, zb_stream_t stream);
+/* Single-process multi-GPU (tests, NVLink probes): enable the current device's
+ * access to peer_device's memory (cudaDeviceEnablePeerAccess; idempotent). */
+int zb_peer_enable(int peer_device);
 /* Bound of every flag spin (seconds; 0 = unbounded; default 120).  A spin that
  * exceeds it prints the flag it waited for and traps. */
 int zb_peer_set_timeout(double seconds);

@@ -60,6 +60,7 @@ SIGNATURES = {
     "zb_peer_signal": [P, P, I, P],
     "zb_peer_allgather_v": [P, I, I, P, P, I, P, P, U64, P, I, I, P],
     "zb_peer_wait": [P, I, I, U64, P, I, P],
+    "zb_peer_enable": [I],
     "zb_peer_set_timeout": [ctypes.c_double],
     "zb_peer_rs_adamw": [P, I, I, U64, I64, I64, U64, P, P, P, P, P, P, P, F, F, F, F, F, F, P, P],
     "zb_min_cut": [P, I64, P, P, P, P],

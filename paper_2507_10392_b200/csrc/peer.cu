@@ -274,6 +274,17 @@ typedef CUresult (*GetAddressRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 using namespace zb;
 
+extern "C" int zb_peer_enable(int peer_device) {
+  // Single-process multi-GPU use (tests / NVLink probes): map peer_device's memory
+  // into the current device's address space.  Multi-process ranks use CUDA IPC.
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return 0;
+  }
+  return e == cudaSuccess ? 0 : set_cuda_error(e, "cudaDeviceEnablePeerAccess");
+}
+
 extern "C" int zb_peer_set_timeout(double seconds) {
   if (!(seconds >= 0.0)) return set_error(ZB_ERR_INVALID, "peer timeout must be >= 0");
   g_timeout_ns = (uint64_t)(seconds * 1e9);
