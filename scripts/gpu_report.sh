@@ -9,4 +9,5 @@ timeout 600 $TR --nproc-per-node 4 --master-port 29532 scripts/report.py --out g
 timeout 600 python scripts/report.py --out gpurun_out --tag bench_n1 > gpurun_out/report_bench1.log 2>&1
 timeout 900 $TR --nproc-per-node 4 --master-port 29533 scripts/report.py --out gpurun_out --config xl_1+3 --tag xl_1+3_n4 > gpurun_out/report_xl.log 2>&1
 timeout 900 $TR --nproc-per-node 4 --master-port 29534 scripts/report.py --out gpurun_out --config llama13b_plan4 --steps 3 --tag llama13b_plan4_n4 > gpurun_out/report_13b.log 2>&1
+timeout 900 $TR --nproc-per-node 4 --master-port 29535 scripts/report.py --out gpurun_out --config llama7b_2x2 --steps 3 --tag llama7b_2x2_n4 > gpurun_out/report_7b.log 2>&1
 grep -h "latency\|GB\|report" gpurun_out/report_*.log | grep -v Warning | head -40
