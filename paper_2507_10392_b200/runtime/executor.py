@@ -54,6 +54,7 @@ they are dealt contiguously to devices in ``routing[group][m]`` order
 
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -259,7 +260,7 @@ class StageExecutor:
                  rank_of: Dict[str, int], world_comm, group_comm, ops, device,
                  seed: int = 1234, adam: AdamConfig = AdamConfig(), init_device="cpu",
                  schedule: str = "gpipe", streams: bool = False,
-                 offload_acts: Optional[bool] = None):
+                 offload_acts: Optional[bool] = None, keep_attention: bool = True):
         if plan.routing is None:
             raise ValueError("plan has no routing; attach it (configure.attach_routing) first")
         if ctx.model.num_layers != cfg.n_layer:
@@ -421,6 +422,21 @@ class StageExecutor:
                         self.gbuf[key] = torch.empty(n, d, **bf)
         self.rc_acts = alloc_acts(cfg, self.n_tok, device)   # one layer's recompute set
         self.fwd_acts = alloc_acts(cfg, self.n_tok, device)
+        # Selective recompute (keep_attention): the attention output and its
+        # log-sum-exp of every (layer, microbatch) are kept from the forward pass, so
+        # the backward's recompute skips the attention forward — the standard
+        # selective activation recomputation (Korthikanti et al. 2022): one extra
+        # [share*S, d] bf16 unit (+ fp32 lse) per layer and microbatch.
+        self.keep_attention = bool(keep_attention) and self.n_tok > 0
+        self.kept: Dict[Tuple[int, int], tuple] = {}
+        if self.keep_attention:
+            seqs = max(self.n_tok // S, 1)
+            for s in self.my_stages:
+                for layer in range(*self.ranges[s]):
+                    for m in range(self.M):
+                        self.kept[(layer, m)] = (
+                            torch.empty(n, d, **bf),
+                            torch.empty(seqs, cfg.n_head, S, device=device, dtype=torch.float32))
         self.fwd_out = torch.empty(n, d, **bf)
         self.bscr = alloc_bwd_scratch(cfg, self.n_tok, device)
         self.dy_pp = [torch.empty(n, d, **bf), torch.empty(n, d, **bf)]
@@ -479,7 +495,9 @@ class StageExecutor:
         return {"params_shard": shard_bf16, "params_window": window,
                 "grads_window": self.win.n_grad_slots * self.grad_slot_bytes,
                 "optim": sum(12 * pu.shard_numel for pu in self.units.values()),
-                "checkpoints": sum(acts.values()), "grad_slots": self.win.n_grad_slots,
+                "checkpoints": sum(acts.values()),
+                "kept_attention": sum(a.numel() * 2 + b.numel() * 4 for a, b in self.kept.values()),
+                "grad_slots": self.win.n_grad_slots,
                 "param_slots": len(self.param_slots) or len(self.layer_slots)}
 
     # ------------------------------------------------------------ step
@@ -677,8 +695,12 @@ class StageExecutor:
             self.model.embed_fwd(self.units["embed"].p, self.tokens[m], self.act[(lo, m)], n)
 
         def body(layer):
+            a = self.fwd_acts
+            if self.keep_attention:
+                attn, lse = self.kept[(layer, m)]
+                a = dataclasses.replace(a, attn=attn, lse=lse)
             self.model.layer_fwd(self.units[layer].p, self.act[(layer, m)][:n],
-                                 self.act[(layer + 1, m)][:n], self.fwd_acts, n)
+                                 self.act[(layer + 1, m)][:n], a, n)
         self._layers(list(range(lo, hi)), body)
         if s == self.n_stages - 1:
             hu = self.units["head"]
@@ -705,8 +727,13 @@ class StageExecutor:
             dx = self.gbuf[(lo, m)][:n] if j == 0 else self.dy_pp[j & 1][:n]
             u = self.units[layer]
             x = self.act[(layer, m)][:n]
-            self.model.layer_fwd(u.p, x, self.fwd_out[:n], self.rc_acts, n, need_out=False)
-            self.model.layer_bwd(u.p, u.g, x, state["dy"], dx, self.rc_acts, self.bscr, n)
+            a = self.rc_acts
+            if self.keep_attention:
+                attn, lse = self.kept[(layer, m)]
+                a = dataclasses.replace(a, attn=attn, lse=lse)
+            self.model.layer_fwd(u.p, x, self.fwd_out[:n], a, n, need_out=False,
+                                 kept=self.keep_attention)
+            self.model.layer_bwd(u.p, u.g, x, state["dy"], dx, a, self.bscr, n)
             state["dy"] = dx
         self._layers(list(reversed(range(lo, hi))), body)
         if s == 0:

@@ -241,16 +241,19 @@ class GptOps:
         self.wlane = WgradLane()
 
     def layer_fwd(self, p: Dict[str, torch.Tensor], x: torch.Tensor, out: torch.Tensor,
-                  a: LayerActs, n_tok: int, need_out: bool = True) -> None:
+                  a: LayerActs, n_tok: int, need_out: bool = True, kept=False) -> None:
         """out = block(x); fills ``a`` (the recompute set).  ``need_out=False``
         (activation recompute) skips the fc2 GEMM: backward never reads the
-        block output, only its internals."""
+        block output, only its internals.  ``kept``: a.attn / a.lse hold the
+        attention output of this (layer, microbatch) kept from the forward pass, so
+        the recompute skips the attention forward (selective recompute)."""
         o, cfg = self.ops, self.cfg
         n_seq = n_tok // cfg.seq_len
         o.layernorm_fwd(x, p["ln1_w"], p["ln1_b"], a.h1[:n_tok], a.mean1[:n_tok], a.rstd1[:n_tok])
         o.gemm(a.h1[:n_tok], p["qkv_w"], a.qkv[:n_tok], epilogue=EPI_BIAS, bias=p["qkv_b"])
-        o.attn_fwd(a.qkv[:n_tok], a.attn[:n_tok], a.lse[:n_seq], n_seq, cfg.seq_len, cfg.n_head,
-                   cfg.head_dim, self.scale)
+        if not kept:
+            o.attn_fwd(a.qkv[:n_tok], a.attn[:n_tok], a.lse[:n_seq], n_seq, cfg.seq_len,
+                       cfg.n_head, cfg.head_dim, self.scale)
         o.gemm(a.attn[:n_tok], p["proj_w"], a.x_mid[:n_tok], epilogue=EPI_BIAS_RESID,
                bias=p["proj_b"], resid=x)
         o.layernorm_fwd(a.x_mid[:n_tok], p["ln2_w"], p["ln2_b"], a.h2[:n_tok], a.mean2[:n_tok],
@@ -335,15 +338,17 @@ class LlamaOps:
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
         self.wlane = WgradLane()
 
-    def layer_fwd(self, p, x, out, a: LlamaActs, n_tok: int, need_out: bool = True) -> None:
+    def layer_fwd(self, p, x, out, a: LlamaActs, n_tok: int, need_out: bool = True,
+                  kept=False) -> None:
         o, cfg = self.ops, self.cfg
         n = n_tok
         n_seq = n // cfg.seq_len
         o.rmsnorm_fwd(x, p["attn_norm"], a.h1[:n], a.rstd1[:n])
         o.gemm(a.h1[:n], p["qkv_w"], a.qkv[:n])
         o.rope(a.qkv[:n], cfg.seq_len, cfg.n_head, cfg.head_dim, self.ROPE_THETA)
-        o.attn_fwd(a.qkv[:n], a.attn[:n], a.lse[:n_seq], n_seq, cfg.seq_len, cfg.n_head,
-                   cfg.head_dim, self.scale)
+        if not kept:
+            o.attn_fwd(a.qkv[:n], a.attn[:n], a.lse[:n_seq], n_seq, cfg.seq_len, cfg.n_head,
+                       cfg.head_dim, self.scale)
         o.gemm(a.attn[:n], p["o_w"], a.x_mid[:n], epilogue=EPI_RESID, resid=x)
         o.rmsnorm_fwd(a.x_mid[:n], p["mlp_norm"], a.h2[:n], a.rstd2[:n])
         o.gemm(a.h2[:n], p["gu_w"], a.gu[:n])
