@@ -431,14 +431,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_commit();
       }
     };
+    const size_t vrow0 = ((size_t)b * H + h) * S + kt * T + r;  // lse / delta one tile ahead
+    float nl = 0.f, nd = 0.f;
+    if (half == 0) {
+      nl = lse[vrow0];
+      nd = delta[vrow0];
+    }
     for (int i = 0; i < ntile; ++i) {
       const int qt = kt + i;
       float* vl = vec + (i & 1) * 2 * T;
       float* vd = vl + T;
-      const size_t vrow = ((size_t)b * H + h) * S + qt * T + r;
       if (half == 0) {
-        vl[r] = lse[vrow] * LOG2E;
-        vd[r] = delta[vrow];
+        vl[r] = nl * LOG2E;
+        vd[r] = nd;
+        if (i + 1 < ntile) {
+          nl = lse[vrow0 + (size_t)(i + 1) * T];
+          nd = delta[vrow0 + (size_t)(i + 1) * T];
+        }
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");  // the eight math warps
       mbar_wait(s_full, i & 1);
@@ -534,6 +543,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 // dkdv_kernel<64, true>; barrier parities run on global tile / item counters, the
 // Q/dO ring continues across items, and `acc_empty` hands the dK/dV accumulators
 // back to the MMA warp once the epilogue read them.
+// Shared memory of the persistent fused kernel: P^T lives in TMEM (written over its
+// own S^T columns as bf16 and read by the dV MMA as the A operand), which frees the
+// room for a DOUBLE-buffered dS^T — the math warps of query tile i+1 no longer wait
+// for the dK / dQ MMAs of tile i to finish reading the previous dS^T.
+template <int D>
+struct DkvqSmem {
+  static constexpr int NST = 2;  // Q / dO stages
+  static constexpr int TILE = T * D * 2;
+  static constexpr int OFF_K = 0, OFF_V = TILE;
+  static constexpr int OFF_Q = 2 * TILE;               // [NST] Q_i
+  static constexpr int OFF_DO = OFF_Q + NST * TILE;    // [NST] dO_i
+  static constexpr int OFF_DST = OFF_DO + NST * TILE;  // [2] dS^T [128 keys][128 queries]
+  static constexpr int OFF_VEC = OFF_DST + 2 * T * T * 2;  // [2][2][128] lse*log2e, delta
+  static constexpr int OFF_STG = OFF_VEC + 2 * 2 * T * 4;  // [8 warps] 32x32 fp32 dQ staging
+  static constexpr int OFF_BAR = OFF_STG + kMath * 4096;
+  static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+};
+
+// Persistent fused backward (D = 64): one CTA per SM walks (key tile, head, sequence)
+// items heavy-first.  Per query tile i of an item the MMA issuer runs
+//   dV += P^T(i) dO(i)   [A = P^T from TMEM]     then, in order,
+//   S^T(i+1), dP^T(i+1)  [overwrites P^T(i) only after the dV MMA read it]
+//   dK += dS^T(i) Q(i),  dQ_i = dS(i) K  [dS^T from the smem buffer of parity i]
+// while the math warps turn S^T / dP^T of tile i+1 into P^T (TMEM) and dS^T (the other
+// smem buffer) and drain dQ_i (TMA reduce-add into the fp32 accumulator).
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     dkdvq_persistent_kernel(const __grid_constant__ CUtensorMap tm_qkv,
@@ -542,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const float* __restrict__ lse, const float* __restrict__ delta,
                             __nv_bfloat16* __restrict__ dqkv, int S, int H, int n_seq, int ld,
                             float scale) {
-  using L = DkvSmem<D, true>;
+  using L = DkvqSmem<D>;
   constexpr int NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -552,14 +586,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* qo_full = bar + 1;          // [NST]
   uint64_t* qo_empty = bar + 1 + NST;   // [NST]
   uint64_t* s_full = bar + 1 + 2 * NST;
-  uint64_t* s_empty = s_full + 1;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* p_empty = s_full + 3;
-  uint64_t* done = s_full + 4;        // item's last MMAs complete
-  uint64_t* dqp_full = s_full + 5;    // [2]
-  uint64_t* dqp_empty = s_full + 7;   // [2]
-  uint64_t* kv_empty = s_full + 9;    // item's K / V no longer read
-  uint64_t* acc_empty = s_full + 10;  // epilogue read dK / dV (count kMath)
+  uint64_t* p_full = s_full + 1;        // P^T (TMEM) and dS^T (smem) of a tile written
+  uint64_t* dst_empty = s_full + 2;     // [2] dS^T buffer read by dK / dQ
+  uint64_t* done = s_full + 4;          // item's last MMAs complete
+  uint64_t* dqp_full = s_full + 5;      // [2]
+  uint64_t* dqp_empty = s_full + 7;     // [2]
+  uint64_t* kv_empty = s_full + 9;      // item's K / V no longer read
+  uint64_t* acc_empty = s_full + 10;    // epilogue read dK / dV (count kMath)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 11);
   float* vec = reinterpret_cast<float*>(sm + L::OFF_VEC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -585,14 +618,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&qo_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_empty, kMath);
     mbar_init(p_full, kMath);
-    mbar_init(p_empty, 1);
-    mbar_init(done, 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&dst_empty[i], 1);
       mbar_init(&dqp_full[i], 1);
       mbar_init(&dqp_empty[i], kMath);
     }
+    mbar_init(done, 1);
     mbar_init(kv_empty, 1);
     mbar_init(acc_empty, kMath);
     fence_barrier_init();
@@ -643,12 +675,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_o = umma_idesc_bf16(T, D, 0, 1);
       constexpr uint32_t idesc_q = umma_idesc_bf16(T, D, 1, 1);
       const uint32_t k_base = smem_u32(sm + L::OFF_K), v_base = smem_u32(sm + L::OFF_V);
-      const uint32_t pt_base = smem_u32(sm + L::OFF_PT), dst_base = smem_u32(sm + L::OFF_DST);
       int g = 0, lt = 0;
-      auto issue_s = [&](int gi) {
+      auto issue_s = [&](int gi) {  // S^T(gi) = K Q^T, dP^T(gi) = V dO^T
         const int st = gi % NST;
         mbar_wait(&qo_full[st], (gi / NST) & 1);
-        mbar_wait(s_empty, (gi & 1) ^ 1);
         tc_fence_after();
         const uint32_t q_base = smem_u32(sm + L::OFF_Q + st * L::TILE);
         const uint32_t do_base = smem_u32(sm + L::OFF_DO + st * L::TILE);
@@ -665,21 +695,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ntile = nqt - kt;
         mbar_wait(kv_full, lt & 1);
         tc_fence_after();
-        issue_s(g);
+        issue_s(g);   // the previous item's last dV (reader of P^T in t_st) was issued before
         for (int i = 0; i < ntile; ++i) {
-          const int gi = g + i, st = gi % NST;
-          if (i + 1 < ntile) issue_s(gi + 1);
+          const int gi = g + i, st = gi % NST, bb = gi & 1;
           mbar_wait(p_full, gi & 1);
           if (i == 0) mbar_wait(acc_empty, (lt & 1) ^ 1);  // previous item's dK / dV read
           tc_fence_after();
           const uint32_t q_base = smem_u32(sm + L::OFF_Q + st * L::TILE);
           const uint32_t do_base = smem_u32(sm + L::OFF_DO + st * L::TILE);
+          const uint32_t dst_base = smem_u32(sm + L::OFF_DST + bb * T * T * 2);
+          // dV += P^T dO: P^T keys x queries in TMEM; queries [64h, 64h+64) sit in the
+          // S^T columns [64h, 64h+32) (each math half wrote its own columns)
 #pragma unroll
-          for (int kk = 0; kk < T / 16; ++kk) {
-            mma_bf16_ss(t_dv, desc_k(pt_base, kk), desc_mn(do_base, kk), idesc_o, (i > 0 || kk > 0));
+          for (int kk = 0; kk < T / 16; ++kk)
+            mma_bf16_ts(t_dv, t_st + (kk >> 2) * 64 + (kk & 3) * 8, desc_mn(do_base, kk), idesc_o,
+                        (i > 0 || kk > 0) ? 1u : 0u);
+          if (i + 1 < ntile) issue_s(gi + 1);  // in order: after the dV MMAs read P^T(i)
+#pragma unroll
+          for (int kk = 0; kk < T / 16; ++kk)
             mma_bf16_ss(t_dk, desc_k(dst_base, kk), desc_mn(q_base, kk), idesc_o, (i > 0 || kk > 0));
-          }
-          const int bb = gi & 1;
           mbar_wait(&dqp_empty[bb], ((gi >> 1) & 1) ^ 1);
           tc_fence_after();
 #pragma unroll
@@ -688,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         kk > 0 ? 1u : 0u);
           mma_commit(&dqp_full[bb]);
           mma_commit(&qo_empty[st]);
-          mma_commit(p_empty);
+          mma_commit(&dst_empty[bb]);
         }
         mma_commit(kv_empty);
         mma_commit(done);
@@ -731,21 +765,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_commit();
         }
       };
+      // lse / delta of query tile i are loaded from global one tile ahead
+      const size_t vrow0 = ((size_t)b * H + h) * S + kt * T + r;
+      float nl = 0.f, nd = 0.f;
+      if (half == 0) {
+        nl = lse[vrow0];
+        nd = delta[vrow0];
+      }
       for (int i = 0; i < ntile; ++i) {
-        const int gi = g + i, qt = kt + i;
-        float* vl = vec + (gi & 1) * 2 * T;
+        const int gi = g + i, qt = kt + i, bb = gi & 1;
+        float* vl = vec + bb * 2 * T;
         float* vd = vl + T;
-        const size_t vrow = ((size_t)b * H + h) * S + qt * T + r;
         if (half == 0) {
-          vl[r] = lse[vrow] * LOG2E;
-          vd[r] = delta[vrow];
+          vl[r] = nl * LOG2E;
+          vd[r] = nd;
+          if (i + 1 < ntile) {
+            nl = lse[vrow0 + (size_t)(i + 1) * T];
+            nd = delta[vrow0 + (size_t)(i + 1) * T];
+          }
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");  // the eight math warps
         mbar_wait(s_full, gi & 1);
-        mbar_wait(p_empty, (gi & 1) ^ 1);
+        mbar_wait(&dst_empty[bb], ((gi >> 1) & 1) ^ 1);  // dK / dQ of tile gi-2 read it
         tc_fence_after();
-        uint8_t* pt = sm + L::OFF_PT;
-        uint8_t* dst = sm + L::OFF_DST;
+        uint8_t* dst = sm + L::OFF_DST + bb * T * T * 2;
         auto chunk = [&](int c, auto diag_c) {
           constexpr bool DG = decltype(diag_c)::value;
           uint32_t sv[32], dv[32];
@@ -753,22 +796,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_32x32b_x32(t_dpt + lo + c * 32, dv);
           tmem_ld_wait_regs(sv);
           reg_tie(dv);
-          float p[32], ds[32];
+          float ds[32];
+          uint32_t pk[16];
 #pragma unroll
           for (int t4 = 0; t4 < 32; t4 += 4) {
             const float4 l4 = *reinterpret_cast<const float4*>(vl + c * 32 + t4);
             const float4 d4 = *reinterpret_cast<const float4*>(vd + c * 32 + t4);
             const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
+            float p4[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int tt = t4 + u;
               float x = exp2_fast(fmaf(__uint_as_float(sv[tt]), sl2, -lv[u]));
               if (DG && c * 32 + tt < r) x = 0.f;
-              p[tt] = x;
+              p4[u] = x;
               ds[tt] = x * (__uint_as_float(dv[tt]) - dl[u]);
             }
+            pk[t4 / 2] = pack_bf16(p4[0], p4[1]);
+            pk[t4 / 2 + 1] = pack_bf16(p4[2], p4[3]);
           }
-          st_row32(pt, r, c * 32, p);
+          // P^T columns [c*32, c*32+32) -> packed TMEM columns inside this half's own
+          // (already read) S^T columns
+          tmem_st_32x32b_x16(t_st + lo + half * 64 + (c - half * (T / 64)) * 16, pk);
           st_row32(dst, r, c * 32, ds);
         };
         constexpr int CH = T / 64;
@@ -779,9 +828,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
           for (int c = half * CH; c < (half + 1) * CH; ++c) chunk(c, std::false_type{});
         }
+        tmem_st_wait();
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(s_empty);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
@@ -913,9 +961,6 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(dkdv_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                DkvSmem<D, false>::TOTAL);
-    if (e == cudaSuccess && D == 64)
-      e = cudaFuncSetAttribute(dkdv_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               DkvSmem<D, true>::TOTAL);
     if (e != cudaSuccess) return set_cuda_error(e, "attn_bwd: cudaFuncSetAttribute");
     configured = true;
   }
@@ -934,7 +979,7 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = DkvSmem<D, true>::TOTAL;
+    cfg.dynamicSmemBytes = DkvqSmem<D>::TOTAL;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -945,7 +990,7 @@ static int run(const void* qkv, const void* out, const void* dout, const void* l
     if (!cfg_p) {
       cudaError_t e0 = cudaFuncSetAttribute(dkdvq_persistent_kernel<D>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            DkvSmem<D, true>::TOTAL);
+                                            DkvqSmem<D>::TOTAL);
       if (e0 != cudaSuccess) return set_cuda_error(e0, "attn_bwd: cudaFuncSetAttribute");
       cfg_p = true;
     }
