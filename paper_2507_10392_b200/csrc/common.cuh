@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -377,6 +378,55 @@ ZB_DEVICE float gelu_tanh_grad(float x) {
   float u = k0 * (x + k1 * x2 * x);
   float t = tanh_fast(u);
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
+}
+
+// GELU(tanh) on pairs in f16x2 arithmetic: tanh.approx.f16x2 does two tanh per MUFU
+// op and the polynomial runs on HFMA2, half the instructions of the fp32 form.  The
+// result is rounded to bf16 by the caller, whose 8-bit mantissa dominates the f16
+// error.  Inputs are clamped to +-6e4 (the f16 range) first.
+ZB_DEVICE __half2 tanh_h2(__half2 x) {
+  uint32_t xi = *reinterpret_cast<uint32_t*>(&x), yi;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(yi) : "r"(xi));
+  return *reinterpret_cast<__half2*>(&yi);
+}
+ZB_DEVICE __half2 to_h2(float a, float b) {
+  return __floats2half2_rn(fminf(fmaxf(a, -6.0e4f), 6.0e4f), fminf(fmaxf(b, -6.0e4f), 6.0e4f));
+}
+ZB_DEVICE __half2 gelu_tanh_h2(__half2 x) {
+  const __half2 k0 = __float2half2_rn(0.7978845608028654f);
+  const __half2 k1 = __float2half2_rn(0.044715f), hf = __float2half2_rn(0.5f);
+  const __half2 x2 = __hmul2(x, x);
+  const __half2 u = __hmul2(k0, __hfma2(__hmul2(k1, x2), x, x));  // k0 (x + k1 x^3)
+  const __half2 hx = __hmul2(hf, x);
+  return __hfma2(hx, tanh_h2(u), hx);                              // 0.5 x (1 + t)
+}
+ZB_DEVICE __half2 gelu_tanh_grad_h2(__half2 x) {
+  const __half2 k0 = __float2half2_rn(0.7978845608028654f);
+  const __half2 k1 = __float2half2_rn(0.044715f), hf = __float2half2_rn(0.5f);
+  const __half2 one = __float2half2_rn(1.f), k3 = __float2half2_rn(3.f * 0.044715f);
+  const __half2 hk0 = __float2half2_rn(0.5f * 0.7978845608028654f);
+  const __half2 x2 = __hmul2(x, x);
+  const __half2 t = tanh_h2(__hmul2(k0, __hfma2(__hmul2(k1, x2), x, x)));
+  const __half2 a = __hfma2(hf, t, hf);                            // 0.5 (1 + t)
+  const __half2 b = __hfma2(__hneg2(t), t, one);                   // 1 - t^2
+  const __half2 c = __hfma2(k3, x2, one);                          // 1 + 3 k1 x^2
+  return __hfma2(__hmul2(__hmul2(hk0, x), b), c, a);
+}
+// v[j] = gelu(bf16(v[j])) for 32 values (the forward GELU of the bf16-rounded
+// pre-activation, so forward and backward agree).  fp32 tanh: the f16x2 form measured
+// 4-5% SLOWER here (its rounding / clamp conversions cost more than the halved tanh).
+ZB_DEVICE void gelu32_bf16in(float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
+}
+// v[j] *= gelu'(in[j]) for 32 values, in f16x2 (measured +8% on the fc2-dgrad GEMM).
+ZB_DEVICE void gelu_grad_mul32(float (&v)[32], const float (&in)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const float2 g = __half22float2(gelu_tanh_grad_h2(to_h2(in[j], in[j + 1])));
+    v[j] *= g.x;
+    v[j + 1] *= g.y;
+  }
 }
 
 ZB_DEVICE uint32_t pack_bf16(float a, float b) {

@@ -200,30 +200,27 @@ ZB_DEVICE void epilogue_chunk(const GemmArgs& args, const uint32_t (&r)[32], int
     } else {
       _Pragma("unroll") for (int j = 0; j < 32; ++j) if (col0 + j < args.N) Ap[j] = __float2bfloat16(v[j]);
     }
-    // GELU of the bf16-rounded pre-activation, so forward and backward agree.
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
+    gelu32_bf16in(v);   // GELU of the bf16-rounded pre-activation, so forward and backward agree
   }
-  if (EPI == EPI_BIAS_GELU_NA) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
-  }
+  if (EPI == EPI_BIAS_GELU_NA) gelu32_bf16in(v);
   if (EPI == EPI_GELU_BWD) {
     const __nv_bfloat16* Ap = args.aux + (size_t)row * args.ldaux + col0;
     if (full) {
 #pragma unroll
+      float in[32];
       for (int j = 0; j < 32; j += 8) {
         uint4 q = *reinterpret_cast<const uint4*>(Ap + j);
         float2 f0 = unpack_bf16(q.x), f1 = unpack_bf16(q.y), f2 = unpack_bf16(q.z),
                f3 = unpack_bf16(q.w);
-        v[j] *= gelu_tanh_grad(f0.x); v[j + 1] *= gelu_tanh_grad(f0.y);
-        v[j + 2] *= gelu_tanh_grad(f1.x); v[j + 3] *= gelu_tanh_grad(f1.y);
-        v[j + 4] *= gelu_tanh_grad(f2.x); v[j + 5] *= gelu_tanh_grad(f2.y);
-        v[j + 6] *= gelu_tanh_grad(f3.x); v[j + 7] *= gelu_tanh_grad(f3.y);
+        in[j] = f0.x; in[j + 1] = f0.y; in[j + 2] = f1.x; in[j + 3] = f1.y;
+        in[j + 4] = f2.x; in[j + 5] = f2.y; in[j + 6] = f3.x; in[j + 7] = f3.y;
       }
+      gelu_grad_mul32(v, in);
     } else {
-      _Pragma("unroll") for (int j = 0; j < 32; ++j) if (col0 + j < args.N)
-        v[j] *= gelu_tanh_grad(__bfloat162float(Ap[j]));
+      float in[32];
+      _Pragma("unroll") for (int j = 0; j < 32; ++j)
+        in[j] = col0 + j < args.N ? __bfloat162float(Ap[j]) : 0.f;
+      gelu_grad_mul32(v, in);
     }
   }
   __nv_bfloat16* Cp = reinterpret_cast<__nv_bfloat16*>(args.C) + (size_t)row * args.ldc + col0;
@@ -371,8 +368,7 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
       float in[32];
       ld_row_bf16(slot, lane, in);
       if (EPI == EPI_GELU_BWD) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] *= gelu_tanh_grad(in[j]);
+        gelu_grad_mul32(v, in);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += in[j];
@@ -389,15 +385,10 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
       if (lane == 0) bulk_wait_read<0>();  // aux -> slot 0, C -> slot 1
       __syncwarp();
       st_row_bf16(stg, lane, v);
-      // GELU of the bf16-rounded pre-activation, so forward and backward agree.
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
+      gelu32_bf16in(v);   // GELU of the bf16-rounded pre-activation (= the stored aux)
       st_row_bf16(stg + kEpiSlot, lane, v);
     } else {
-      if (EPI == EPI_BIAS_GELU_NA) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__bfloat162float(__float2bfloat16(v[j])));
-      }
+      if (EPI == EPI_BIAS_GELU_NA) gelu32_bf16in(v);
       // slots alternate over a running chunk count (across tiles), so the slot
       // written now was last stored two chunks ago
       slot = stg + (ecnt & 1) * kEpiSlot;

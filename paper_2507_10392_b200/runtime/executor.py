@@ -422,11 +422,12 @@ class StageExecutor:
                         self.gbuf[key] = torch.empty(n, d, **bf)
         self.rc_acts = alloc_acts(cfg, self.n_tok, device)   # one layer's recompute set
         self.fwd_acts = alloc_acts(cfg, self.n_tok, device)
-        # Selective recompute (keep_attention): the attention output and its
-        # log-sum-exp of every (layer, microbatch) are kept from the forward pass, so
-        # the backward's recompute skips the attention forward — the standard
-        # selective activation recomputation (Korthikanti et al. 2022): one extra
-        # [share*S, d] bf16 unit (+ fp32 lse) per layer and microbatch.
+        # Selective recompute (keep_attention): the attention block's outputs of every
+        # (layer, microbatch) — attention output, its log-sum-exp and x_mid = x +
+        # proj(attn) — are kept from the forward pass, so the backward's recompute
+        # skips the attention forward and the projection GEMM (selective activation
+        # recomputation, Korthikanti et al. 2022): two extra [share*S, d] bf16 units
+        # (+ fp32 lse) per layer and microbatch.
         self.keep_attention = bool(keep_attention) and self.n_tok > 0
         self.kept: Dict[Tuple[int, int], tuple] = {}
         if self.keep_attention:
@@ -436,7 +437,8 @@ class StageExecutor:
                     for m in range(self.M):
                         self.kept[(layer, m)] = (
                             torch.empty(n, d, **bf),
-                            torch.empty(seqs, cfg.n_head, S, device=device, dtype=torch.float32))
+                            torch.empty(seqs, cfg.n_head, S, device=device, dtype=torch.float32),
+                            torch.empty(n, d, **bf))
         self.fwd_out = torch.empty(n, d, **bf)
         self.bscr = alloc_bwd_scratch(cfg, self.n_tok, device)
         self.dy_pp = [torch.empty(n, d, **bf), torch.empty(n, d, **bf)]
@@ -496,7 +498,8 @@ class StageExecutor:
                 "grads_window": self.win.n_grad_slots * self.grad_slot_bytes,
                 "optim": sum(12 * pu.shard_numel for pu in self.units.values()),
                 "checkpoints": sum(acts.values()),
-                "kept_attention": sum(a.numel() * 2 + b.numel() * 4 for a, b in self.kept.values()),
+                "kept_attention": sum(a.numel() * 2 + b.numel() * 4 + c.numel() * 2
+                                      for a, b, c in self.kept.values()),
                 "grad_slots": self.win.n_grad_slots,
                 "param_slots": len(self.param_slots) or len(self.layer_slots)}
 
@@ -697,8 +700,8 @@ class StageExecutor:
         def body(layer):
             a = self.fwd_acts
             if self.keep_attention:
-                attn, lse = self.kept[(layer, m)]
-                a = dataclasses.replace(a, attn=attn, lse=lse)
+                attn, lse, x_mid = self.kept[(layer, m)]
+                a = dataclasses.replace(a, attn=attn, lse=lse, x_mid=x_mid)
             self.model.layer_fwd(self.units[layer].p, self.act[(layer, m)][:n],
                                  self.act[(layer + 1, m)][:n], a, n)
         self._layers(list(range(lo, hi)), body)
@@ -729,8 +732,8 @@ class StageExecutor:
             x = self.act[(layer, m)][:n]
             a = self.rc_acts
             if self.keep_attention:
-                attn, lse = self.kept[(layer, m)]
-                a = dataclasses.replace(a, attn=attn, lse=lse)
+                attn, lse, x_mid = self.kept[(layer, m)]
+                a = dataclasses.replace(a, attn=attn, lse=lse, x_mid=x_mid)
             self.model.layer_fwd(u.p, x, self.fwd_out[:n], a, n, need_out=False,
                                  kept=self.keep_attention)
             self.model.layer_bwd(u.p, u.g, x, state["dy"], dx, a, self.bscr, n)

@@ -244,9 +244,10 @@ class GptOps:
                   a: LayerActs, n_tok: int, need_out: bool = True, kept=False) -> None:
         """out = block(x); fills ``a`` (the recompute set).  ``need_out=False``
         (activation recompute) skips the fc2 GEMM: backward never reads the
-        block output, only its internals.  ``kept``: a.attn / a.lse hold the
-        attention output of this (layer, microbatch) kept from the forward pass, so
-        the recompute skips the attention forward (selective recompute)."""
+        block output, only its internals.  ``kept``: a.attn / a.lse / a.x_mid hold
+        the attention block's outputs of this (layer, microbatch) kept from the
+        forward pass, so the recompute skips the attention forward and the
+        projection GEMM (selective recompute)."""
         o, cfg = self.ops, self.cfg
         n_seq = n_tok // cfg.seq_len
         o.layernorm_fwd(x, p["ln1_w"], p["ln1_b"], a.h1[:n_tok], a.mean1[:n_tok], a.rstd1[:n_tok])
@@ -254,8 +255,8 @@ class GptOps:
         if not kept:
             o.attn_fwd(a.qkv[:n_tok], a.attn[:n_tok], a.lse[:n_seq], n_seq, cfg.seq_len,
                        cfg.n_head, cfg.head_dim, self.scale)
-        o.gemm(a.attn[:n_tok], p["proj_w"], a.x_mid[:n_tok], epilogue=EPI_BIAS_RESID,
-               bias=p["proj_b"], resid=x)
+            o.gemm(a.attn[:n_tok], p["proj_w"], a.x_mid[:n_tok], epilogue=EPI_BIAS_RESID,
+                   bias=p["proj_b"], resid=x)
         o.layernorm_fwd(a.x_mid[:n_tok], p["ln2_w"], p["ln2_b"], a.h2[:n_tok], a.mean2[:n_tok],
                         a.rstd2[:n_tok])
         if need_out:  # forward pass: backward reads the recompute's pre-activation, not this one
@@ -349,7 +350,7 @@ class LlamaOps:
         if not kept:
             o.attn_fwd(a.qkv[:n], a.attn[:n], a.lse[:n_seq], n_seq, cfg.seq_len, cfg.n_head,
                        cfg.head_dim, self.scale)
-        o.gemm(a.attn[:n], p["o_w"], a.x_mid[:n], epilogue=EPI_RESID, resid=x)
+            o.gemm(a.attn[:n], p["o_w"], a.x_mid[:n], epilogue=EPI_RESID, resid=x)
         o.rmsnorm_fwd(a.x_mid[:n], p["mlp_norm"], a.h2[:n], a.rstd2[:n])
         o.gemm(a.h2[:n], p["gu_w"], a.gu[:n])
         o.swiglu_fwd(a.gu[:n], a.m[:n])
