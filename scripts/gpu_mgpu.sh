@@ -3,7 +3,7 @@
 # layouts with memory vs the plan's estimate, bench N=2/4.  Output -> gpurun_out/
 mkdir -p gpurun_out
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
-for L in dp2:2 dp2z3:2 pp2:2 pp1+3:4 dp4z3:4 pp2x2:4 llama1f1b2x2:4 xl1+3:4; do
+for L in dp2:2 dp2z3:2 pp2:2 cfg1_tiny:3 pp1+3:4 dp4z3:4 pp2x2:4 llama1f1b2x2:4 xl1+3:4; do
   name=${L%%:*}; n=${L##*:}
   timeout 600 $TR --nproc-per-node $n --master-port 29511 scripts/mgpu_check.py $name >> gpurun_out/mgpu_parity.jsonl 2>> gpurun_out/mgpu_parity.err
   echo "$name rc=$?" >> gpurun_out/mgpu_parity.rc

@@ -41,11 +41,14 @@ LAYOUTS = {
     # Llama, 1F1B, 2 stages x 2-way ZeRO-3 DP (config 4 in miniature)
     "llama1f1b2x2": ([("n0", ["b200", "b200"]), ("n1", ["b200", "b200"])],
                      [["n0-0", "n0-1"], ["n1-0", "n1-1"]], 4, [1, 1], "pp-zero3", 8),
+    # BASELINE config 1 exactly: tiny GPT (4 layers, d 256, seq 128, V 50304), the golden
+    # `tiny` plan (tests/golden/plans.json): 2 asymmetric stages, uneven 2-rank ZeRO-3 group
+    "cfg1_tiny": (E.CONFIG_NODES["tiny-2stage"], [["n0-0", "n0-1"], ["n1-0"]], 2, [1, 1], "zorse", 8),
     # GPT-2-XL widths, asymmetric 1 + 3 stages (config 3 in miniature)
     "xl1+3": ([("n0", ["b200"]), ("n1", ["b200", "b200", "b200h"])],
               [["n0-0"], ["n1-0", "n1-1", "n1-2"]], 4, [1, 1], "zorse", 8),
 }
-CFGS = {"llama1f1b2x2": LLAMA, "xl1+3": XLW}
+CFGS = {"llama1f1b2x2": LLAMA, "xl1+3": XLW, "cfg1_tiny": E.TINY_GPT}
 SCHED = {"llama1f1b2x2": "1f1b"}
 
 
@@ -64,6 +67,10 @@ def main():
     plan = P.build_plan(ctx, prof, P.make_partition(ctx.graph, groups), M, counts,
                         P.Strategy(strategy), P.cluster_fingerprint(prof), "transformer")
     P.attach_routing(plan, rt, "transformer")
+    if name == "cfg1_tiny":   # the very plan the reference emits for config 1 (golden bytes)
+        with open(os.path.join(ROOT, "tests", "golden", "plans.json")) as fh:
+            golden = next(c for c in json.load(fh) if c["name"] == "tiny")
+        assert plan.dumps() == golden["plan_json"], "config-1 plan differs from the reference's"
     graph = os.environ.get("ZB_GRAPH", "1") == "1"   # script option: step 2 replays a graph
     tr = ZorseTrainer(plan, ctx, CFG, world_rank=rank, world_size=world,
                       schedule=SCHED.get(name, "gpipe"))

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("layout,n", [("dp2", 2), ("pp2", 2), ("pp1+3", 4), ("dp4z3", 4),
+@pytest.mark.parametrize("layout,n", [("dp2", 2), ("pp2", 2), ("cfg1_tiny", 3), ("pp1+3", 4), ("dp4z3", 4),
                                       ("pp2x2", 4), ("llama1f1b2x2", 4), ("xl1+3", 4)])
 def test_multi_gpu_layout(layout, n):
     if torch.cuda.device_count() < n:
