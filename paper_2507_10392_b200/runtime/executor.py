@@ -260,7 +260,7 @@ class StageExecutor:
                  rank_of: Dict[str, int], world_comm, group_comm, ops, device,
                  seed: int = 1234, adam: AdamConfig = AdamConfig(), init_device="cpu",
                  schedule: str = "gpipe", streams: bool = False,
-                 offload_acts: Optional[bool] = None, keep_attention: bool = True):
+                 offload_acts: Optional[bool] = None, recompute: str = "auto"):
         if plan.routing is None:
             raise ValueError("plan has no routing; attach it (configure.attach_routing) first")
         if ctx.model.num_layers != cfg.n_layer:
@@ -420,25 +420,49 @@ class StageExecutor:
                 for key in ((lo, m), (hi, m)):
                     if key not in self.gbuf:
                         self.gbuf[key] = torch.empty(n, d, **bf)
+        # Recompute policy.  The paper checkpoints every layer boundary and recomputes
+        # the block internals in the backward to save memory; on a
+        # 180 GB B200 the plan's memory budget usually leaves room to keep them:
+        #   "full"      recompute every block internal from the checkpoint (the paper);
+        #   "selective" keep the attention block's outputs (attention output + LSE,
+        #               x_mid = x + proj(attn)) of every (layer, microbatch): the
+        #               recompute skips the attention forward and the projection GEMM
+        #               (selective activation recomputation, Korthikanti et al. 2022);
+        #   "none"      keep the whole recompute set of every (layer, microbatch): the
+        #               backward recomputes nothing;
+        #   "auto"      "none" when it fits this device's memory budget (90% of the
+        #               device, as memory_fits uses) after the allocations above, else
+        #               "selective".
+        # Numerics are identical either way (the recomputed values are bit-identical
+        # to the forward's).
+        if recompute not in ("auto", "none", "selective", "full"):
+            raise ValueError(f"recompute must be auto|none|selective|full, not {recompute!r}")
+        pairs = [(layer, m) for s in self.my_stages for layer in range(*self.ranges[s])
+                 for m in range(self.M)]
+        if recompute == "auto":
+            recompute = "none"
+            if device.type == "cuda" and self.n_tok > 0:
+                probe = alloc_acts(cfg, self.n_tok, device)
+                per = sum(t.numel() * t.element_size() for t in vars(probe).values())
+                del probe
+                budget = 0.9 * torch.cuda.get_device_properties(device).total_memory
+                if torch.cuda.memory_allocated(device) + 3 * per + len(pairs) * per > budget:
+                    recompute = "selective"
+        self.recompute = recompute if self.n_tok > 0 else "full"
+        self.kept: Dict[Tuple[int, int], tuple] = {}
+        self.kept_acts: Dict[Tuple[int, int], object] = {}
+        if self.recompute == "selective":
+            seqs = max(self.n_tok // S, 1)
+            for key in pairs:
+                self.kept[key] = (torch.empty(n, d, **bf),
+                                  torch.empty(seqs, cfg.n_head, S, device=device,
+                                              dtype=torch.float32),
+                                  torch.empty(n, d, **bf))
+        elif self.recompute == "none":
+            for key in pairs:
+                self.kept_acts[key] = alloc_acts(cfg, self.n_tok, device)
         self.rc_acts = alloc_acts(cfg, self.n_tok, device)   # one layer's recompute set
         self.fwd_acts = alloc_acts(cfg, self.n_tok, device)
-        # Selective recompute (keep_attention): the attention block's outputs of every
-        # (layer, microbatch) — attention output, its log-sum-exp and x_mid = x +
-        # proj(attn) — are kept from the forward pass, so the backward's recompute
-        # skips the attention forward and the projection GEMM (selective activation
-        # recomputation, Korthikanti et al. 2022): two extra [share*S, d] bf16 units
-        # (+ fp32 lse) per layer and microbatch.
-        self.keep_attention = bool(keep_attention) and self.n_tok > 0
-        self.kept: Dict[Tuple[int, int], tuple] = {}
-        if self.keep_attention:
-            seqs = max(self.n_tok // S, 1)
-            for s in self.my_stages:
-                for layer in range(*self.ranges[s]):
-                    for m in range(self.M):
-                        self.kept[(layer, m)] = (
-                            torch.empty(n, d, **bf),
-                            torch.empty(seqs, cfg.n_head, S, device=device, dtype=torch.float32),
-                            torch.empty(n, d, **bf))
         self.fwd_out = torch.empty(n, d, **bf)
         self.bscr = alloc_bwd_scratch(cfg, self.n_tok, device)
         self.dy_pp = [torch.empty(n, d, **bf), torch.empty(n, d, **bf)]
@@ -498,8 +522,11 @@ class StageExecutor:
                 "grads_window": self.win.n_grad_slots * self.grad_slot_bytes,
                 "optim": sum(12 * pu.shard_numel for pu in self.units.values()),
                 "checkpoints": sum(acts.values()),
-                "kept_attention": sum(a.numel() * 2 + b.numel() * 4 + c.numel() * 2
-                                      for a, b, c in self.kept.values()),
+                "kept_activations": sum(a.numel() * 2 + b.numel() * 4 + c.numel() * 2
+                                        for a, b, c in self.kept.values()) +
+                sum(t.numel() * t.element_size() for acts in self.kept_acts.values()
+                    for t in vars(acts).values()),
+                "recompute": self.recompute,
                 "grad_slots": self.win.n_grad_slots,
                 "param_slots": len(self.param_slots) or len(self.layer_slots)}
 
@@ -699,11 +726,14 @@ class StageExecutor:
 
         def body(layer):
             a = self.fwd_acts
-            if self.keep_attention:
+            if self.recompute == "selective":
                 attn, lse, x_mid = self.kept[(layer, m)]
                 a = dataclasses.replace(a, attn=attn, lse=lse, x_mid=x_mid)
+            elif self.recompute == "none":
+                a = self.kept_acts[(layer, m)]
             self.model.layer_fwd(self.units[layer].p, self.act[(layer, m)][:n],
-                                 self.act[(layer + 1, m)][:n], a, n)
+                                 self.act[(layer + 1, m)][:n], a, n,
+                                 keep_preact=self.recompute == "none")
         self._layers(list(range(lo, hi)), body)
         if s == self.n_stages - 1:
             hu = self.units["head"]
@@ -730,12 +760,15 @@ class StageExecutor:
             dx = self.gbuf[(lo, m)][:n] if j == 0 else self.dy_pp[j & 1][:n]
             u = self.units[layer]
             x = self.act[(layer, m)][:n]
-            a = self.rc_acts
-            if self.keep_attention:
-                attn, lse, x_mid = self.kept[(layer, m)]
-                a = dataclasses.replace(a, attn=attn, lse=lse, x_mid=x_mid)
-            self.model.layer_fwd(u.p, x, self.fwd_out[:n], a, n, need_out=False,
-                                 kept=self.keep_attention)
+            if self.recompute == "none":
+                a = self.kept_acts[(layer, m)]
+            else:
+                a = self.rc_acts
+                if self.recompute == "selective":
+                    attn, lse, x_mid = self.kept[(layer, m)]
+                    a = dataclasses.replace(a, attn=attn, lse=lse, x_mid=x_mid)
+                self.model.layer_fwd(u.p, x, self.fwd_out[:n], a, n, need_out=False,
+                                     kept=self.recompute == "selective")
             self.model.layer_bwd(u.p, u.g, x, state["dy"], dx, a, self.bscr, n)
             state["dy"] = dx
         self._layers(list(reversed(range(lo, hi))), body)

@@ -241,13 +241,16 @@ class GptOps:
         self.wlane = WgradLane()
 
     def layer_fwd(self, p: Dict[str, torch.Tensor], x: torch.Tensor, out: torch.Tensor,
-                  a: LayerActs, n_tok: int, need_out: bool = True, kept=False) -> None:
+                  a: LayerActs, n_tok: int, need_out: bool = True, kept=False,
+                  keep_preact=False) -> None:
         """out = block(x); fills ``a`` (the recompute set).  ``need_out=False``
         (activation recompute) skips the fc2 GEMM: backward never reads the
         block output, only its internals.  ``kept``: a.attn / a.lse / a.x_mid hold
         the attention block's outputs of this (layer, microbatch) kept from the
         forward pass, so the recompute skips the attention forward and the
-        projection GEMM (selective recompute)."""
+        projection GEMM (selective recompute).  ``keep_preact``: the forward also
+        writes the fc1 pre-activation (the backward reads it when nothing is
+        recomputed)."""
         o, cfg = self.ops, self.cfg
         n_seq = n_tok // cfg.seq_len
         o.layernorm_fwd(x, p["ln1_w"], p["ln1_b"], a.h1[:n_tok], a.mean1[:n_tok], a.rstd1[:n_tok])
@@ -259,7 +262,7 @@ class GptOps:
                    bias=p["proj_b"], resid=x)
         o.layernorm_fwd(a.x_mid[:n_tok], p["ln2_w"], p["ln2_b"], a.h2[:n_tok], a.mean2[:n_tok],
                         a.rstd2[:n_tok])
-        if need_out:  # forward pass: backward reads the recompute's pre-activation, not this one
+        if need_out and not keep_preact:  # backward reads the recompute's pre-activation
             o.gemm(a.h2[:n_tok], p["fc1_w"], a.g[:n_tok], epilogue=EPI_BIAS_GELU_NA,
                    bias=p["fc1_b"])
         else:
@@ -340,7 +343,7 @@ class LlamaOps:
         self.wlane = WgradLane()
 
     def layer_fwd(self, p, x, out, a: LlamaActs, n_tok: int, need_out: bool = True,
-                  kept=False) -> None:
+                  kept=False, keep_preact=False) -> None:
         o, cfg = self.ops, self.cfg
         n = n_tok
         n_seq = n // cfg.seq_len

@@ -27,7 +27,7 @@ class ZorseTrainer:
                  world_rank: int = 0, world_size: int = 1, seed: int = 1234,
                  adam: AdamConfig = AdamConfig(), init_device: str = "cpu",
                  schedule: str = "gpipe", streams: bool = True,
-                 offload_acts: Optional[bool] = None, keep_attention: bool = True,
+                 offload_acts: Optional[bool] = None, recompute: str = "auto",
                  _ops=None, _comms=None, _device=None):
         devices = list(ctx.graph.vertices)
         if len(devices) != world_size:
@@ -60,7 +60,7 @@ class ZorseTrainer:
         self.exec = StageExecutor(plan, ctx, cfg, self.dev_id, self.rank_of, world, group, ops,
                                   device, seed=seed, adam=adam, init_device=init_device,
                                   schedule=schedule, streams=streams, offload_acts=offload_acts,
-                                  keep_attention=keep_attention)
+                                  recompute=recompute)
         if _ops is None and world_size > 1:
             # AG-v / fused RS-v+AdamW over NVLink peer memory (csrc/peer.cu)
             from .comm import PeerGroup

@@ -79,6 +79,18 @@ def test_single_rank_matches_oracle(n_mb, counts, strategy):
     _check([_run_rank(tr, 2)], 2)
 
 
+@pytest.mark.parametrize("recompute", ["full", "selective", "none"])
+@pytest.mark.parametrize("cfg", [CFG, LLAMA], ids=["gpt", "llama"])
+def test_recompute_policies_match_oracle(recompute, cfg):
+    """The three recompute policies (paper: recompute every block internal from the
+    layer checkpoint; selective: keep the attention block's outputs; none: keep the
+    whole recompute set) give the same step, two ministages x two microbatches."""
+    plan, ctx = _setup([("n0", ["b200"])], [["n0-0"]], 2, [2], "zorse", cfg=cfg)
+    tr = ZorseTrainer(plan, ctx, cfg, _ops=cpu_ops, recompute=recompute)
+    assert tr.exec.recompute == recompute
+    _check([_run_rank(tr, 2)], 2, cfg)
+
+
 @pytest.mark.parametrize("n_mb,counts", [(4, [1]), (8, [2])])
 def test_activation_offload_matches_oracle(n_mb, counts):
     """OffloadAct / LoadAct as real host copies with a 2-microbatch device ring for

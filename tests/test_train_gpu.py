@@ -60,9 +60,10 @@ def run_and_compare(tr, cfg, batches, lr=1e-3):
     # activation offload to pinned host memory (OffloadAct / LoadAct on the host stream)
     (E.TINY_GPT, 8, 4, [1], "zorse", True),
 ])
-def test_training_steps_match_oracle(cuda, cfg, gb, n_mb, counts, strategy, offload):
+@pytest.mark.parametrize("recompute", ["auto", "full"])
+def test_training_steps_match_oracle(cuda, cfg, gb, n_mb, counts, strategy, offload, recompute):
     plan, ctx = _setup(cfg, gb, n_mb, counts, strategy)
-    tr = ZorseTrainer(plan, ctx, cfg, offload_acts=offload)
+    tr = ZorseTrainer(plan, ctx, cfg, offload_acts=offload, recompute=recompute)
     assert tr.exec.offload == offload
     batches = [synthetic_batch(cfg.vocab, cfg.seq_len, gb, s) for s in (1, 2)]
     losses, records = run_and_compare(tr, cfg, batches)
