@@ -428,6 +428,8 @@ def run_ours(args):
                 "n_microbatches": plan.n_microbatches, "ministages": len(plan.groups[0].ministage_sizes),
                 "collectives": "nvlink peer memory" if world > 1 else None,
                 "l2": "per-step working set (params+grads+activations) >> 126 MB L2; no flush",
+                "recompute": ex.recompute,
+                "max_memory_allocated_gib": torch.cuda.max_memory_allocated() / 2**30,
             },
             "loss": loss,
             "model_tflops_per_gpu": step_flops * args.steps / (ms * 1e-3) / 1e12 / world,
