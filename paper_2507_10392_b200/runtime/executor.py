@@ -472,6 +472,7 @@ class StageExecutor:
             self.hf_mean = torch.empty(n, device=device)
             self.hf_rstd = torch.empty(n, device=device)
             self.dhf = torch.empty(n, d, **bf)
+            self.dhf32 = torch.empty(n, d, device=device, dtype=torch.float32)
         self.tokens = torch.zeros(self.M, n, device=device, dtype=torch.int32)
         self.labels = torch.zeros(self.M, n, device=device, dtype=torch.int32)
         self.loss_sum = torch.zeros(1, device=device, dtype=torch.float32)
@@ -536,8 +537,8 @@ class StageExecutor:
         the current stream; does not synchronise."""
         self.step_count += 1
         self.ops.step_increment(self.step_dev)
-        self.loss_sum.zero_()
-        self.gsumsq.zero_()
+        self.ops.fill_f32(self.loss_sum, 0.0)
+        self.ops.fill_f32(self.gsumsq, 0.0)
         self._done = {}
         if not self.multistream:
             for ev in self.events:
@@ -633,7 +634,7 @@ class StageExecutor:
                 for u in self.chunks[prev]:
                     self.group_comm.wait_consumed(self.units[u], 0 if same_step else -1,
                                                   self.step_dev)
-            region[:used].zero_()
+            self.ops.fill_f32(region[:used], 0.0)
         if ps is not None:
             e = torch.cuda.Event()
             e.record(ps)
@@ -740,7 +741,7 @@ class StageExecutor:
             self.model.head_fwd_bwd(hu.p, hu.g, self.act[(hi, m)][:n], self.labels[m],
                                     self.gbuf[(hi, m)][:n], self.logits, self.hf, self.hf_mean,
                                     self.hf_rstd, self.dhf, self.loss_sum,
-                                    1.0 / self.global_tokens, n)
+                                    1.0 / self.global_tokens, n, dhf32=self.dhf32)
 
     def _on_bwd(self, ev: Event) -> None:
         """Recompute + backward, layer by layer in reverse (each layer's internals are

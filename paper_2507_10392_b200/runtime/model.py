@@ -317,7 +317,7 @@ class GptOps:
         self.ops.embedding_bwd(tokens[:n_tok], dx, gr["wte"], gr["wpe"], self.cfg.seq_len)
 
     def head_fwd_bwd(self, p, gr, x, labels, dx, logits, hf, mean, rstd, dhf, loss_sum, scale,
-                     n_tok):
+                     n_tok, dhf32=None):
         """Final LayerNorm + LM head + cross-entropy, and straight away its
         backward: dx (grad of the last block's output) and head grads."""
         o = self.ops
@@ -327,7 +327,7 @@ class GptOps:
         o.xent_fwd_bwd(logits[:n], labels[:n], loss_sum, logits[:n], scale)
         # (LM-head wgrad inline: forking it measured neutral; both GEMMs fill the GPU)
         o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
-        o.gemm(logits[:n], p["head_w"], dhf[:n], b_t=True)
+        head_dgrad(o, logits[:n], p["head_w"], dhf[:n], None if dhf32 is None else dhf32[:n])
         o.layernorm_bwd(dhf[:n], x, p["lnf_w"], mean[:n], rstd[:n], dx, gr["lnf_w"], gr["lnf_b"])
 
 
@@ -397,7 +397,7 @@ class LlamaOps:
         self.ops.embedding_bwd(tokens[:n_tok], dx, gr["wte"], None, self.cfg.seq_len)
 
     def head_fwd_bwd(self, p, gr, x, labels, dx, logits, hf, mean, rstd, dhf, loss_sum, scale,
-                     n_tok):
+                     n_tok, dhf32=None):
         o = self.ops
         n = n_tok
         o.rmsnorm_fwd(x, p["norm_w"], hf[:n], rstd[:n])
@@ -405,8 +405,21 @@ class LlamaOps:
         o.xent_fwd_bwd(logits[:n], labels[:n], loss_sum, logits[:n], scale)
         # (LM-head wgrad inline: forking it measured neutral; both GEMMs fill the GPU)
         o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
-        o.gemm(logits[:n], p["head_w"], dhf[:n], b_t=True)
+        head_dgrad(o, logits[:n], p["head_w"], dhf[:n], None if dhf32 is None else dhf32[:n])
         o.rmsnorm_bwd(dhf[:n], x, p["norm_w"], rstd[:n], dx, gr["norm_w"])
+
+
+def head_dgrad(o, dlogits, head_w, dhf, dhf32=None) -> None:
+    """dhf = dlogits @ head_w.  The output has only d columns (3-4 tiles across) and K is
+    the vocabulary, so a bf16 GEMM runs 1.3 waves of tiles; accumulating in fp32 with
+    K split (TMA reduce-add) fills the GPU and the cast back is a 6 us pass: 529 -> 467
+    us at GPT-2 small (profiles/r02_gemm_ab.jsonl)."""
+    if dhf32 is None:
+        o.gemm(dlogits, head_w, dhf, b_t=True)
+        return
+    o.fill_f32(dhf32, 0.0)
+    o.gemm(dlogits, head_w, dhf32, b_t=True, epilogue=EPI_F32, beta=1.0)
+    o.cast_f32_bf16(dhf32, dhf)
 
 
 def make_model_ops(cfg: ModelConfig, ops):

@@ -21,6 +21,7 @@ SHAPES = [  # (name, M, N, K, kwargs builder)
     ("fc2 fwd bias+resid", T, 768, 3072, "bias_resid"), ("fc2 dgrad gelu'", T, 3072, 768, "gelu_bwd"),
     ("fc1 dgrad", T, 768, 3072, "dgrad"), ("qkv dgrad", T, 768, 2304, "dgrad"),
     ("fc1 wgrad", 3072, 768, T, "wgrad"), ("lm head", T, 50304, 768, "plain"),
+    ("lm dgrad bf16", T, 768, 50304, "dgrad"), ("lm dgrad f32 split-K", T, 768, 50304, "dgrad_f32"),
 ]
 
 
@@ -30,15 +31,18 @@ def main():
     for name, M, N, Kd, kind in SHAPES:
         r = lambda *s: (torch.randn(*s, device="cuda") * 0.05).bfloat16()  # noqa: E731
         kw = {}
-        if kind == "dgrad":
+        if kind in ("dgrad", "dgrad_f32"):
             a, b = r(M, Kd), r(Kd, N)
             kw["b_t"] = True
+            if kind == "dgrad_f32":
+                kw.update(epilogue=K.EPI_F32, beta=1.0)
         elif kind == "wgrad":
             a, b = r(Kd, M), r(Kd, N)
             kw.update(a_t=True, b_t=True, epilogue=K.EPI_F32, beta=1.0)
         else:
             a, b = r(M, Kd), r(N, Kd)
-        o = torch.empty(M, N, device="cuda", dtype=torch.float32 if kind == "wgrad" else torch.bfloat16)
+        o = torch.empty(M, N, device="cuda",
+                        dtype=torch.float32 if kind in ("wgrad", "dgrad_f32") else torch.bfloat16)
         if kind in ("bias", "bias_resid", "gelu", "gelu_na"):
             kw["bias"] = r(N)
         if kind == "bias":
@@ -65,6 +69,8 @@ def main():
             torch.cuda.synchronize()
             best = min(best, s.elapsed_time(e) / 20)
         out.append({"gemm": name, "M": M, "N": N, "K": Kd, "us": best * 1e3,
+                    "tile": K.gemm_choice(M, N, Kd, a_t=kw.get("a_t", False), b_t=kw.get("b_t", False),
+                                          epilogue=kw.get("epilogue", 0), beta=kw.get("beta", 0.0)),
                     "tflops": 2 * M * N * Kd / (best * 1e-3) / 1e12})
         print(json.dumps(out[-1]), flush=True)
 

@@ -30,6 +30,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--append", action="store_true", help="keep entries of other shapes")
+    ap.add_argument("--out", default=TABLE, help="where to write the table")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     cfg, plan, ctx, gb = bench.build_workload(args.gpus)
@@ -70,14 +71,14 @@ def main():
             parts = ln.split()
             if len(parts) == 12 and parts[0] == TAG and tuple(map(int, parts[1:9])) not in rows:
                 old.append(ln.rstrip("\n"))
-    with open(TABLE, "w") as fh:
+    with open(args.out, "w") as fh:
         fh.write("# zorse B200 GEMM tile table (scripts/tune_gemm.py): tag M N K a_mn b_mn epi "
                  "beta1 ldc pair bn splits\n")
         for ln in old:
             fh.write(ln + "\n")
         for key, val in rows.items():
             fh.write(" ".join(map(str, (TAG,) + key + val)) + "\n")
-    print(f"wrote {len(rows)} shapes (+{len(old)} kept) to {TABLE}")
+    print(f"wrote {len(rows)} shapes (+{len(old)} kept) to {args.out}")
 
 
 if __name__ == "__main__":
