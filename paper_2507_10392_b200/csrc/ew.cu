@@ -24,12 +24,23 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
   if (row >= rows) return;
   const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * d);
   const int nv = d >> 3;
-  uint4 q[MAXV];
+  uint4 q[MAXV], qw[MAXV], qb[MAXV];
   float s = 0.f;
+  // weight / bias vectors are loaded with the row, so their latency overlaps the
+  // two reductions instead of following them
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  const uint4* br = reinterpret_cast<const uint4*>(b);
 #pragma unroll
   for (int j = 0; j < MAXV; ++j) {
     const int v = lane + 32 * j;
     q[j] = v < nv ? xr[v] : make_uint4(0, 0, 0, 0);
+    if (v < nv) {
+      qw[j] = wr[v];
+      qb[j] = br[v];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
     const uint32_t* qi = &q[j].x;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -51,15 +62,12 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
     }
   }
   const float rstd = rsqrtf(warp_sum(ss) / d + eps);
-  const uint4* wr = reinterpret_cast<const uint4*>(w);
-  const uint4* br = reinterpret_cast<const uint4*>(b);
   uint4* yr = reinterpret_cast<uint4*>(y + (size_t)row * d);
 #pragma unroll
   for (int j = 0; j < MAXV; ++j) {
     const int v = lane + 32 * j;
     if (v >= nv) continue;
-    const uint4 qw = wr[v], qb = br[v];
-    const uint32_t *qi = &q[j].x, *wi = &qw.x, *bi = &qb.x;
+    const uint32_t *qi = &q[j].x, *wi = &qw[j].x, *bi = &qb[j].x;
     uint4 o;
     uint32_t* oi = &o.x;
 #pragma unroll
@@ -98,23 +106,23 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(
   const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * d);
   const uint4* wr = reinterpret_cast<const uint4*>(w);
   const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + (size_t)row * d) : nullptr;
-  uint4 qd[MAXV], qx[MAXV], qr[MAXV];
+  uint4 qd[MAXV], qx[MAXV], qr[MAXV], qw[MAXV];
+  const float mean = mean_in[row], rstd = rstd_in[row];
 #pragma unroll
-  for (int j = 0; j < MAXV; ++j) {
+  for (int j = 0; j < MAXV; ++j) {   // every load of the row in flight at once
     const int v = lane + 32 * j;
     const bool ok = v < nv;
     qd[j] = ok ? dyr[v] : make_uint4(0, 0, 0, 0);
     qx[j] = ok ? xr[v] : make_uint4(0, 0, 0, 0);
     qr[j] = (ok && rr) ? rr[v] : make_uint4(0, 0, 0, 0);
+    qw[j] = ok ? wr[v] : make_uint4(0, 0, 0, 0);
   }
-  const float mean = mean_in[row], rstd = rstd_in[row];
   float sg = 0.f, sgx = 0.f;
 #pragma unroll
   for (int j = 0; j < MAXV; ++j) {
     const int v = lane + 32 * j;
     if (v >= nv) continue;
-    const uint4 qw = wr[v];
-    const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw.x;
+    const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw[j].x;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       float2 dv = unpack_bf16(di[k]), xv = unpack_bf16(xi[k]), wv = unpack_bf16(wi[k]);
@@ -130,8 +138,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(
   for (int j = 0; j < MAXV; ++j) {
     const int v = lane + 32 * j;
     if (v >= nv) continue;
-    const uint4 qw = wr[v];
-    const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw.x, *ri = &qr[j].x;
+    const uint32_t *di = &qd[j].x, *xi = &qx[j].x, *wi = &qw[j].x, *ri = &qr[j].x;
     uint4 o;
     uint32_t* oi = &o.x;
 #pragma unroll
