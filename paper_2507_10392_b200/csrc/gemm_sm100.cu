@@ -101,12 +101,23 @@ constexpr int kSmemMax = 232448;  // max dynamic shared memory per block (227 KB
 // Chunk range [cb, ce) of epilogue part p for a tile of `nch` 32-column chunks.
 __host__ __device__ constexpr int epi_cb(int p, int nch) { return p * nch / kEpiParts; }
 
+// Epilogue staging slots (2 KB each) per epilogue warp: 4 when the smem budget holds
+// them without losing a pipeline stage or still leaves >= 6 stages (the TMA stores of
+// up to three earlier chunks then stay in flight), else 2.
+constexpr int epi_slots(int stage_bytes) {
+  return ((kSmemMax - 1536 - kEpiWarps * 8192) / stage_bytes ==
+              (kSmemMax - 1536 - kEpiWarps * 4096) / stage_bytes ||
+          (kSmemMax - 1536 - kEpiWarps * 8192) / stage_bytes >= 6)
+             ? 4 : 2;
+}
+
 template <int BN>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * 4096;  // per-epilogue-warp TMA staging
+  static constexpr int NS = epi_slots(STAGE_BYTES);
+  static constexpr int EPI_BYTES = kEpiWarps * NS * 2048;  // per-epilogue-warp TMA staging
   static constexpr int FIT = (kSmemMax - 1536 - EPI_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = FIT < 8 ? FIT : 8;
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;  // two accumulators, pow2 alloc
@@ -249,7 +260,6 @@ ZB_DEVICE void epilogue_chunk(const GemmArgs& args, const uint32_t (&r)[32], int
 // pieces per instruction.  Residual / GELU-backward operands are TMA-loaded into
 // the slot (prefetched one chunk ahead) and read back from shared memory.
 constexpr int kEpiSlot = 2048;
-constexpr int kEpiWarpBytes = 2 * kEpiSlot;
 
 struct EpiMaps {
   const CUtensorMap* C;
@@ -288,7 +298,7 @@ ZB_DEVICE void ld_row_bf16(const uint8_t* slot, int r, float (&o)[32]) {
 // quarter in the accumulator; chunks [cb, ce) of 32 columns; row0 / n0 = global
 // coordinates of the slab's first row / the tile's first column.  `release` is
 // called once the last TMEM read retired (the accumulator may be reused).
-template <int EPI, typename Release>
+template <int EPI, int NS, typename Release>
 ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* stg,
                             uint64_t* ebar, uint32_t& eph, uint32_t& ecnt, uint32_t tacc,
                             uint64_t* tfull,
@@ -375,25 +385,38 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
       }
       st_row_bf16(slot, lane, v);   // in place: each thread rewrites only its own row
     } else if (EPI == EPI_F32) {
-      if (lane == 0) bulk_wait_read<0>();  // one 4 KB slot
+      // one 4 KB slot per chunk; with NS = 4 two of them alternate (the slot written
+      // now was last stored two chunks ago)
+      slot = stg + (NS == 4 ? (ecnt & 1) * 2 * kEpiSlot : 0);
+      ++ecnt;
+      if (lane == 0) {
+        if (NS == 4) bulk_wait_read<1>(); else bulk_wait_read<0>();
+      }
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        *reinterpret_cast<float4*>(stg + sw128(lane, j)) =
+        *reinterpret_cast<float4*>(slot + sw128(lane, j)) =
             make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
     } else if (EPI == EPI_BIAS_GELU) {
-      if (lane == 0) bulk_wait_read<0>();  // aux -> slot 0, C -> slot 1
+      // aux -> even slot, C -> odd slot of a pair; with NS = 4 two pairs alternate
+      slot = stg + (NS == 4 ? (ecnt & 1) * 2 * kEpiSlot : 0);
+      ++ecnt;
+      if (lane == 0) {
+        if (NS == 4) bulk_wait_read<1>(); else bulk_wait_read<0>();
+      }
       __syncwarp();
-      st_row_bf16(stg, lane, v);
+      st_row_bf16(slot, lane, v);
       gelu32_bf16in(v);   // GELU of the bf16-rounded pre-activation (= the stored aux)
-      st_row_bf16(stg + kEpiSlot, lane, v);
+      st_row_bf16(slot + kEpiSlot, lane, v);
     } else {
       if (EPI == EPI_BIAS_GELU_NA) gelu32_bf16in(v);
-      // slots alternate over a running chunk count (across tiles), so the slot
-      // written now was last stored two chunks ago
-      slot = stg + (ecnt & 1) * kEpiSlot;
+      // slots rotate over a running chunk count (across tiles), so the slot written
+      // now was last stored NS chunks ago
+      slot = stg + (ecnt % NS) * kEpiSlot;
       ++ecnt;
-      if (lane == 0) bulk_wait_read<1>();
+      if (lane == 0) {
+        if (NS == 4) bulk_wait_read<3>(); else bulk_wait_read<1>();
+      }
       __syncwarp();
       st_row_bf16(slot, lane, v);
     }
@@ -402,12 +425,12 @@ ZB_DEVICE void epilogue_tma(const GemmArgs& args, const EpiMaps& maps, uint8_t* 
     if (lane == 0) {
       if (EPI == EPI_F32) {
         if (args.splits > 1 || args.beta != 0.f)
-          tma_reduce_add_2d(maps.C, stg, col0, row0);
+          tma_reduce_add_2d(maps.C, slot, col0, row0);
         else
-          tma_store_2d(maps.C, stg, col0, row0);
+          tma_store_2d(maps.C, slot, col0, row0);
       } else if (EPI == EPI_BIAS_GELU) {
-        tma_store_2d(maps.aux, stg, col0, row0);
-        tma_store_2d(maps.C, stg + kEpiSlot, col0, row0);
+        tma_store_2d(maps.aux, slot, col0, row0);
+        tma_store_2d(maps.C, slot + kEpiSlot, col0, row0);
       } else {
 #if ZB_GEMM_EXP != 1  // experiment 1: no output stores
         tma_store_2d(maps.C, slot, col0, row0);
@@ -572,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int local = 0;
     if (args.tma_epi) {
       const EpiMaps maps{&tmC, &tmAux, &tmR};
-      uint8_t* stg = smE + (warp - 4) * kEpiWarpBytes;
+      uint8_t* stg = smE + (warp - 4) * Cfg::NS * kEpiSlot;
       uint64_t* ebar = epi_bar + 2 * (warp - 4);
       uint32_t eph = 0, ecnt = 0;
       for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
@@ -582,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_mn(args, tile, mt, nt);
         const int m0 = mt * BM;
         const int n0 = nt * BN;
-        epilogue_tma<EPI>(args, maps, stg, ebar, eph, ecnt,
+        epilogue_tma<EPI, Cfg::NS>(args, maps, stg, ebar, eph, ecnt,
                           tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN, &tfull_bar[acc],
                           (local >> 1) & 1, m0 + ew * 32, n0, cb, ce, lane,
                           [&] { if (lane == 0) mbar_arrive(&tempty_bar[acc]); });
@@ -634,7 +657,8 @@ struct Gemm2Cfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * 4096;
+  static constexpr int NS = epi_slots(STAGE_BYTES);
+  static constexpr int EPI_BYTES = kEpiWarps * NS * 2048;
   static constexpr int FIT = (kSmemMax - 1536 - EPI_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = FIT < 8 ? FIT : 8;
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
@@ -809,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int local = 0;
     if (args.tma_epi) {
       const EpiMaps maps{&tmC, &tmAux, &tmR};
-      uint8_t* stg = smE + (warp - 4) * kEpiWarpBytes;
+      uint8_t* stg = smE + (warp - 4) * Cfg::NS * kEpiSlot;
       uint64_t* ebar = epi_bar + 2 * (warp - 4);
       uint32_t eph = 0, ecnt = 0;
       for (int unit = cluster; unit < num_units; unit += nclusters, ++local) {
@@ -819,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         coords(tile, mt, nt);
         const int m0 = mt * 256 + (int)rank * 128;
         const int n0 = nt * BN;
-        epilogue_tma<EPI>(args, maps, stg, ebar, eph, ecnt,
+        epilogue_tma<EPI, Cfg::NS>(args, maps, stg, ebar, eph, ecnt,
                           tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN, &tfull_bar[acc],
                           (local >> 1) & 1, m0 + ew * 32, n0, cb, ce, lane, [&] {
                             if (lane == 0) {

@@ -1,9 +1,13 @@
 #!/bin/bash
 mkdir -p gpurun_out
-python scripts/gemm_ab.py > gpurun_out/gemm_ab_new_1.jsonl 2>&1
-cat gpurun_out/gemm_ab_new_1.jsonl | python -c "
-import json,sys
-for l in sys.stdin:
-    try: d=json.loads(l)
-    except Exception: print(l.strip()); continue
-    print(f\"{d['gemm']:28s} {d['us']:8.1f} us {d['tflops']:7.1f} TF/s tile {d['tile']}\")"
+for i in 1 2; do
+python scripts/gemm_ab.py paper_2507_10392_b200/libzorse_b200_old.so > gpurun_out/gemm_ab_old_$i.jsonl 2>&1
+python scripts/gemm_ab.py > gpurun_out/gemm_ab_new_$i.jsonl 2>&1
+done
+python - <<'PY'
+import json
+def load(f): return {d["gemm"]: d for d in map(json.loads, open(f)) }
+for i in (1, 2):
+    o, n = load(f"gpurun_out/gemm_ab_old_{i}.jsonl"), load(f"gpurun_out/gemm_ab_new_{i}.jsonl")
+    for k in o: print(i, f"{k:28s} old {o[k]['tflops']:7.1f} new {n[k]['tflops']:7.1f} TF/s  x{n[k]['tflops']/o[k]['tflops']:.3f} {n[k]['tile']}")
+PY
