@@ -226,6 +226,23 @@ int zb_peer_rs_adamw(void* const* bases, int nranks, int me, uint64_t grad_off, 
 int zb_min_cut(const double* weights, int64_t n, const int64_t* lexrank, double* cut_out,
                int64_t* side_out, int64_t* side_len);
 
+/* ---- host: planner Eq.1 latency (csrc/eq1.cpp) ---------------------------------------
+ * Iteration latency of one candidate plan — the planner's hot loop (costs.py:204-535:
+ * _compute_per_microbatch :220-249, phase recurrence :323-360, total_iteration_latency
+ * :384-535), bit-identical to the Python restatement.  n ministages in global order:
+ * grp[s], q[s] (group, round); layer classes of stage s = lay_cls[lay_off[s] ..
+ * lay_off[s+1]); distinct (kind, share > 0) members of its group = mem_kind / mem_share
+ * [mem_off[s] .. mem_off[s+1]); fits[(kind * n_cls + cls) * 4 + {fwd_alpha, fwd_beta,
+ * bwd_alpha, bwd_beta}]; ag / rs / p2p / stage_params per stage (summed AllGather,
+ * ReduceScatter, incoming boundary transfer time, parameter count); group_size per
+ * group.  out = {l_forwards, l_backwards, l_startup}. */
+int zb_eq1_latency(int n, int m, int z3, int offloads, int rounds, const int* grp, const int* q,
+                   const int* lay_off, const int* lay_cls, const int* mem_off,
+                   const int* mem_kind, const int* mem_share, int n_cls, const double* fits,
+                   const double* ag, const double* rs, const double* p2p,
+                   const double* stage_params, int n_groups, const int* group_size,
+                   double optim_per_param, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,8 @@ SIGNATURES = {
     "zb_peer_set_timeout": [ctypes.c_double],
     "zb_peer_rs_adamw": [P, I, I, U64, I64, I64, U64, P, P, P, P, P, P, P, F, F, F, F, F, F, P, P],
     "zb_min_cut": [P, I64, P, P, P, P],
+    "zb_eq1_latency": [I, I, I, I, I, P, P, P, P, P, P, P, I, P, P, P, P, P, I, P,
+                       ctypes.c_double, P],
     "zb_version": [],
     "zb_device_sync": [],
 }

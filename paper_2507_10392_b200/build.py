@@ -58,6 +58,8 @@ def build(verbose: bool = False, jobs: int = 8, defines=(), out: str = OUT) -> s
                *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
+        else:  # host planner code: no FMA contraction (bit parity with the Python planner)
+            cmd[1:1] = ["-Xcompiler", "-ffp-contract=off"]
         cmds.append(cmd)
     procs = []
     for cmd in cmds:

@@ -10,6 +10,7 @@ types, so a plan selected here is byte-identical to the reference's plan file
 
 from __future__ import annotations
 
+import ctypes
 from typing import TYPE_CHECKING, Dict, List, Optional, Sequence, Tuple
 
 from .costs import (CostContext, LatencyEstimate, MemoryEstimate, Strategy, allgather_time,
@@ -137,8 +138,89 @@ def phase_makespan(groups_seq, chain_mb, lane_round, head_round, rs_tail, d_in, 
     return t_chain, lane_end
 
 
+def _native_eq1():
+    from .mincut import native_kernel
+    if native_kernel() is None:      # library absent: the Python restatement below
+        return None
+    from .._lib import lib
+    return lib().zb_eq1_latency
+
+
+def _fit_table(ctx: CostContext):
+    """(kind index, class index, flat fits) of the runtime model, cached on it."""
+    rt = ctx.runtime
+    tab = getattr(rt, "_zb_fit_table", None)
+    if tab is None:
+        kinds = sorted({k for k, _ in rt.fits})
+        classes = sorted({c for _, c in rt.fits})
+        flat = []
+        for k in kinds:
+            for c in classes:
+                f = rt.fits.get((k, c))
+                flat += [f.fwd_alpha, f.fwd_beta, f.bwd_alpha, f.bwd_beta] if f else [0.0] * 4
+        tab = ({k: i for i, k in enumerate(kinds)}, {c: i for i, c in enumerate(classes)},
+               (ctypes.c_double * len(flat))(*flat), len(classes))
+        rt._zb_fit_table = tab
+    return tab
+
+
 def total_iteration_latency(ctx: CostContext, plan: "TrainingPlan") -> LatencyEstimate:
-    """Eq.1: forward pass + backward pass + trailing optimizer (costs.py:384-535)."""
+    """Eq.1: forward pass + backward pass + trailing optimizer (costs.py:384-535).
+
+    The per-microbatch compute times and the phase recurrences run in C++
+    (csrc/eq1.cpp, ``zb_eq1_latency``) when the library is present — bit-identical
+    to ``total_iteration_latency_py`` (tests/test_plan_units.py) — like the
+    reference's compiled min-cut with its Python twin (partition.py:26-38)."""
+    fn = _native_eq1()
+    if fn is None:
+        return total_iteration_latency_py(ctx, plan)
+    v = _PlanView(ctx, plan)
+    n = v.n
+    kind_ix, cls_ix, fits, n_cls = _fit_table(ctx)
+    grp, q, lay_off, lay_cls, mem_off, mem_kind, mem_share = [], [], [0], [], [0], [], []
+    ag, rs, params = [], [], []
+    members = {}
+    for s, (g, qq) in enumerate(v.order):
+        grp.append(g)
+        q.append(qq)
+        layers = v.layers(s)
+        lay_cls += [cls_ix[ctx.model.class_of(layer)] for layer in layers]
+        lay_off.append(len(lay_cls))
+        mem = members.get(g)
+        if mem is None:
+            group, seen, mem = plan.groups[g], set(), []
+            for dev in group.devices:
+                share = group.shares[dev.id]
+                if share <= 0 or (dev.kind, share) in seen:
+                    continue
+                seen.add((dev.kind, share))
+                mem.append((kind_ix[dev.kind], share))
+            members[g] = mem
+        for k, share in mem:
+            mem_kind.append(k)
+            mem_share.append(share)
+        mem_off.append(len(mem_kind))
+        ag.append(sum(v.gathers(s)))
+        rs.append(v.scatter(s))
+        params.append(float(sum(ctx.model.params_of(layer) for layer in layers)))
+    p2p = v.boundary_p2p()
+    I = lambda xs: (ctypes.c_int * len(xs))(*xs)  # noqa: E731,E741
+    D = lambda xs: (ctypes.c_double * len(xs))(*xs)  # noqa: E731
+    out = (ctypes.c_double * 3)()
+    sizes = [len(g.devices) for g in plan.groups]
+    rc = fn(n, plan.n_microbatches, int(plan.strategy.gathers_per_microbatch),
+            int(plan.strategy.offloads), plan.n_ministage_rounds, I(grp), I(q), I(lay_off),
+            I(lay_cls), I(mem_off), I(mem_kind), I(mem_share), n_cls, fits, D(ag), D(rs), D(p2p),
+            D(params), len(sizes), I(sizes), ctypes.c_double(ctx.optim_update_per_param), out)
+    if rc:
+        from .._lib import lib
+        raise ValueError(lib().zb_last_error().decode())
+    return LatencyEstimate(l_forwards=out[0], l_backwards=out[1], l_startup=out[2],
+                           n_ministages=plan.n_ministage_rounds)
+
+
+def total_iteration_latency_py(ctx: CostContext, plan: "TrainingPlan") -> LatencyEstimate:
+    """Eq.1 in Python (the restatement the C++ path is pinned against)."""
     v = _PlanView(ctx, plan)
     n, m = v.n, plan.n_microbatches
     z3 = plan.strategy.gathers_per_microbatch

@@ -179,3 +179,30 @@ def test_native_min_cut_matches_numpy_twin():
         w = w + w.T
         rank = rng.permutation(n).astype(np.int64)
         assert MC.min_cut_native(w, rank) == MC.min_cut_python(w, rank), trial
+
+
+def test_native_eq1_latency_bit_identical():
+    """zb_eq1_latency (csrc/eq1.cpp) equals the Python Eq.1 restatement bit for bit on
+    every golden plan (reference layouts, searches, the reference's agreement suite)."""
+    import json
+    import os
+    from paper_2507_10392_b200.plan import estimate as ES
+    if ES._native_eq1() is None:
+        pytest.skip("library not built")
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    cases = json.load(open(os.path.join(gold, "plans.json")))
+    checked = 0
+    for case in cases:
+        prof = P.load_cluster_profile(os.path.join(gold, case["cluster"]))
+        model, workload = P.load_model_workload(os.path.join(gold, case["model"]))
+        ctx = P.CostContext(graph=P.build_cluster_graph(prof), runtime=P.fit_runtime_model(prof),
+                            model=model, workload=workload)
+        plan = P.TrainingPlan.from_json_dict(json.loads(case["plan_json"]), prof)
+        for strat in (P.Strategy.INTERLEAVED, P.Strategy.PP_ZERO2, P.Strategy.PP_ZERO3):
+            plan.strategy = strat
+            a = ES.total_iteration_latency(ctx, plan)
+            b = ES.total_iteration_latency_py(ctx, plan)
+            assert (a.l_forwards, a.l_backwards, a.l_startup) == \
+                (b.l_forwards, b.l_backwards, b.l_startup), (case["name"], strat)
+            checked += 1
+    assert checked == 3 * len(cases)
