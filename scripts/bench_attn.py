@@ -1,6 +1,9 @@
 """Time the tcgen05 attention kernels at GPT-2 / Llama shapes (TF/s, causal FLOPs)."""
 import sys, os, json, math
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2507_10392_b200 import _lib
+if len(sys.argv) > 1:   # A/B: another library build
+    _lib.LIB_PATH = os.path.abspath(sys.argv[1])
 import torch
 from paper_2507_10392_b200 import kernels as K
 
