@@ -756,7 +756,13 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
   uint64_t* p_full = s_full + 2;          // [2] per tile (count 4)
   uint64_t* o_done = s_full + 4;          // [2] per tile: last PV of the item
   uint64_t* o_empty = s_full + 6;         // [2] per tile: epilogue read O (count 4)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
+  uint64_t* pv_done = s_full + 8;         // [2] per tile: each PV MMA complete (SEP)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 10);
+  // SEP (D = 64): P is written to its own TMEM columns [384 + 64x, 448 + 64x) instead of
+  // over S, so S_x(j+1) is issued as soon as the softmax of block j is done reading
+  // S_x(j) — before PV_x(j) — and the next softmax waits one MMA less.  The softmax then
+  // waits PV_x(j) (pv_done) before rescaling O or writing P(j+1).
+  constexpr bool SEP = D == 64;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int npair = S / (2 * BQ);
@@ -786,6 +792,7 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
       mbar_init(&p_full[x], 4 * HV);
       mbar_init(&o_done[x], 1);
       mbar_init(&o_empty[x], 4 * HV);
+      mbar_init(&pv_done[x], 1);
     }
     fence_barrier_init();
   }
@@ -798,6 +805,7 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
   griddep_launch();
   const uint32_t t_s[2] = {tmem, tmem + 128};
   const uint32_t t_o[2] = {tmem + 256, tmem + 256 + D};
+  const uint32_t t_p[2] = {tmem + 384, tmem + 448};   // SEP only
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -842,6 +850,7 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
       constexpr uint32_t idesc_o = umma_idesc_bf16(BQ, D, 0, 1);
       const uint32_t q_base0 = smem_u32(sm + L::OFF_QA), q_base1 = smem_u32(sm + L::OFF_QB);
       const uint32_t ts0 = tmem, ts1 = tmem + 128, to0 = tmem + 256, to1 = tmem + 256 + D;
+      const uint32_t tp0 = tmem + 384, tp1 = tmem + 448;
       int g = 0, lt = 0;
       int ns0 = 0, ns1 = 0;  // S blocks issued per tile (parity of p_full waits)
       // (tile index x is a compile-time constant in every call below: no
@@ -878,10 +887,13 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
           for (int kk = 0; kk < BKV / 16; ++kk) {
             const uint64_t bdesc = umma_desc_sw128(
                 v_base + (kk >> 2) * (D / 64) * 8192 + (kk & 3) * 2048, 8192, 1024);
-            // P keys [64h, 64h+64) sit in the S columns of half h (see the softmax)
-            const uint32_t a_tm = HV == 2 ? tsx + (kk >> 2) * 64 + (kk & 3) * 8 : tsx + kk * 8;
+            // P keys [64h, 64h+64) sit in the S columns of half h (see the softmax), or
+            // contiguously in the tile's own P columns (SEP)
+            const uint32_t a_tm = SEP ? (x ? tp1 : tp0) + kk * 8
+                                      : (HV == 2 ? tsx + (kk >> 2) * 64 + (kk & 3) * 8 : tsx + kk * 8);
             mma_bf16_ts(tox, a_tm, bdesc, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           }
+          if (SEP) mma_commit(&pv_done[x]);
           if (j == (x ? qb : qa)) mma_commit(&o_done[x]);
         };
         using X0 = std::integral_constant<int, 0>;
@@ -889,13 +901,26 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
         issue_s(X0{}, 0);
         issue_s(X1{}, 0);
         for (int j = 0; j <= qb; ++j) {
-          if (j <= qa) {
-            issue_pv(X0{}, j);
-            if (j + 1 <= qa) issue_s(X0{}, j + 1);
+          if constexpr (SEP) {
+            // S_x(j+1) right after the softmax released S_x(j) (p_full), then PV_x(j)
+            if (j <= qa) {
+              mbar_wait(&p_full[0], ns0 & 1);
+              if (j + 1 <= qa) issue_s(X0{}, j + 1);
+              issue_pv(X0{}, j);
+            }
+            mbar_wait(&p_full[1], ns1 & 1);
+            if (j + 1 <= qb) issue_s(X1{}, j + 1);
+            issue_pv(X1{}, j);
+            mma_commit(&kv_empty[(g + j) % NST]);  // K_j, V_j no longer read
+          } else {
+            if (j <= qa) {
+              issue_pv(X0{}, j);
+              if (j + 1 <= qa) issue_s(X0{}, j + 1);
+            }
+            issue_pv(X1{}, j);
+            mma_commit(&kv_empty[(g + j) % NST]);  // K_j, V_j no longer read
+            if (j + 1 <= qb) issue_s(X1{}, j + 1);
           }
-          issue_pv(X1{}, j);
-          mma_commit(&kv_empty[(g + j) % NST]);  // K_j, V_j no longer read
-          if (j + 1 <= qb) issue_s(X1{}, j + 1);
         }
         mma_commit(q_empty);
         g += qb + 1;
@@ -917,6 +942,8 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
     constexpr float RESCALE_T = 8.f;
     constexpr int NCH = (BKV / 32) / HV;  // 32-column S chunks per warp
     const uint32_t ts = x ? t_s[1] : t_s[0], to = x ? t_o[1] : t_o[0];
+    const uint32_t tp = x ? t_p[1] : t_p[0];
+    int npv = 0;  // PV MMAs of this tile issued before the current block (SEP)
     float* xch = reinterpret_cast<float*>(sm + L::OFF_X) + x * 2 * BQ;
     auto pair_sync = [&]() {
       if constexpr (HV == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + x * 4 + wq) : "memory");
@@ -966,6 +993,11 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
           mh = fmaxf(mh, xch[(hf ^ 1) * BQ + r]);
           pair_sync();
         }
+        if constexpr (SEP) {  // PV(previous block) complete: O may be rescaled, P rewritten
+          if (npv > 0) mbar_wait(&pv_done[x], (npv - 1) & 1);
+          ++npv;
+          tc_fence_after();
+        }
         const float mx = mh * sl2;
         const bool move = mx > m + RESCALE_T;
         const float m_new = move ? mx : m;
@@ -1004,7 +1036,10 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
               rs4[(i >> 1) & 3] += p0 + p1;
               pk[i >> 1] = pack_bf16(p0, p1);
             }
-            tmem_st_32x32b_x16(ts + lane_off + hf * 64 + cc * 16, pk);
+            if constexpr (SEP)
+              tmem_st_32x32b_x16(tp + lane_off + hf * 32 + cc * 16, pk);
+            else
+              tmem_st_32x32b_x16(ts + lane_off + hf * 64 + cc * 16, pk);
           }
           return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
         };
