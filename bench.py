@@ -181,6 +181,18 @@ def oracle_steps(steps: int, warmup: int, n_seq: int):
     return steps * n_seq * cfg.seq_len / el, el / steps, threads
 
 
+L2_POLICY = "per-step working set (params+grads+activations) >> 126 MB L2; no flush"
+
+
+def workload_config(n: int) -> dict:
+    """The `config` object both arms print (identical dicts, so the driver can
+    compare them); run-specific details go in the line's `details`."""
+    return {"workload": f"gpt2-small-124m (L12 d768 s1024) 1 stage x {n}-rank "
+                        "uneven ZeRO-3 DP, planner shares",
+            "model": "gpt2-small-124m", "global_batch": PER_GPU_BATCH * n, "seq_len": 1024,
+            "parallelism": f"dp{n}", "l2": L2_POLICY}
+
+
 def cpu_baseline_sample():
     """Bounded CPU sample for the GPU arm's cpu_baseline (rank 0, N=1): one warm-up
     and one timed oracle step of the full N=1 workload (8 x 1024 tokens)."""
@@ -210,11 +222,8 @@ def run_reference(args):
         "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": s_per * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (uniform tokens, random init)",
-        "config": {"workload": f"gpt2-small-124m (L12 d768 s1024) 1 stage x {args.gpus}-rank "
-                               "uneven ZeRO-3 DP, planner shares",
-                   "model": "gpt2-small-124m", "global_batch": gb, "seq_len": 1024,
-                   "tokens_per_timed_step": PER_GPU_BATCH * 1024,
-                   "parallelism": f"dp{args.gpus}"},
+        "config": workload_config(args.gpus),
+        "tokens_per_timed_step": PER_GPU_BATCH * 1024,
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -419,15 +428,11 @@ def run_ours(args):
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random init)",
-            "config": {
-                "workload": f"{cfg.name} (L{cfg.n_layer} d{cfg.d_model} s{cfg.seq_len}) 1 stage x "
-                            f"{world}-rank uneven ZeRO-3 DP, planner shares",
-                "model": cfg.name, "global_batch": gb, "seq_len": cfg.seq_len,
-                "parallelism": f"dp{world}", "shares": [plan.groups[0].shares[d]
-                                                         for d in plan.groups[0].device_ids],
+            "config": workload_config(world),
+            "details": {
+                "shares": [plan.groups[0].shares[d] for d in plan.groups[0].device_ids],
                 "n_microbatches": plan.n_microbatches, "ministages": len(plan.groups[0].ministage_sizes),
                 "collectives": "nvlink peer memory" if world > 1 else None,
-                "l2": "per-step working set (params+grads+activations) >> 126 MB L2; no flush",
                 "recompute": ex.recompute,
                 "max_memory_allocated_gib": torch.cuda.max_memory_allocated() / 2**30,
             },
