@@ -720,6 +720,24 @@ static int run(const void* qkv, void* out, void* lse, int n_seq, int S, int H, i
 // tcgen05 MMAs of one thread execute in order, so S_X(j+1) completing also means
 // PV_X(j) consumed P_X(j) and O_X holds P_X(j) V_j (the rescale point).
 // TMEM: S_A | S_B | O_A | O_B = 256 + 2D columns.  K/V blocks are shared by the two tiles.
+#ifdef ZB_EXP_TRACE  // phase cycle totals per role (debug builds only)
+#define TR_DECL long long tr_acc[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tr_t0 = clock64(), tr_start = tr_t0; int tr_n = 0
+#define TR_T0() (tr_t0 = clock64())
+#define TR_ACC(i) do { const long long t_ = clock64(); tr_acc[i] += t_ - tr_t0; tr_t0 = t_; } while (0)
+#define TR_N() (++tr_n)
+#define TR_PRINT(name, xi)                                                                      \
+  if (blockIdx.x == 0 || blockIdx.x == 74 || blockIdx.x == 147)                                 \
+  printf("cta %d %s%d: n %d total %lld ph %lld %lld %lld %lld %lld %lld | %lld %lld | %lld %lld %lld %lld %lld\n", \
+         blockIdx.x, name, (int)(xi), tr_n, clock64() - tr_start, tr_acc[0], tr_acc[1],         \
+         tr_acc[2], tr_acc[3], tr_acc[4], tr_acc[5], tr_acc[6], tr_acc[7], tr_acc[8], tr_acc[9], \
+         tr_acc[10], tr_acc[11], tr_acc[12])
+#else
+#define TR_DECL
+#define TR_T0()
+#define TR_ACC(i)
+#define TR_N()
+#define TR_PRINT(name, xi)
+#endif
 namespace fa_pp {
 constexpr int BQ = 128, BKV = 128;
 // HV = softmax warps per TMEM lane quarter and tile (column halves of S / O)
@@ -729,8 +747,11 @@ template <int D>
 struct Smem {
   static constexpr int NST = (D == 64) ? 4 : 2;
   static constexpr int Q_BYTES = BQ * D * 2, KV_BYTES = BKV * D * 2;
-  static constexpr int OFF_QA = 0, OFF_QB = Q_BYTES;
-  static constexpr int OFF_K = 2 * Q_BYTES;
+  // Q tile pairs: double-buffered at D = 64, so the next item's Q is resident before
+  // the current item's MMAs finish (D = 128: no room)
+  static constexpr int QBUF = (D == 64) ? 2 : 1;
+  __host__ __device__ static constexpr int off_q(int buf, int x) { return (buf * 2 + x) * Q_BYTES; }
+  static constexpr int OFF_K = 2 * QBUF * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NST * KV_BYTES;
   static constexpr int OFF_X = OFF_V + NST * KV_BYTES;  // [2 tiles][2 halves][128] exchange
   static constexpr int OFF_BAR = OFF_X + 2 * 2 * BQ * 4;
@@ -748,11 +769,12 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t* q_full = bar + 0;
-  uint64_t* q_empty = bar + 1;
-  uint64_t* kv_full = bar + 2;            // [NST]
-  uint64_t* kv_empty = bar + 2 + NST;     // [NST]
-  uint64_t* s_full = bar + 2 + 2 * NST;   // [2] per tile
+  constexpr int QBUF = L::QBUF;
+  uint64_t* q_full = bar + 0;             // [QBUF]
+  uint64_t* q_empty = bar + 2;            // [QBUF]
+  uint64_t* kv_full = bar + 4;            // [NST]
+  uint64_t* kv_empty = bar + 4 + NST;     // [NST]
+  uint64_t* s_full = bar + 4 + 2 * NST;   // [2] per tile
   uint64_t* p_full = s_full + 2;          // [2] per tile (count 4)
   uint64_t* o_done = s_full + 4;          // [2] per tile: last PV of the item
   uint64_t* o_empty = s_full + 6;         // [2] per tile: epilogue read O (count 4)
@@ -781,8 +803,10 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_rows128);
     tma_prefetch_desc(&tm_rows64);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int i = 0; i < QBUF; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
     for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
@@ -807,6 +831,7 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
   const uint32_t t_o[2] = {tmem + 256, tmem + 256 + D};
   const uint32_t t_p[2] = {tmem + 384, tmem + 448};   // SEP only
 
+  TR_DECL;
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -815,18 +840,23 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
         int pr, h, b;
         decode(t, pr, h, b);
         const int row0 = b * S, qa = 2 * pr, qb = qa + 1;
-        mbar_wait(q_empty, (lt & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full, 2 * L::Q_BYTES);
+        TR_T0();
+        const int qbuf = lt % QBUF;
+        mbar_wait(&q_empty[qbuf], ((lt / QBUF) & 1) ^ 1);
+        TR_ACC(0);
+        mbar_arrive_expect_tx(&q_full[qbuf], 2 * L::Q_BYTES);
 #pragma unroll
         for (int kc = 0; kc < D / 64; ++kc) {
-          tma_load_2d(sm + L::OFF_QA + kc * BQ * 128, &tm_rows128, q_full, h * D + kc * 64,
-                      row0 + qa * BQ);
-          tma_load_2d(sm + L::OFF_QB + kc * BQ * 128, &tm_rows128, q_full, h * D + kc * 64,
-                      row0 + qb * BQ);
+          tma_load_2d(sm + L::off_q(qbuf, 0) + kc * BQ * 128, &tm_rows128, &q_full[qbuf],
+                      h * D + kc * 64, row0 + qa * BQ);
+          tma_load_2d(sm + L::off_q(qbuf, 1) + kc * BQ * 128, &tm_rows128, &q_full[qbuf],
+                      h * D + kc * 64, row0 + qb * BQ);
         }
         for (int j = 0; j <= qb; ++j, ++g) {
           const int st = g % NST;
+          TR_T0();
           mbar_wait(&kv_empty[st], ((g / NST) & 1) ^ 1);
+          TR_ACC(1);
           mbar_arrive_expect_tx(&kv_full[st], 2 * L::KV_BYTES);
           uint8_t* kd = sm + L::OFF_K + st * L::KV_BYTES;
           uint8_t* vd = sm + L::OFF_V + st * L::KV_BYTES;
@@ -842,44 +872,53 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
                           2 * HD + h * D + dc * 64, kr + kb * 64);
         }
       }
+      TR_PRINT("tma", 0);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(BQ, BKV, 0, 0);
       constexpr uint32_t idesc_o = umma_idesc_bf16(BQ, D, 0, 1);
-      const uint32_t q_base0 = smem_u32(sm + L::OFF_QA), q_base1 = smem_u32(sm + L::OFF_QB);
       const uint32_t ts0 = tmem, ts1 = tmem + 128, to0 = tmem + 256, to1 = tmem + 256 + D;
       const uint32_t tp0 = tmem + 384, tp1 = tmem + 448;
       int g = 0, lt = 0;
       int ns0 = 0, ns1 = 0;  // S blocks issued per tile (parity of p_full waits)
+      bool s0_next = false;  // the next item's S_0(0) was issued early (SEP)
       // (tile index x is a compile-time constant in every call below: no
       // dynamically indexed local arrays on the issue path)
       for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
         int pr, h, b;
         decode(t, pr, h, b);
         const int qa = 2 * pr, qb = qa + 1;
-        mbar_wait(q_full, lt & 1);
-        auto issue_s = [&](auto xc, int j) {  // S_x(j) = Q_x K_j^T
+        const int qbuf = lt % QBUF;
+        mbar_wait(&q_full[qbuf], (lt / QBUF) & 1);
+        // S_x(j) = Q_x K_j^T for the item whose Q sits in buffer qbf and whose K/V blocks
+        // start at ring position gb
+        auto issue_s_at = [&](auto xc, int j, int qbf, int gb) {
           constexpr int x = decltype(xc)::value;
-          const int st = (g + j) % NST;
-          mbar_wait(&kv_full[st], ((g + j) / NST) & 1);
+          const int st = (gb + j) % NST;
+          TR_T0();
+          mbar_wait(&kv_full[st], ((gb + j) / NST) & 1);
+          TR_ACC(0);
           tc_fence_after();
           const uint32_t k_base = smem_u32(sm + L::OFF_K + st * L::KV_BYTES);
-          const uint32_t qb_ = x ? q_base1 : q_base0;
+          const uint32_t qb_ = smem_u32(sm + L::off_q(qbf, x));
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
             mma_bf16_ss(x ? ts1 : ts0, desc_kmajor(qb_, kk, BQ), desc_kmajor(k_base, kk, BKV),
                         idesc_s, kk > 0 ? 1u : 0u);
           mma_commit(&s_full[x]);
         };
+        auto issue_s = [&](auto xc, int j) { issue_s_at(xc, j, qbuf, g); };
         auto issue_pv = [&](auto xc, int j) {  // O_x += P_x(j) V_j, P_x from TMEM
           constexpr int x = decltype(xc)::value;
           const int st = (g + j) % NST;
           int& ns = x ? ns1 : ns0;
           mbar_wait(&p_full[x], ns & 1);
           ++ns;
+          TR_T0();
           if (j == 0) mbar_wait(&o_empty[x], (lt & 1) ^ 1);
+          TR_ACC(2);
           tc_fence_after();
           const uint32_t v_base = smem_u32(sm + L::OFF_V + st * L::KV_BYTES);
           const uint32_t tsx = x ? ts1 : ts0, tox = x ? to1 : to0;
@@ -898,17 +937,30 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
         };
         using X0 = std::integral_constant<int, 0>;
         using X1 = std::integral_constant<int, 1>;
-        issue_s(X0{}, 0);
+        if (!s0_next) issue_s(X0{}, 0);
+        s0_next = false;
         issue_s(X1{}, 0);
         for (int j = 0; j <= qb; ++j) {
           if constexpr (SEP) {
             // S_x(j+1) right after the softmax released S_x(j) (p_full), then PV_x(j)
             if (j <= qa) {
+              TR_T0();
               mbar_wait(&p_full[0], ns0 & 1);
+              TR_ACC(1);
               if (j + 1 <= qa) issue_s(X0{}, j + 1);
               issue_pv(X0{}, j);
             }
+            if (j == qb && QBUF == 2 && item_of(k + 1) < items) {
+              // tile 0 is done with this item: start the next item's S_0(0) now, while
+              // tile 1 finishes its last (diagonal) block
+              const int nbuf = (lt + 1) % QBUF;
+              mbar_wait(&q_full[nbuf], ((lt + 1) / QBUF) & 1);
+              issue_s_at(X0{}, 0, nbuf, g + qb + 1);
+              s0_next = true;
+            }
+            TR_T0();
             mbar_wait(&p_full[1], ns1 & 1);
+            TR_ACC(1);
             if (j + 1 <= qb) issue_s(X1{}, j + 1);
             issue_pv(X1{}, j);
             mma_commit(&kv_empty[(g + j) % NST]);  // K_j, V_j no longer read
@@ -922,9 +974,10 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
             if (j + 1 <= qb) issue_s(X1{}, j + 1);
           }
         }
-        mma_commit(q_empty);
+        mma_commit(&q_empty[qbuf]);
         g += qb + 1;
       }
+      TR_PRINT("mma", 0);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax: per tile, 4*HV warps
@@ -948,62 +1001,106 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
     auto pair_sync = [&]() {
       if constexpr (HV == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + x * 4 + wq) : "memory");
     };
+    // ALT: the exponential passes of tile 0 and tile 1 take turns (named barriers E0 / E1,
+    // both tiles' softmax warps), so one tile's S wait / row max / rescale overlap the
+    // other tile's MUFU-bound pass instead of both tiles contending for the MUFU at once.
+    // Per item tile 0 runs qa+1 passes and tile 1 qa+2: order T0(0) T1(0) ... T0(qa)
+    // T1(qa) T1(qb); T1(qb) hands over to the next item's T0(0).
+    constexpr int kAltE0 = 9, kAltE1 = 10, kAltN = 2 * 4 * HV * 32;
+    auto alt_sync = [&](int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kAltN) : "memory"); };
+    auto alt_arrive = [&](int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kAltN) : "memory"); };
     int nb = 0, lt = 0;  // S blocks consumed by this tile (s_full parity)
     for (int k = 0, t = item_of(0); t < items; t = item_of(++k), ++lt) {
       int pr, h, b;
       decode(t, pr, h, b);
       const int qx = 2 * pr + x;             // this warpgroup's query tile
+      const bool last_item = item_of(k + 1) >= items;
       const int row0 = b * S;
       const int q = qx * BQ + r;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j <= qx; ++j) {
         const bool diag = j == qx;
+        TR_T0();
         mbar_wait(&s_full[x], nb & 1);
         ++nb;
         tc_fence_after();
+        TR_ACC(0);
+        // The warp's S columns are read as 16-column sub-chunks, software-pipelined: the
+        // load of sub-chunk sc+1 is in flight while sub-chunk sc is processed (one
+        // tcgen05.wait::ld per sub-chunk covers it).
+        constexpr int NS16 = 2 * NCH;
+        const uint32_t s_cols = ts + lane_off + hf * NCH * 32;
+        const int col0 = hf * NCH * 32;
+        auto s_pass = [&](auto&& proc) {
+          uint32_t va[16], vb[16];
+          tmem_ld_32x32b_x16(s_cols, va);
+          tmem_ld_wait_regs16(va);
+#pragma unroll
+          for (int sc = 0; sc < NS16; sc += 2) {
+            tmem_ld_32x32b_x16(s_cols + (sc + 1) * 16, vb);
+            proc(va, sc);
+            tmem_ld_wait_regs16(vb);
+            if (sc + 2 < NS16) tmem_ld_32x32b_x16(s_cols + (sc + 2) * 16, va);
+            proc(vb, sc + 1);
+            if (sc + 2 < NS16) tmem_ld_wait_regs16(va);
+          }
+        };
         auto row_max = [&](auto diag_c) {
           constexpr bool DG = decltype(diag_c)::value;
           float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+          s_pass([&](const uint32_t (&v)[16], int sc) {
+            float xs[16];
 #pragma unroll
-          for (int cc = 0; cc < NCH; ++cc) {
-            const int c = hf * NCH + cc;
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(ts + lane_off + c * 32, v);
-            tmem_ld_wait_regs(v);
-            float xs[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < 16; ++i) {
               xs[i] = __uint_as_float(v[i]);
-              if (DG && c * 32 + i > r) xs[i] = -INFINITY;
+              if (DG && col0 + sc * 16 + i > r) xs[i] = -INFINITY;
             }
 #pragma unroll
-            for (int i = 0; i < 32; i += 8) {
+            for (int i = 0; i < 16; i += 8) {
               mx4[0] = fmax3(mx4[0], xs[i], xs[i + 1]);
               mx4[1] = fmax3(mx4[1], xs[i + 2], xs[i + 3]);
               mx4[2] = fmax3(mx4[2], xs[i + 4], xs[i + 5]);
               mx4[3] = fmax3(mx4[3], xs[i + 6], xs[i + 7]);
             }
-          }
+          });
           return fmaxf(fmax3(mx4[0], mx4[1], mx4[2]), mx4[3]);
         };
-        float mh = diag ? row_max(std::true_type{}) : row_max(std::false_type{});
-        if constexpr (HV == 2) {
-          xch[hf * BQ + r] = mh;
-          pair_sync();
-          mh = fmaxf(mh, xch[(hf ^ 1) * BQ + r]);
-          pair_sync();
-        }
-        if constexpr (SEP) {  // PV(previous block) complete: O may be rescaled, P rewritten
-          if (npv > 0) mbar_wait(&pv_done[x], (npv - 1) & 1);
-          ++npv;
-          tc_fence_after();
-        }
-        const float mx = mh * sl2;
-        const bool move = mx > m + RESCALE_T;
-        const float m_new = move ? mx : m;
-        const float corr = move ? exp2_fast(m - m_new) : 1.f;
-        m = m_new;
-        if (j > 0 && __any_sync(0xffffffffu, move)) {  // O holds P(j-1) V_{j-1} (see above)
+        // exponentials with the running max m; P lands in the tile's P columns (SEP) or
+        // inside this warp's own (already read) S columns
+        auto exp_pack = [&](auto diag_c) {
+          constexpr bool DG = decltype(diag_c)::value;
+          float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+          const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+          s_pass([&](const uint32_t (&v)[16], int sc) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+              const float2 e = ffma2(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])),
+                                     sl2x2, nm2);
+              float p0 = exp2_fast(e.x);
+              float p1 = exp2_fast(e.y);
+              if (DG && col0 + sc * 16 + i > r) p0 = 0.f;
+              if (DG && col0 + sc * 16 + i + 1 > r) p1 = 0.f;
+              rs2[(i >> 1) & 1] = fadd2(rs2[(i >> 1) & 1], make_float2(p0, p1));
+              pk[i >> 1] = pack_bf16(p0, p1);
+            }
+            if constexpr (SEP)
+              tmem_st_32x32b_x8(tp + lane_off + hf * 32 + sc * 8, pk);
+            else
+              tmem_st_32x32b_x8(ts + lane_off + hf * 64 + sc * 8, pk);
+          });
+          return (rs2[0].x + rs2[1].x) + (rs2[0].y + rs2[1].y);
+        };
+        auto exchange_max = [&](float mh) {
+          if constexpr (HV == 2) {
+            xch[hf * BQ + r] = mh;
+            pair_sync();
+            mh = fmaxf(mh, xch[(hf ^ 1) * BQ + r]);
+            pair_sync();
+          }
+          return mh;
+        };
+        auto rescale_o = [&](float corr) {  // O holds P(j-1) V_{j-1} (see above)
 #pragma unroll
           for (int c = hf * (D / 32 / HV); c < (hf + 1) * (D / 32 / HV); ++c) {
             uint32_t v[32];
@@ -1013,44 +1110,50 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
             for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
             tmem_st_32x32b_x32(to + lane_off + c * 32, v);
           }
-        }
-        // exponentials; P for S chunk c lands in S columns [pbase + 16(c - first), +16),
-        // inside this warp's own (already read) S columns
-        auto exp_pack = [&](auto diag_c) {
-          constexpr bool DG = decltype(diag_c)::value;
-          float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int cc = 0; cc < NCH; ++cc) {
-            const int c = hf * NCH + cc;
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(ts + lane_off + c * 32, v);
-            tmem_ld_wait_regs(v);
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              float p0 = exp2_fast(fmaf(__uint_as_float(v[i]), sl2, -m));
-              const float x1 = fmaf(__uint_as_float(v[i + 1]), sl2, -m);
-              float p1 = exp2_fast(x1);  // (FMA-pipe exp2_poly offload measured: no gain here)
-              if (DG && c * 32 + i > r) p0 = 0.f;
-              if (DG && c * 32 + i + 1 > r) p1 = 0.f;
-              rs4[(i >> 1) & 3] += p0 + p1;
-              pk[i >> 1] = pack_bf16(p0, p1);
-            }
-            if constexpr (SEP)
-              tmem_st_32x32b_x16(tp + lane_off + hf * 32 + cc * 16, pk);
-            else
-              tmem_st_32x32b_x16(ts + lane_off + hf * 64 + cc * 16, pk);
-          }
-          return (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
         };
+        // exponential passes of the two tiles alternate (see ALT above)
+        auto alt_enter = [&]() {
+          if constexpr (!SEP) return;
+          if (x == 0 && !(k == 0 && j == 0)) alt_sync(kAltE0);
+          if (x == 1 && j < qx) alt_sync(kAltE1);
+        };
+        auto alt_leave = [&]() {
+          if constexpr (!SEP) return;
+          if (x == 0) alt_arrive(kAltE1);
+          if (x == 1 && (j < qx - 1 || (j == qx && !last_item))) alt_arrive(kAltE0);
+        };
+        float mh = diag ? row_max(std::true_type{}) : row_max(std::false_type{});
+        TR_ACC(1);
+        mh = exchange_max(mh);
+        TR_ACC(2);
+        if constexpr (SEP) {  // PV(previous block) complete: O may be rescaled, P rewritten
+          if (npv > 0) mbar_wait(&pv_done[x], (npv - 1) & 1);
+          ++npv;
+          tc_fence_after();
+        }
+        TR_ACC(3);
+        const float mx = mh * sl2;
+        const bool move = mx > m + RESCALE_T;
+        const float m_new = move ? mx : m;
+        const float corr = move ? exp2_fast(m - m_new) : 1.f;
+        m = m_new;
+        if (j > 0 && __any_sync(0xffffffffu, move)) rescale_o(corr);
+        TR_ACC(4);
+        alt_enter();
+        TR_ACC(6);
         const float rs = diag ? exp_pack(std::true_type{}) : exp_pack(std::false_type{});
+        alt_leave();
         l = l * corr + rs;
+        TR_ACC(5);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[x]);
+        TR_ACC(7);
+        TR_N();
       }
       // epilogue
+      TR_T0();
       float lt_sum = l;
       if constexpr (HV == 2) {
         xch[hf * BQ + r] = l;
@@ -1058,30 +1161,41 @@ __global__ void __launch_bounds__(threads_for<HV>(), 1)
         lt_sum = l + xch[(hf ^ 1) * BQ + r];
         pair_sync();
       }
+      TR_ACC(8);
       mbar_wait(&o_done[x], lt & 1);
       tc_fence_after();
+      TR_ACC(9);
       const float inv = 1.f / lt_sum;
       __nv_bfloat16* orow = out + ((size_t)row0 + q) * HD + h * D;
+      const bool st256 = ((reinterpret_cast<uintptr_t>(out) | (HD * 2)) & 31) == 0;
 #pragma unroll
       for (int c = hf * (D / 32 / HV); c < (hf + 1) * (D / 32 / HV); ++c) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(to + lane_off + c * 32, v);
         tmem_ld_wait_regs(v);
+        TR_ACC(11);
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 pk;
-          pk.x = pack_bf16(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
-          pk.y = pack_bf16(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
-          pk.z = pack_bf16(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
-          pk.w = pack_bf16(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
-          *reinterpret_cast<uint4*>(orow + c * 32 + i) = pk;
+        for (int i = 0; i < 32; i += 16) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            pk[e] = pack_bf16(__uint_as_float(v[i + 2 * e]) * inv, __uint_as_float(v[i + 2 * e + 1]) * inv);
+          if (st256) {
+            st_global_256(orow + c * 32 + i, pk);
+          } else {
+            *reinterpret_cast<uint4*>(orow + c * 32 + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(orow + c * 32 + i + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
         }
       }
+      TR_ACC(12);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[x]);
-      if (hf == 0) lse[((size_t)b * H + h) * S + q] = (m + __log2f(lt_sum)) / LOG2E;
+      if (hf == 0) lse[((size_t)b * H + h) * S + q] = (m + __log2f(lt_sum)) * (1.f / LOG2E);
+      TR_ACC(10);
     }
+    if (r == 0 && hf == 0) TR_PRINT("softmax", x);
   }
 
   tc_fence_before();
