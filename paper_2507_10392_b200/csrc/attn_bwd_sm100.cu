@@ -16,6 +16,7 @@
 // rows of TMEM lane quarter (w-4)%4 and column half (w-4)/4 (no cross-column state
 // in the backward, so the per-row work splits freely).
 #include "common.cuh"
+#include "trace.cuh"
 #include "zb_internal.h"
 
 #include <type_traits>
@@ -47,6 +48,21 @@ ZB_DEVICE void st_row32(uint8_t* tile, int r, int c0, const float* v) {
     pk.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
     pk.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
     pk.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+    *reinterpret_cast<uint4*>(tile + (ch >> 3) * (T * 128) + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) = pk;
+  }
+}
+
+// 16 fp32 values of row r, columns [c0, c0+16) (c0 % 16 == 0) -> bf16 into the same
+// SWIZZLE_128B tile layout as st_row32.
+ZB_DEVICE void st_row16(uint8_t* tile, int r, int c0, const float2 (&v)[8]) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int ch = (c0 >> 3) + q;
+    uint4 pk;
+    pk.x = pack_bf16(v[q * 4 + 0].x, v[q * 4 + 0].y);
+    pk.y = pack_bf16(v[q * 4 + 1].x, v[q * 4 + 1].y);
+    pk.z = pack_bf16(v[q * 4 + 2].x, v[q * 4 + 2].y);
+    pk.w = pack_bf16(v[q * 4 + 3].x, v[q * 4 + 3].y);
     *reinterpret_cast<uint4*>(tile + (ch >> 3) * (T * 128) + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) = pk;
   }
 }
@@ -638,6 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t t_dqp = tmem + 256 + 2 * D;
   griddep_wait();
   griddep_launch();
+  TR_DECL;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -678,7 +695,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int g = 0, lt = 0;
       auto issue_s = [&](int gi) {  // S^T(gi) = K Q^T, dP^T(gi) = V dO^T
         const int st = gi % NST;
+        TR_T0();
         mbar_wait(&qo_full[st], (gi / NST) & 1);
+        TR_ACC(3);
         tc_fence_after();
         const uint32_t q_base = smem_u32(sm + L::OFF_Q + st * L::TILE);
         const uint32_t do_base = smem_u32(sm + L::OFF_DO + st * L::TILE);
@@ -698,8 +717,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue_s(g);   // the previous item's last dV (reader of P^T in t_st) was issued before
         for (int i = 0; i < ntile; ++i) {
           const int gi = g + i, st = gi % NST, bb = gi & 1;
+          TR_T0();
           mbar_wait(p_full, gi & 1);
+          TR_ACC(0);
           if (i == 0) mbar_wait(acc_empty, (lt & 1) ^ 1);  // previous item's dK / dV read
+          TR_ACC(1);
           tc_fence_after();
           const uint32_t q_base = smem_u32(sm + L::OFF_Q + st * L::TILE);
           const uint32_t do_base = smem_u32(sm + L::OFF_DO + st * L::TILE);
@@ -714,7 +736,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < T / 16; ++kk)
             mma_bf16_ss(t_dk, desc_k(dst_base, kk), desc_mn(q_base, kk), idesc_o, (i > 0 || kk > 0));
+          TR_T0();
           mbar_wait(&dqp_empty[bb], ((gi >> 1) & 1) ^ 1);
+          TR_ACC(2);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < T / 16; ++kk)
@@ -728,6 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(done);
         g += ntile;
       }
+      TR_PRINT("mma", 0);
     }
   } else if (warp >= 4) {
     const int wq = (warp - 4) & 3, half = (warp - 4) >> 2, r = wq * 32 + lane;
@@ -741,8 +766,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto drain_dq = [&](int j) {  // j: tile index within the item
         uint8_t* stg = sm + L::OFF_STG + (warp - 4) * 4096;
         const int gj = g + j, bb = gj & 1;
+        TR_T0();
         mbar_wait(&dqp_full[bb], (gj >> 1) & 1);
         tc_fence_after();
+        TR_ACC(6);
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_dqp + bb * D + lo + half * 32, v);
         tmem_ld_wait_regs(v);
@@ -753,6 +780,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_wait_read<0>();
         }
         __syncwarp();
+        TR_ACC(7);
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
@@ -784,63 +812,97 @@ __global__ void __launch_bounds__(kThreads, 1)
             nd = delta[vrow0 + (size_t)(i + 1) * T];
           }
         }
+        TR_T0();
         asm volatile("bar.sync 1, 256;" ::: "memory");  // the eight math warps
+        TR_ACC(0);
         mbar_wait(s_full, gi & 1);
+        TR_ACC(1);
         mbar_wait(&dst_empty[bb], ((gi >> 1) & 1) ^ 1);  // dK / dQ of tile gi-2 read it
         tc_fence_after();
+        TR_ACC(2);
         uint8_t* dst = sm + L::OFF_DST + bb * T * T * 2;
-        auto chunk = [&](int c, auto diag_c) {
+        // The half's 64 S^T / dP^T columns as four 16-column sub-chunks, software-pipelined
+        // (the loads of sub-chunk sc+1 are in flight while sc is processed); fp32 pairs
+        // go through FFMA2 / FADD2 / FMUL2.
+        const uint32_t s_cols = t_st + lo + half * 64, d_cols = t_dpt + lo + half * 64;
+        auto sub = [&](auto diag_c, const uint32_t (&sv)[16], const uint32_t (&dv)[16], int sc) {
           constexpr bool DG = decltype(diag_c)::value;
-          uint32_t sv[32], dv[32];
-          tmem_ld_32x32b_x32(t_st + lo + c * 32, sv);
-          tmem_ld_32x32b_x32(t_dpt + lo + c * 32, dv);
-          tmem_ld_wait_regs(sv);
-          reg_tie(dv);
-          float ds[32];
-          uint32_t pk[16];
+          const int c0 = half * 64 + sc * 16;  // query column of element 0
+          float2 ds[8];
+          uint32_t pk[8];
 #pragma unroll
-          for (int t4 = 0; t4 < 32; t4 += 4) {
-            const float4 l4 = *reinterpret_cast<const float4*>(vl + c * 32 + t4);
-            const float4 d4 = *reinterpret_cast<const float4*>(vd + c * 32 + t4);
-            const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
-            float p4[4];
+          for (int t4 = 0; t4 < 16; t4 += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(vl + c0 + t4);
+            const float4 d4 = *reinterpret_cast<const float4*>(vd + c0 + t4);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 4; u += 2) {
               const int tt = t4 + u;
-              float x = exp2_fast(fmaf(__uint_as_float(sv[tt]), sl2, -lv[u]));
-              if (DG && c * 32 + tt < r) x = 0.f;
-              p4[u] = x;
-              ds[tt] = x * (__uint_as_float(dv[tt]) - dl[u]);
+              const float2 e = ffma2(make_float2(__uint_as_float(sv[tt]), __uint_as_float(sv[tt + 1])),
+                                     make_float2(sl2, sl2),
+                                     make_float2(-(u ? l4.z : l4.x), -(u ? l4.w : l4.y)));
+              float p0 = exp2_fast(e.x), p1 = exp2_fast(e.y);
+              if (DG && c0 + tt < r) p0 = 0.f;
+              if (DG && c0 + tt + 1 < r) p1 = 0.f;
+              const float2 dd = fadd2(make_float2(__uint_as_float(dv[tt]), __uint_as_float(dv[tt + 1])),
+                                      make_float2(-(u ? d4.z : d4.x), -(u ? d4.w : d4.y)));
+              ds[tt >> 1] = fmul2(make_float2(p0, p1), dd);
+              pk[tt >> 1] = pack_bf16(p0, p1);
             }
-            pk[t4 / 2] = pack_bf16(p4[0], p4[1]);
-            pk[t4 / 2 + 1] = pack_bf16(p4[2], p4[3]);
           }
-          // P^T columns [c*32, c*32+32) -> packed TMEM columns inside this half's own
-          // (already read) S^T columns
-          tmem_st_32x32b_x16(t_st + lo + half * 64 + (c - half * (T / 64)) * 16, pk);
-          st_row32(dst, r, c * 32, ds);
+          // P^T -> packed TMEM columns inside this half's own (already read) S^T columns
+          tmem_st_32x32b_x8(s_cols + sc * 8, pk);
+          st_row16(dst, r, c0, ds);
         };
-        constexpr int CH = T / 64;
-        if (qt == kt) {
-#pragma unroll 1
-          for (int c = half * CH; c < (half + 1) * CH; ++c) chunk(c, std::true_type{});
-        } else {
-#pragma unroll 1
-          for (int c = half * CH; c < (half + 1) * CH; ++c) chunk(c, std::false_type{});
-        }
+        auto pass = [&](auto diag_c) {
+          uint32_t sa[16], da[16], sb[16], db[16];
+          tmem_ld_32x32b_x16(s_cols, sa);
+          tmem_ld_32x32b_x16(d_cols, da);
+          tmem_ld_wait_regs16(sa);
+          reg_tie16(da);
+#pragma unroll
+          for (int sc = 0; sc < 4; sc += 2) {
+            tmem_ld_32x32b_x16(s_cols + (sc + 1) * 16, sb);
+            tmem_ld_32x32b_x16(d_cols + (sc + 1) * 16, db);
+            sub(diag_c, sa, da, sc);
+            tmem_ld_wait_regs16(sb);
+            reg_tie16(db);
+            if (sc + 2 < 4) {
+              tmem_ld_32x32b_x16(s_cols + (sc + 2) * 16, sa);
+              tmem_ld_32x32b_x16(d_cols + (sc + 2) * 16, da);
+            }
+            sub(diag_c, sb, db, sc + 1);
+            if (sc + 2 < 4) {
+              tmem_ld_wait_regs16(sa);
+              reg_tie16(da);
+            }
+          }
+        };
+        if (qt == kt)
+          pass(std::true_type{});
+        else
+          pass(std::false_type{});
+        TR_ACC(3);
         tmem_st_wait();
         tc_fence_before();
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
+        TR_ACC(4);
         if (i > 0) drain_dq(i - 1);
+        TR_ACC(5);
+        TR_N();
       }
+      TR_T0();
       drain_dq(ntile - 1);
+      TR_ACC(8);
       mbar_wait(done, lt & 1);
       tc_fence_after();
+      TR_ACC(9);
       const int kr = kt * T + r;
       __nv_bfloat16* dk_row = dqkv + ((size_t)row0 + kr) * ld + HD + h * D;
       __nv_bfloat16* dv_row = dk_row + HD;
+      // 32-byte stores when every row segment is 32-byte aligned
+      const bool st256 = ((reinterpret_cast<uintptr_t>(dqkv) | (ld * 2) | (HD * 2)) & 31) == 0;
 #pragma unroll
       for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
         uint32_t v[32], w[32];
@@ -849,26 +911,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait_regs(v);
         reg_tie(w);
 #pragma unroll
-        for (int tt = 0; tt < 32; tt += 8) {
-          uint4 a, bq;
-          a.x = pack_bf16(__uint_as_float(v[tt]) * scale, __uint_as_float(v[tt + 1]) * scale);
-          a.y = pack_bf16(__uint_as_float(v[tt + 2]) * scale, __uint_as_float(v[tt + 3]) * scale);
-          a.z = pack_bf16(__uint_as_float(v[tt + 4]) * scale, __uint_as_float(v[tt + 5]) * scale);
-          a.w = pack_bf16(__uint_as_float(v[tt + 6]) * scale, __uint_as_float(v[tt + 7]) * scale);
-          bq.x = pack_bf16(__uint_as_float(w[tt]), __uint_as_float(w[tt + 1]));
-          bq.y = pack_bf16(__uint_as_float(w[tt + 2]), __uint_as_float(w[tt + 3]));
-          bq.z = pack_bf16(__uint_as_float(w[tt + 4]), __uint_as_float(w[tt + 5]));
-          bq.w = pack_bf16(__uint_as_float(w[tt + 6]), __uint_as_float(w[tt + 7]));
-          *reinterpret_cast<uint4*>(dk_row + c * 32 + tt) = a;
-          *reinterpret_cast<uint4*>(dv_row + c * 32 + tt) = bq;
+        for (int tt = 0; tt < 32; tt += 16) {
+          uint32_t a[8], bq[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            a[e] = pack_bf16(__uint_as_float(v[tt + 2 * e]) * scale,
+                             __uint_as_float(v[tt + 2 * e + 1]) * scale);
+            bq[e] = pack_bf16(__uint_as_float(w[tt + 2 * e]), __uint_as_float(w[tt + 2 * e + 1]));
+          }
+          if (st256) {
+            st_global_256(dk_row + c * 32 + tt, a);
+            st_global_256(dv_row + c * 32 + tt, bq);
+          } else {
+            *reinterpret_cast<uint4*>(dk_row + c * 32 + tt) = make_uint4(a[0], a[1], a[2], a[3]);
+            *reinterpret_cast<uint4*>(dk_row + c * 32 + tt + 8) = make_uint4(a[4], a[5], a[6], a[7]);
+            *reinterpret_cast<uint4*>(dv_row + c * 32 + tt) = make_uint4(bq[0], bq[1], bq[2], bq[3]);
+            *reinterpret_cast<uint4*>(dv_row + c * 32 + tt + 8) = make_uint4(bq[4], bq[5], bq[6], bq[7]);
+          }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty);
+      TR_ACC(10);
       g += ntile;
     }
     if (lane == 0) bulk_wait_all();
+    if (r == 0 && half == 0) TR_PRINT("math", wq);
   }
   tc_fence_before();
   __syncthreads();

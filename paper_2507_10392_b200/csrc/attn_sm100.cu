@@ -15,6 +15,7 @@
 //
 // Layout as in attn.cu: qkv rows [q|k|v] (pitch ld), sequence b = rows [b*S, (b+1)*S).
 #include "common.cuh"
+#include "trace.cuh"
 #include "zb_internal.h"
 
 #include <cstdlib>
@@ -720,24 +721,6 @@ static int run(const void* qkv, void* out, void* lse, int n_seq, int S, int H, i
 // tcgen05 MMAs of one thread execute in order, so S_X(j+1) completing also means
 // PV_X(j) consumed P_X(j) and O_X holds P_X(j) V_j (the rescale point).
 // TMEM: S_A | S_B | O_A | O_B = 256 + 2D columns.  K/V blocks are shared by the two tiles.
-#ifdef ZB_EXP_TRACE  // phase cycle totals per role (debug builds only)
-#define TR_DECL long long tr_acc[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tr_t0 = clock64(), tr_start = tr_t0; int tr_n = 0
-#define TR_T0() (tr_t0 = clock64())
-#define TR_ACC(i) do { const long long t_ = clock64(); tr_acc[i] += t_ - tr_t0; tr_t0 = t_; } while (0)
-#define TR_N() (++tr_n)
-#define TR_PRINT(name, xi)                                                                      \
-  if (blockIdx.x == 0 || blockIdx.x == 74 || blockIdx.x == 147)                                 \
-  printf("cta %d %s%d: n %d total %lld ph %lld %lld %lld %lld %lld %lld | %lld %lld | %lld %lld %lld %lld %lld\n", \
-         blockIdx.x, name, (int)(xi), tr_n, clock64() - tr_start, tr_acc[0], tr_acc[1],         \
-         tr_acc[2], tr_acc[3], tr_acc[4], tr_acc[5], tr_acc[6], tr_acc[7], tr_acc[8], tr_acc[9], \
-         tr_acc[10], tr_acc[11], tr_acc[12])
-#else
-#define TR_DECL
-#define TR_T0()
-#define TR_ACC(i)
-#define TR_N()
-#define TR_PRINT(name, xi)
-#endif
 namespace fa_pp {
 constexpr int BQ = 128, BKV = 128;
 // HV = softmax warps per TMEM lane quarter and tile (column halves of S / O)

@@ -13,7 +13,16 @@ torch.manual_seed(0)
 qkv = torch.randn(T, 3 * H * D, device="cuda").bfloat16()
 out = torch.empty(T, H * D, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(n, H, S, device="cuda")
+dout = torch.randn(T, H * D, device="cuda").bfloat16()
+dqkv = torch.empty_like(qkv)
+delta = torch.empty(n, H, S, device="cuda")
+dq = torch.empty(T, H * D, device="cuda") if D == 64 else None
+bwd = os.environ.get("TRACE_BWD") == "1"
 for i in range(2):
     print(f"=== launch {i}", flush=True)
     K.attn_fwd(qkv, out, lse, n, S, H, D, 1 / math.sqrt(D))
     torch.cuda.synchronize()
+    if bwd:
+        print(f"=== bwd launch {i}", flush=True)
+        K.attn_bwd(qkv, out, dout, lse, dqkv, dq, delta, n, S, H, D, 1 / math.sqrt(D))
+        torch.cuda.synchronize()
