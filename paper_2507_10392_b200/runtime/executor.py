@@ -476,6 +476,7 @@ class StageExecutor:
         self.tokens = torch.zeros(self.M, n, device=device, dtype=torch.int32)
         self.labels = torch.zeros(self.M, n, device=device, dtype=torch.int32)
         self.loss_sum = torch.zeros(1, device=device, dtype=torch.float32)
+        self._head_fresh = False   # the head's gradient slot awaits its first accumulation
         self.step_dev = torch.zeros(1, device=device, dtype=torch.int32)  # Adam t on the device
         self.gsumsq = torch.zeros(1, device=device, dtype=torch.float32)
 
@@ -624,6 +625,12 @@ class StageExecutor:
         region = self.arena.view(base, self.grad_slot_bytes // 4, torch.float32)
         last = units[-1]
         used = self._grad_unit_off[last] // 4 + self.units[last].numel
+        if last == "head" and self.n_tok > 0:
+            # head_w (the head unit's last entry) is written by the LM-head wgrad GEMM with
+            # beta = 0 on the slot's first accumulation (_on_fwd): no clearing needed
+            hw_off = dict((n, o) for n, o, _ in self.units[last].layout.entries)["head_w"]
+            used = self._grad_unit_off[last] // 4 + hw_off
+            self._head_fresh = True
         prev, same_step = self.win.grad_prev[s]
         ps = self.prep_stream if self.multistream else None
         if prev is not None and same_step:
@@ -741,7 +748,9 @@ class StageExecutor:
             self.model.head_fwd_bwd(hu.p, hu.g, self.act[(hi, m)][:n], self.labels[m],
                                     self.gbuf[(hi, m)][:n], self.logits, self.hf, self.hf_mean,
                                     self.hf_rstd, self.dhf, self.loss_sum,
-                                    1.0 / self.global_tokens, n, dhf32=self.dhf32)
+                                    1.0 / self.global_tokens, n, dhf32=self.dhf32,
+                                    first=self._head_fresh)
+            self._head_fresh = False
 
     def _on_bwd(self, ev: Event) -> None:
         """Recompute + backward, layer by layer in reverse (each layer's internals are

@@ -275,7 +275,9 @@ class GptOps:
     def layer_bwd(self, p: Dict[str, torch.Tensor], gr: Dict[str, torch.Tensor], x: torch.Tensor,
                   dy: torch.Tensor, dx: torch.Tensor, a: LayerActs, s: BwdScratch,
                   n_tok: int) -> None:
-        """dx = d(block)/dx . dy ; parameter grads accumulate into ``gr`` (fp32)."""
+        """dx = d(block)/dx . dy ; parameter grads accumulate into ``gr`` (fp32).
+        (The weight-gradient GEMMs always accumulate: their tiles split K and reduce-add
+        into the slot, which therefore has to start at zero.)"""
         o, cfg = self.ops, self.cfg
         n_seq = n_tok // cfg.seq_len
         n = n_tok
@@ -317,7 +319,7 @@ class GptOps:
         self.ops.embedding_bwd(tokens[:n_tok], dx, gr["wte"], gr["wpe"], self.cfg.seq_len)
 
     def head_fwd_bwd(self, p, gr, x, labels, dx, logits, hf, mean, rstd, dhf, loss_sum, scale,
-                     n_tok, dhf32=None):
+                     n_tok, dhf32=None, first=False):
         """Final LayerNorm + LM head + cross-entropy, and straight away its
         backward: dx (grad of the last block's output) and head grads."""
         o = self.ops
@@ -325,8 +327,11 @@ class GptOps:
         o.layernorm_fwd(x, p["lnf_w"], p["lnf_b"], hf[:n], mean[:n], rstd[:n])
         o.gemm(hf[:n], p["head_w"], logits[:n])
         o.xent_fwd_bwd(logits[:n], labels[:n], loss_sum, logits[:n], scale)
-        # (LM-head wgrad inline: forking it measured neutral; both GEMMs fill the GPU)
-        o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        # (LM-head wgrad inline: forking it measured neutral; both GEMMs fill the GPU).
+        # first: the first accumulation into a freshly bound gradient slot overwrites
+        # (beta = 0; its tiles do not split K), so the slot's head_w span is not cleared.
+        o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32,
+               beta=0.0 if first else 1.0)
         head_dgrad(o, logits[:n], p["head_w"], dhf[:n], None if dhf32 is None else dhf32[:n])
         o.layernorm_bwd(dhf[:n], x, p["lnf_w"], mean[:n], rstd[:n], dx, gr["lnf_w"], gr["lnf_b"])
 
@@ -397,14 +402,17 @@ class LlamaOps:
         self.ops.embedding_bwd(tokens[:n_tok], dx, gr["wte"], None, self.cfg.seq_len)
 
     def head_fwd_bwd(self, p, gr, x, labels, dx, logits, hf, mean, rstd, dhf, loss_sum, scale,
-                     n_tok, dhf32=None):
+                     n_tok, dhf32=None, first=False):
         o = self.ops
         n = n_tok
         o.rmsnorm_fwd(x, p["norm_w"], hf[:n], rstd[:n])
         o.gemm(hf[:n], p["head_w"], logits[:n])
         o.xent_fwd_bwd(logits[:n], labels[:n], loss_sum, logits[:n], scale)
-        # (LM-head wgrad inline: forking it measured neutral; both GEMMs fill the GPU)
-        o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32, beta=1.0)
+        # (LM-head wgrad inline: forking it measured neutral; both GEMMs fill the GPU).
+        # first: the first accumulation into a freshly bound gradient slot overwrites
+        # (beta = 0; its tiles do not split K), so the slot's head_w span is not cleared.
+        o.gemm(logits[:n], hf[:n], gr["head_w"], a_t=True, b_t=True, epilogue=EPI_F32,
+               beta=0.0 if first else 1.0)
         head_dgrad(o, logits[:n], p["head_w"], dhf[:n], None if dhf32 is None else dhf32[:n])
         o.rmsnorm_bwd(dhf[:n], x, p["norm_w"], rstd[:n], dx, gr["norm_w"])
 
