@@ -149,6 +149,21 @@ int zb_adamw_shard_dstep(void* master, void* exp_avg, void* exp_avg_sq, const vo
                          void* param_bf16, void* sumsq, int64_t n, float lr, float beta1,
                          float beta2, float eps, float weight_decay, float grad_scale,
                          const void* step_dev, zb_stream_t stream);
+/* Row-split update of a [rows, d] embedding table whose gradient is nonzero only in the
+ * rows of this step's tokens.  zb_embed_mark: mark[tok] = *stamp_dev (the device step
+ * counter) for every token.  zb_embed_zero_rows: grad rows of the tokens <- 0.
+ * zb_adamw_rows_dstep: AdamW over the rows with (mark[r] == *step_dev) == marked; marked = 0
+ * updates with g = 0 and reads no gradient (grad may be NULL).  Per element identical to
+ * zb_adamw_shard_dstep with a zero gradient in the unmarked rows. */
+int zb_embed_mark(const void* tokens, int64_t n, int rows, void* mark, const void* stamp_dev,
+                  zb_stream_t stream);
+int zb_embed_zero_rows(const void* tokens, int64_t n, int rows, void* grad, int d,
+                       zb_stream_t stream);
+int zb_adamw_rows_dstep(void* master, void* exp_avg, void* exp_avg_sq, const void* grad,
+                        void* param_bf16, void* sumsq, int rows, int d, const void* mark,
+                        int marked, float lr, float beta1, float beta2, float eps,
+                        float weight_decay, float grad_scale, const void* step_dev,
+                        zb_stream_t stream);
 int zb_step_increment(void* step_dev, zb_stream_t stream);
 
 /* ---------------------------------------------------------------- collectives

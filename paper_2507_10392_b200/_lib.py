@@ -36,6 +36,9 @@ SIGNATURES = {
     "zb_attn_bwd": [P, P, P, P, P, P, P, I, I, I, I, I, F, P],
     "zb_adamw_shard": [P, P, P, P, P, P, I64, F, F, F, F, F, F, I, P],
     "zb_adamw_shard_dstep": [P, P, P, P, P, P, I64, F, F, F, F, F, F, P, P],
+    "zb_embed_mark": [P, I64, I, P, P, P],
+    "zb_embed_zero_rows": [P, I64, I, P, I, P],
+    "zb_adamw_rows_dstep": [P, P, P, P, P, P, I, I, P, I, F, F, F, F, F, F, P, P],
     "zb_step_increment": [P, P],
     "zb_rmsnorm_fwd": [P, P, P, P, I, I, F, P],
     "zb_rmsnorm_bwd": [P, P, P, P, P, P, P, I, I, P],

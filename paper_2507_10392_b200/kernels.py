@@ -214,6 +214,32 @@ def adamw_shard(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, lr, beta1,
          float(weight_decay), float(grad_scale), int(step), _stream())
 
 
+def embed_mark(tokens, rows, mark, step_dev):
+    """mark[tok] = step (device counter) for every token (row-split embedding update)."""
+    _need_cuda(tokens, mark, step_dev)
+    call("zb_embed_mark", _ptr(tokens), tokens.numel(), int(rows), _ptr(mark), _ptr(step_dev),
+         _stream())
+
+
+def embed_zero_rows(tokens, grad_table):
+    """grad_table[tok, :] = 0 for every token; grad_table: fp32 [rows, d]."""
+    _need_cuda(tokens, grad_table)
+    rows, d = grad_table.shape
+    call("zb_embed_zero_rows", _ptr(tokens), tokens.numel(), rows, _ptr(grad_table), d, _stream())
+
+
+def adamw_rows(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, mark, marked, lr, beta1,
+               beta2, eps, weight_decay, grad_scale, step_dev):
+    """AdamW over the rows r of [rows, d] tables with (mark[r] == step) == marked;
+    marked=False: g = 0, ``grad`` unused (may be None)."""
+    _need_cuda(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, mark, step_dev)
+    rows, d = master.shape
+    call("zb_adamw_rows_dstep", _ptr(master), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(grad),
+         _ptr(param_bf16), _ptr(sumsq), rows, d, _ptr(mark), int(bool(marked)), float(lr),
+         float(beta1), float(beta2), float(eps), float(weight_decay), float(grad_scale),
+         _ptr(step_dev), _stream())
+
+
 def cast_f32_bf16(src, dst):
     _need_cuda(src, dst)
     call("zb_cast_f32_bf16", _ptr(src), _ptr(dst), src.numel(), _stream())

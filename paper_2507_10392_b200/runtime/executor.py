@@ -301,6 +301,7 @@ class StageExecutor:
                                  "host": torch.cuda.Stream(device=device)}
             self.gather_stream = torch.cuda.Stream(device=device)
             self.prep_stream = torch.cuda.Stream(device=device)   # gradient-slot handover
+            self.opt_stream = torch.cuda.Stream(device=device)    # early embedding update
         self.record_timeline = False  # measured Gantt (see measured_timeline)
         self._marks = []
         self.capture_grads = False   # tests: keep each reduced grad shard before Adam
@@ -479,6 +480,13 @@ class StageExecutor:
         self._head_fresh = False   # the head's gradient slot awaits its first accumulation
         self.step_dev = torch.zeros(1, device=device, dtype=torch.int32)  # Adam t on the device
         self.gsumsq = torch.zeros(1, device=device, dtype=torch.float32)
+        # Row-split token-embedding update (single-rank group owning the embedding): the
+        # table's gradient is nonzero only in the rows of this step's tokens, so only those
+        # rows are cleared before the embedding backward and updated after it; the other
+        # rows get their (zero-gradient) AdamW step early, off the critical path.
+        self.sparse_embed = self.has_embed and self.g_size == 1 and self.n_tok > 0
+        if self.sparse_embed:
+            self.embed_mark = torch.zeros(cfg.vocab, device=device, dtype=torch.int32)
 
         # ---------------- sample ranges and boundary transfer lists ----------
         self._sample_ranges = sample_ranges(plan)
@@ -541,11 +549,28 @@ class StageExecutor:
         self.ops.fill_f32(self.loss_sum, 0.0)
         self.ops.fill_f32(self.gsumsq, 0.0)
         self._done = {}
+        if self.sparse_embed:
+            self.ops.embed_mark(self.tokens, self.cfg.vocab, self.embed_mark, self.step_dev)
         if not self.multistream:
+            if self.sparse_embed:
+                self._embed_update(marked=False)
             for ev in self.events:
                 _DISPATCH[ev.kind](self, ev)
             return
         self._step_multistream()
+
+    def _wte(self, t: torch.Tensor) -> torch.Tensor:
+        """The token-embedding table's [V, d] view of an embed-unit flat buffer."""
+        return t[:self.cfg.vocab * self.cfg.d_model].view(self.cfg.vocab, self.cfg.d_model)
+
+    def _embed_update(self, marked: bool) -> None:
+        """AdamW over the token-embedding rows this step's tokens touched (marked, after
+        the backward) or did not touch (g = 0; any time in the step)."""
+        pu, a = self.units["embed"], self.adam
+        self.ops.adamw_rows(self._wte(pu.master), self._wte(pu.exp_avg), self._wte(pu.exp_avg_sq),
+                            self._wte(pu.grad) if marked else None, self._wte(pu.shard),
+                            self.gsumsq, self.embed_mark, marked, a.lr, a.beta1, a.beta2,
+                            a.eps, a.weight_decay, 1.0, self.step_dev)
 
     def _step_multistream(self) -> None:
         main = torch.cuda.current_stream(self.device)
@@ -554,8 +579,12 @@ class StageExecutor:
         start.record(main)
         self._marks = [("start", start)] if timed else []
         streams = {"compute": main, **self.lane_streams}
-        for st in list(self.lane_streams.values()) + [self.gather_stream, self.prep_stream]:
+        for st in list(self.lane_streams.values()) + [self.gather_stream, self.prep_stream,
+                                                      self.opt_stream]:
             st.wait_event(start)                     # fork (also joins a graph capture)
+        if self.sparse_embed:
+            with torch.cuda.stream(self.opt_stream):
+                self._embed_update(marked=False)
         done = self._done                            # task key -> [(stream, event)]
         last = {}
         noop = ("P2PRecv", "Recompute", "OptimStep", "FreeParams")
@@ -585,7 +614,7 @@ class StageExecutor:
                 self._marks.append((ev, b0, e))
             done[ev.key] = [(st, e)]
             last[lane] = e
-        for st in (self.gather_stream, self.prep_stream):
+        for st in (self.gather_stream, self.prep_stream, self.opt_stream):
             j = torch.cuda.Event()
             j.record(st)
             main.wait_event(j)
@@ -641,7 +670,16 @@ class StageExecutor:
                 for u in self.chunks[prev]:
                     self.group_comm.wait_consumed(self.units[u], 0 if same_step else -1,
                                                   self.step_dev)
-            self.ops.fill_f32(region[:used], 0.0)
+            if self.sparse_embed and "embed" in units and not self.capture_grads:
+                # only the rows of this step's tokens of the token-embedding gradient
+                lo_e = self._grad_unit_off["embed"] // 4
+                hi_e = lo_e + self.cfg.vocab * self.cfg.d_model
+                self.ops.fill_f32(region[:lo_e], 0.0)
+                self.ops.fill_f32(region[hi_e:used], 0.0)
+                self.ops.embed_zero_rows(self.tokens, region[lo_e:hi_e].view(self.cfg.vocab,
+                                                                              self.cfg.d_model))
+            else:
+                self.ops.fill_f32(region[:used], 0.0)
         if ps is not None:
             e = torch.cuda.Event()
             e.record(ps)
@@ -707,6 +745,15 @@ class StageExecutor:
             if self.group_comm is not None:
                 self.group_comm.reduce_scatter_adamw(pu, a, self.gsumsq, self.step_dev,
                                                      write_grad=self.capture_grads)
+            elif u == "embed" and self.sparse_embed:
+                # token rows of this step (the others were updated early in the step),
+                # then the rest of the unit (position embeddings) densely
+                self._embed_update(marked=True)
+                k = self.cfg.vocab * self.cfg.d_model
+                if pu.numel > k:
+                    self.ops.adamw_shard(pu.master[k:], pu.exp_avg[k:], pu.exp_avg_sq[k:],
+                                         pu.grad[k:], pu.shard[k:], self.gsumsq, a.lr, a.beta1,
+                                         a.beta2, a.eps, a.weight_decay, 1.0, self.step_dev)
             else:
                 self.ops.adamw_shard(pu.master, pu.exp_avg, pu.exp_avg_sq, pu.grad, pu.shard,
                                      self.gsumsq, a.lr, a.beta1, a.beta2, a.eps,

@@ -151,6 +151,31 @@ def adamw_shard(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, lr, beta1,
     param_bf16.copy_(master)
 
 
+def embed_mark(tokens, rows, mark, step_dev):
+    t = tokens.reshape(-1).long()
+    t = t[(t >= 0) & (t < rows)]
+    mark[t] = int(step_dev.reshape(-1)[0].item())
+
+
+def embed_zero_rows(tokens, grad_table):
+    t = tokens.reshape(-1).long()
+    t = t[(t >= 0) & (t < grad_table.shape[0])]
+    grad_table[t] = 0
+
+
+def adamw_rows(master, exp_avg, exp_avg_sq, grad, param_bf16, sumsq, mark, marked, lr, beta1,
+               beta2, eps, weight_decay, grad_scale, step_dev):
+    sel = (mark == int(step_dev.reshape(-1)[0].item())) == bool(marked)
+    idx = sel.nonzero().reshape(-1)
+    if idx.numel() == 0:
+        return
+    g = grad[idx] if marked else torch.zeros_like(master[idx])
+    m_, a_, v_, p_ = master[idx], exp_avg[idx], exp_avg_sq[idx], param_bf16[idx]
+    adamw_shard(m_, a_, v_, g, p_, sumsq if marked else None, lr, beta1, beta2, eps,
+                weight_decay, grad_scale, step_dev)
+    master[idx], exp_avg[idx], exp_avg_sq[idx], param_bf16[idx] = m_, a_, v_, p_
+
+
 class GlooComm:
     """TEST-ONLY stand-in for runtime.comm.NcclComm over torch.distributed (gloo)."""
 

@@ -179,6 +179,42 @@ def test_adamw_matches_torch(cuda):
     assert abs(ss.item() - sum(((g * s) ** 2).sum().item() for s in (1, 2, 3))) / ss.item() < 1e-4
 
 
+def test_row_split_embedding_adamw_bit_exact(cuda):
+    """Row-split token-embedding update (executor.sparse_embed): unmarked rows with g = 0
+    early, marked rows after the backward == the dense AdamW over a gradient that is zero
+    outside the tokens' rows, bit for bit; the token rows of the gradient are cleared."""
+    torch.manual_seed(9)
+    V, d, n_tok = 5003, 768, 4096
+    tok = torch.randint(0, V, (2, n_tok // 2), device="cuda", dtype=torch.int32)
+    step = torch.tensor([3], device="cuda", dtype=torch.int32)
+    mark = torch.zeros(V, device="cuda", dtype=torch.int32)
+    mark[:7] = 2                                   # stale marks of an earlier step
+    st = {k: torch.randn(V, d, device="cuda") for k in ("p", "m")}
+    st["v"] = torch.rand(V, d, device="cuda")
+    grad = torch.randn(V, d, device="cuda")        # stale slot contents
+    dense = {k: t.clone() for k, t in st.items()}
+    K.embed_mark(tok, V, mark, step)
+    K.embed_zero_rows(tok, grad)
+    rows = torch.unique(tok.long())
+    assert torch.equal(mark == 3, torch.zeros(V, dtype=torch.bool, device="cuda").index_fill_(0, rows, True))
+    assert grad[rows].abs().max().item() == 0.0
+    upd = torch.randn(rows.numel(), d, device="cuda")
+    grad[rows] += upd                              # the embedding backward's scatter-add
+    gd = torch.zeros(V, d, device="cuda")
+    gd[rows] = grad[rows]
+    pb, pbd = torch.empty(V, d, device="cuda", dtype=torch.bfloat16), torch.empty(V, d, device="cuda", dtype=torch.bfloat16)
+    ss, ssd = torch.zeros(1, device="cuda"), torch.zeros(1, device="cuda")
+    hp = (1e-3, 0.9, 0.95, 1e-8, 0.1, 1.0)
+    K.adamw_rows(st["p"], st["m"], st["v"], None, pb, ss, mark, False, *hp, step)
+    K.adamw_rows(st["p"], st["m"], st["v"], grad, pb, ss, mark, True, *hp, step)
+    K.adamw_shard(dense["p"], dense["m"], dense["v"], gd, pbd, ssd, *hp, step)
+    torch.cuda.synchronize()
+    for k in st:
+        assert torch.equal(st[k], dense[k]), k
+    assert torch.equal(pb, pbd)
+    assert abs(ss.item() - ssd.item()) <= 1e-5 * ssd.item()
+
+
 @pytest.mark.parametrize("rows,d", [(300, 512), (64, 4096), (17, 5120)])
 def test_rmsnorm(cuda, rows, d):
     torch.manual_seed(6)
