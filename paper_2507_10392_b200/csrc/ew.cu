@@ -584,13 +584,117 @@ extern "C" int zb_embedding_bwd(const void* tok, const void* dout, void* dwte, v
   return launched("embedding_bwd");
 }
 
+// Shared-memory-resident variant (V <= 64K): one CTA per row copies the row into shared
+// memory with a single bulk TMA copy, so the logits are read from HBM once and no
+// online rescaling is needed: pass 1 row max (no exponentials), pass 2 sum of
+// exp2((x - max) log2e), pass 3 dlogits = exp2((x - lse) log2e) - onehot (scaled) — two
+// exponentials per logit instead of 2.125.  Two CTAs per SM at GPT-2's 50304 columns
+// (98 KB each), so one row's exponential passes overlap the other row's copy.
+constexpr int XS_THREADS = 512;
+constexpr int XS_MAX_V = 65536;
+__global__ void __launch_bounds__(XS_THREADS) xent_smem_kernel(
+    const __nv_bfloat16* logits, const int* __restrict__ labels, float* __restrict__ loss_sum,
+    __nv_bfloat16* dlogits, int V, int ld, float scale) {
+  pdl_enter();
+  constexpr float LOG2E = 1.4426950408889634f;
+  extern __shared__ uint4 row_s[];
+  __shared__ uint64_t bar;
+  __shared__ float red[XS_THREADS / 32];
+  __shared__ float bcast;
+  const int row = blockIdx.x;
+  const __nv_bfloat16* lr = logits + (size_t)row * ld;
+  __nv_bfloat16* gr = dlogits + (size_t)row * ld;
+  const int nv = V >> 3;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    mbar_arrive_expect_tx(&bar, (uint32_t)nv * 16);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(row_s)), "l"(lr), "r"((uint32_t)nv * 16), "r"(smem_u32(&bar))
+        : "memory");
+  }
+  const int label = labels[row];
+  if (label >= V) __trap();
+  const float label_logit = (threadIdx.x == 0 && label >= 0) ? __bfloat162float(lr[label]) : 0.f;
+  __syncthreads();  // barrier initialised before anyone waits on it
+  mbar_wait(&bar, 0);
+  auto block_reduce = [&](float x, bool is_max) {
+    x = is_max ? warp_max(x) : warp_sum(x);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float y = threadIdx.x < XS_THREADS / 32 ? red[threadIdx.x] : (is_max ? -INFINITY : 0.f);
+      y = is_max ? warp_max(y) : warp_sum(y);
+      if (threadIdx.x == 0) bcast = y;
+    }
+    __syncthreads();
+    return bcast;
+  };
+  float mx = -INFINITY;
+  for (int v = threadIdx.x; v < nv; v += XS_THREADS) {
+    const uint4 q = row_s[v];
+    const uint32_t* qi = &q.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = unpack_bf16(qi[e]);
+      mx = fmax3(mx, f.x, f.y);
+    }
+  }
+  const float M = block_reduce(mx, true);
+  const float2 l2 = make_float2(LOG2E, LOG2E), nm2 = make_float2(-M * LOG2E, -M * LOG2E);
+  float2 acc = make_float2(0.f, 0.f);
+  for (int v = threadIdx.x; v < nv; v += XS_THREADS) {
+    const uint4 q = row_s[v];
+    const uint32_t* qi = &q.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 t = ffma2(unpack_bf16(qi[e]), l2, nm2);
+      acc = fadd2(acc, make_float2(exp2_fast(t.x), exp2_fast(t.y)));
+    }
+  }
+  const float lse = M + __logf(block_reduce(acc.x + acc.y, false));
+  if (threadIdx.x == 0 && label >= 0) atomicAdd(loss_sum, lse - label_logit);
+  const float sc = label >= 0 ? scale : 0.f;
+  const float2 nl2 = make_float2(-lse * LOG2E, -lse * LOG2E);
+  for (int v = threadIdx.x; v < nv; v += XS_THREADS) {
+    const uint4 q = row_s[v];
+    const uint32_t* qi = &q.x;
+    uint4 o;
+    uint32_t* oi = &o.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 t = ffma2(unpack_bf16(qi[e]), l2, nl2);
+      const int c = v * 8 + 2 * e;
+      const float p0 = exp2_fast(t.x) - (c == label ? 1.f : 0.f);
+      const float p1 = exp2_fast(t.y) - (c + 1 == label ? 1.f : 0.f);
+      oi[e] = pack_bf16(p0 * sc, p1 * sc);
+    }
+    reinterpret_cast<uint4*>(gr)[v] = o;
+  }
+}
+
 extern "C" int zb_xent_fwd_bwd(const void* logits, const void* labels, void* loss_sum,
                                void* dlogits, int rows, int V, int ld, float scale,
                                cudaStream_t s) {
   if (V % 8 || ld % 8) return set_error(ZB_ERR_INVALID, "xent: V and ld must be multiples of 8");
   if (rows <= 0) return 0;
-  launch_pdl_k(xent_kernel, dim3(rows), dim3(XENT_THREADS), 0, s, (const __nv_bfloat16*)logits,
-               (const int*)labels, (float*)loss_sum, (__nv_bfloat16*)dlogits, V, ld, scale);
+  if (V <= XS_MAX_V && ((uintptr_t)logits & 15) == 0) {
+    const int smem = V * 2;
+    static int configured = 0;
+    if (smem > 48 * 1024 && configured < smem) {
+      cudaError_t e = cudaFuncSetAttribute(xent_smem_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, XS_MAX_V * 2);
+      if (e != cudaSuccess) return set_cuda_error(e, "xent: cudaFuncSetAttribute");
+      configured = XS_MAX_V * 2;
+    }
+    launch_pdl_k(xent_smem_kernel, dim3(rows), dim3(XS_THREADS), (size_t)smem, s,
+                 (const __nv_bfloat16*)logits, (const int*)labels, (float*)loss_sum,
+                 (__nv_bfloat16*)dlogits, V, ld, scale);
+  } else {  // V > 64K: streaming kernel (online max / sum)
+    launch_pdl_k(xent_kernel, dim3(rows), dim3(XENT_THREADS), 0, s, (const __nv_bfloat16*)logits,
+                 (const int*)labels, (float*)loss_sum, (__nv_bfloat16*)dlogits, V, ld, scale);
+  }
   return launched("xent");
 }
 
