@@ -582,9 +582,10 @@ class StageExecutor:
         for st in list(self.lane_streams.values()) + [self.gather_stream, self.prep_stream,
                                                       self.opt_stream]:
             st.wait_event(start)                     # fork (also joins a graph capture)
-        if self.sparse_embed:
+        if self.sparse_embed and not self.has_head:  # (with the head: see _on_fwd)
             with torch.cuda.stream(self.opt_stream):
                 self._embed_update(marked=False)
+
         done = self._done                            # task key -> [(stream, event)]
         last = {}
         noop = ("P2PRecv", "Recompute", "OptimStep", "FreeParams")
@@ -791,6 +792,12 @@ class StageExecutor:
                                  keep_preact=self.recompute == "none")
         self._layers(list(range(lo, hi)), body)
         if s == self.n_stages - 1:
+            if self.sparse_embed and self.multistream and m == 0:
+                # the untouched embedding rows' update (HBM-bound) overlaps the LM head's
+                # compute-bound GEMMs (opt_stream is joined at the end of the step)
+                self.opt_stream.wait_stream(torch.cuda.current_stream(self.device))
+                with torch.cuda.stream(self.opt_stream):
+                    self._embed_update(marked=False)
             hu = self.units["head"]
             self.model.head_fwd_bwd(hu.p, hu.g, self.act[(hi, m)][:n], self.labels[m],
                                     self.gbuf[(hi, m)][:n], self.logits, self.hf, self.hf_mean,
