@@ -1,4 +1,5 @@
-"""Stream-K vs data-parallel 1-CTA tiles on the step's N = 768 GEMM shapes (TF/s).
+"""Stream-K vs data-parallel 1-CTA tiles on the step's N = 768 GEMM shapes (TF/s).  The stream-K
+kernel path was removed after this measurement; splits=-1 now keeps the default.
   python scripts/gemm_sk_ab.py"""
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
