@@ -61,3 +61,23 @@ def test_layernorm_bwd_phase_validates_without_gpu():
     assert rc == 1001 and b"phase" in lib.zb_last_error()
     rc = lib.zb_layernorm_bwd_phase(a, a, a, a, a, a, a, a, None, None, None, 64, 770, 1, None)
     assert rc == 1001 and b"multiple of 8" in lib.zb_last_error()
+
+
+def test_row_split_embedding_update_validates_without_gpu():
+    lib = _lib.lib()
+    a = ctypes.c_void_p(1 << 20)
+    # marked rows need a gradient and the step counter (the stamp)
+    rc = lib.zb_adamw_rows_dstep(a, a, a, None, a, None, 8, 768, a, 1, 1e-3, 0.9, 0.95, 1e-8,
+                                 0.1, 1.0, a, None)
+    assert rc == 1001 and b"NULL" in lib.zb_last_error()
+    rc = lib.zb_adamw_rows_dstep(a, a, a, a, a, None, 8, 770, a, 1, 1e-3, 0.9, 0.95, 1e-8,
+                                 0.1, 1.0, a, None)
+    assert rc == 1001 and b"aligned" in lib.zb_last_error()
+    rc = lib.zb_embed_zero_rows(a, 16, 100, a, 770, None)
+    assert rc == 1001 and b"d % 4" in lib.zb_last_error()
+    rc = lib.zb_embed_mark(a, 16, 100, None, a, None)
+    assert rc == 1001 and b"NULL" in lib.zb_last_error()
+    # empty inputs are no-ops
+    assert lib.zb_adamw_rows_dstep(a, a, a, None, a, None, 0, 768, a, 0, 1e-3, 0.9, 0.95,
+                                   1e-8, 0.1, 1.0, a, None) == 0
+    assert lib.zb_embed_mark(a, 0, 100, a, a, None) == 0
