@@ -126,7 +126,8 @@ def _attn_ref(qkv, n_seq, S, H, D):
 
 @pytest.mark.parametrize("bwd", ["two-pass", "fused-dq"])
 @pytest.mark.parametrize("n_seq,S,H,D", [(2, 128, 4, 64), (1, 1024, 3, 64), (2, 256, 2, 128),
-                                         (1, 2048, 2, 128), (3, 512, 12, 64), (1, 384, 2, 128)])
+                                         (1, 2048, 2, 128), (3, 512, 12, 64), (1, 384, 2, 128),
+                                         (2, 768, 3, 64), (1, 2048, 5, 64)])
 def test_attention_fwd_bwd(cuda, n_seq, S, H, D, bwd):
     """tcgen05 attention vs torch fp32: forward kernels by S % 256 (query-tile pairs,
     else the 2-CTA/SM (D 64) or single-tile (D 128) kernel); backward fused (dQ
