@@ -475,6 +475,10 @@ class StageExecutor:
             self.dhf = torch.empty(n, d, **bf)
             self.dhf32 = torch.empty(n, d, device=device, dtype=torch.float32)
         self.tokens = torch.zeros(self.M, n, device=device, dtype=torch.int32)
+        # this rank's [share, S+1] row block of each microbatch, copied host->device in
+        # one piece (a contiguous slice of the pinned batch: an asynchronous copy)
+        self.batch_stage = torch.zeros(self.M, self.share, S + 1, device=device,
+                                       dtype=torch.int32)
         self.labels = torch.zeros(self.M, n, device=device, dtype=torch.int32)
         self.loss_sum = torch.zeros(1, device=device, dtype=torch.float32)
         self._head_fresh = False   # the head's gradient slot awaits its first accumulation
@@ -510,12 +514,18 @@ class StageExecutor:
         for m in range(self.M):
             lo, hi = self.my_samples(m)
             rows = batch[lo:hi]
+            stage = self.batch_stage[m, :hi - lo]
+            if rows.is_contiguous():
+                stage.copy_(rows, non_blocking=True)   # rows of the batch: contiguous
+                nbytes += rows.numel() * rows.element_size()
+            else:
+                stage.copy_(rows.contiguous(), non_blocking=True)
+                nbytes += rows.numel() * 4
+            n = (hi - lo) * S
             if self.has_embed:
-                self.tokens[m, :self.n_tok].copy_(rows[:, :S].reshape(-1), non_blocking=True)
-                nbytes += self.n_tok * 4
+                self.tokens[m, :n].view(hi - lo, S).copy_(stage[:, :S])
             if self.has_head:
-                self.labels[m, :self.n_tok].copy_(rows[:, 1:].reshape(-1), non_blocking=True)
-                nbytes += self.n_tok * 4
+                self.labels[m, :n].view(hi - lo, S).copy_(stage[:, 1:])
         return nbytes
 
     # ------------------------------------------------------------ memory report
