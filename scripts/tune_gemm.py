@@ -6,7 +6,9 @@ distinct call shapes, times the cost model's tile and its neighbours for each wi
 zb_gemm_tune (scratch outputs; inputs only read) and merges the winners into the
 table, tagged with the current kernel generation ("g1").
 
-  python scripts/tune_gemm.py [--gpus 1] [--append]     (bench workload, GPT-2 small)
+  python scripts/tune_gemm.py [--gpus 1] [--append] [--seqs N]   (bench workload, GPT-2 small)
+  --seqs: sequences on the tuning rank (default 8 = the N=1 bench); the N=2/4/8 layouts
+  put 11 and 5 sequences on their ranks, so their shapes are tuned with --seqs 11 / 5.
 """
 import argparse
 import os
@@ -31,9 +33,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--append", action="store_true", help="keep entries of other shapes")
     ap.add_argument("--out", default=TABLE, help="where to write the table")
+    ap.add_argument("--seqs", type=int, default=8, help="sequences on the tuning rank")
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    cfg, plan, ctx, gb = bench.build_workload(args.gpus)
+    cfg, plan, ctx, gb = bench.build_workload(args.gpus, per_gpu_batch=args.seqs)
     if args.gpus != 1:
         raise SystemExit("single-process tuning: the per-rank shapes of rank 0 of an N-rank "
                          "layout are those of its share; run with --gpus 1 per share size")
