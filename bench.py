@@ -48,12 +48,13 @@ def _peaks():
     return dict(FALLBACK_PEAKS), "fallback"
 
 
-def build_workload(n_gpus: int, per_gpu_batch: int = 8):
-    """GPT-2 small, one stage x an n_gpus-rank uneven ZeRO-3 DP group (product planner)."""
+def build_workload(n_gpus: int, per_gpu_batch: int = 8, cfg=None):
+    """GPT-2 small (or ``cfg``: tile tuning of other models' shapes), one stage x an
+    n_gpus-rank uneven ZeRO-3 DP group (product planner)."""
     from paper_2507_10392_b200 import plan as P
     from paper_2507_10392_b200.plan import emulated as E
 
-    cfg = E.GPT2_SMALL
+    cfg = cfg or E.GPT2_SMALL
     prof = E.profile_from_json(E.profile_json(E.dp_group_nodes(n_gpus)))
     rt = P.fit_runtime_model(prof)
     gb = per_gpu_batch * n_gpus

@@ -34,9 +34,18 @@ def main():
     ap.add_argument("--append", action="store_true", help="keep entries of other shapes")
     ap.add_argument("--out", default=TABLE, help="where to write the table")
     ap.add_argument("--seqs", type=int, default=8, help="sequences on the tuning rank")
+    ap.add_argument("--model", default="gpt2-small-124m",
+                    help="model whose per-rank GEMM shapes are tuned (plan/emulated.py MODELS)")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="layers instantiated for tuning (every layer has the same shapes)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    cfg, plan, ctx, gb = bench.build_workload(args.gpus, per_gpu_batch=args.seqs)
+    import dataclasses
+    from paper_2507_10392_b200.plan import emulated as E
+    mcfg = E.MODELS[args.model]
+    if args.layers:
+        mcfg = dataclasses.replace(mcfg, n_layer=args.layers)
+    cfg, plan, ctx, gb = bench.build_workload(args.gpus, per_gpu_batch=args.seqs, cfg=mcfg)
     if args.gpus != 1:
         raise SystemExit("single-process tuning: the per-rank shapes of rank 0 of an N-rank "
                          "layout are those of its share; run with --gpus 1 per share size")
