@@ -586,10 +586,12 @@ extern "C" int zb_embedding_bwd(const void* tok, const void* dout, void* dwte, v
 
 // Shared-memory-resident variant (V <= 64K): one CTA per row copies the row into shared
 // memory with a single bulk TMA copy, so the logits are read from HBM once and no
-// online rescaling is needed: pass 1 row max (no exponentials), pass 2 sum of
-// exp2((x - max) log2e), pass 3 dlogits = exp2((x - lse) log2e) - onehot (scaled) — two
-// exponentials per logit instead of 2.125.  Two CTAs per SM at GPT-2's 50304 columns
-// (98 KB each), so one row's exponential passes overlap the other row's copy.
+// online rescaling is needed: pass 1 row max (no exponentials), pass 2 e =
+// exp2((x - max) log2e), summed and written back over the row (bf16), pass 3 dlogits =
+// e / sum - onehot (scaled) — one exponential per logit instead of 2.125 (e rounded to
+// bf16 before the division: within the bf16 rounding of the stored dlogits).  Two CTAs
+// per SM at GPT-2's 50304 columns (98 KB each), so one row's passes overlap the other
+// row's copy.
 constexpr int XS_THREADS = 512;
 constexpr int XS_MAX_V = 65536;
 __global__ void __launch_bounds__(XS_THREADS) xent_smem_kernel(
@@ -644,19 +646,27 @@ __global__ void __launch_bounds__(XS_THREADS) xent_smem_kernel(
   const float M = block_reduce(mx, true);
   const float2 l2 = make_float2(LOG2E, LOG2E), nm2 = make_float2(-M * LOG2E, -M * LOG2E);
   float2 acc = make_float2(0.f, 0.f);
+  // pass 2: e = exp2((x - max) log2e) in (0, 1], summed, and kept in place of the row
+  // (bf16) so the last pass needs no second exponential: p = e / sum
   for (int v = threadIdx.x; v < nv; v += XS_THREADS) {
     const uint4 q = row_s[v];
     const uint32_t* qi = &q.x;
+    uint4 eo;
+    uint32_t* ei = &eo.x;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 t = ffma2(unpack_bf16(qi[e]), l2, nm2);
-      acc = fadd2(acc, make_float2(exp2_fast(t.x), exp2_fast(t.y)));
+      const float e0 = exp2_fast(t.x), e1 = exp2_fast(t.y);
+      acc = fadd2(acc, make_float2(e0, e1));
+      ei[e] = pack_bf16(e0, e1);
     }
+    row_s[v] = eo;
   }
-  const float lse = M + __logf(block_reduce(acc.x + acc.y, false));
+  const float sum = block_reduce(acc.x + acc.y, false);
+  const float lse = M + __logf(sum);
   if (threadIdx.x == 0 && label >= 0) atomicAdd(loss_sum, lse - label_logit);
   const float sc = label >= 0 ? scale : 0.f;
-  const float2 nl2 = make_float2(-lse * LOG2E, -lse * LOG2E);
+  const float2 inv2 = make_float2(sc / sum, sc / sum);
   for (int v = threadIdx.x; v < nv; v += XS_THREADS) {
     const uint4 q = row_s[v];
     const uint32_t* qi = &q.x;
@@ -664,11 +674,11 @@ __global__ void __launch_bounds__(XS_THREADS) xent_smem_kernel(
     uint32_t* oi = &o.x;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const float2 t = ffma2(unpack_bf16(qi[e]), l2, nl2);
+      float2 p = fmul2(unpack_bf16(qi[e]), inv2);
       const int c = v * 8 + 2 * e;
-      const float p0 = exp2_fast(t.x) - (c == label ? 1.f : 0.f);
-      const float p1 = exp2_fast(t.y) - (c + 1 == label ? 1.f : 0.f);
-      oi[e] = pack_bf16(p0 * sc, p1 * sc);
+      if (c == label) p.x -= sc;
+      if (c + 1 == label) p.y -= sc;
+      oi[e] = pack_bf16(p.x, p.y);
     }
     reinterpret_cast<uint4*>(gr)[v] = o;
   }
